@@ -1,0 +1,145 @@
+"""ctypes binding of the C ABI in include/nrx_b200.h (libnrx_b200.so).
+
+The shared library is built in-tree (``make`` / ``__graft_entry__.build()``)
+next to this file.  There is no fallback: if the library or a CUDA device is
+missing, the GPU entry points raise instead of silently computing on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+NRX_MAX_PILOT_SYMBOLS = 16
+NRX_MAX_IO = 4
+NRX_FP32, NRX_BF16 = 0, 1
+PRECISIONS = {"fp32": NRX_FP32, "bf16": NRX_BF16}
+VARIANT_IDS = {"single": 0, "masking": 1, "var_io": 2}
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnrx_b200.so")
+
+# every symbol include/nrx_b200.h declares
+EXPORTED = ("nrx_abi_version", "nrx_status_string", "nrx_validate", "nrx_weight_count",
+            "nrx_weight_name", "nrx_weight_numel", "nrx_packed_weight_bytes", "nrx_pack_weights",
+            "nrx_workspace_bytes", "nrx_forward", "nrx_buffer_geometry", "nrx_ls_features",
+            "nrx_forward_launch_count")
+
+
+class ModelDesc(ctypes.Structure):
+    _fields_ = [("d_s", ctypes.c_int32), ("hidden", ctypes.c_int32), ("num_iterations", ctypes.c_int32),
+                ("kernel_size", ctypes.c_int32), ("variant", ctypes.c_int32), ("m_max", ctypes.c_int32),
+                ("n_io", ctypes.c_int32), ("io_orders", ctypes.c_int32 * NRX_MAX_IO),
+                ("num_rx_ant", ctypes.c_int32), ("include_noise_plane", ctypes.c_int32),
+                ("include_freq_encoding", ctypes.c_int32)]
+
+
+class SlotDesc(ctypes.Structure):
+    _fields_ = [("num_subcarriers", ctypes.c_int32), ("num_symbols", ctypes.c_int32),
+                ("num_ues", ctypes.c_int32), ("comb_size", ctypes.c_int32),
+                ("num_pilot_symbols", ctypes.c_int32),
+                ("pilot_symbols", ctypes.c_int32 * NRX_MAX_PILOT_SYMBOLS)]
+
+
+class NrxLibraryError(RuntimeError):
+    pass
+
+
+_LIB = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libnrx_b200.so once; raise loudly if it was not built."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise NrxLibraryError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build())")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I, Z, V = ctypes.POINTER, ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p
+    lib.nrx_abi_version.restype = I
+    lib.nrx_status_string.restype = ctypes.c_char_p
+    lib.nrx_status_string.argtypes = [I]
+    lib.nrx_validate.argtypes = [P(ModelDesc), P(SlotDesc)]
+    lib.nrx_weight_count.argtypes = [P(ModelDesc)]
+    lib.nrx_weight_name.argtypes = [P(ModelDesc), I, ctypes.c_char_p, Z]
+    lib.nrx_weight_numel.argtypes = [P(ModelDesc), I]
+    lib.nrx_weight_numel.restype = ctypes.c_int64
+    lib.nrx_packed_weight_bytes.argtypes = [P(ModelDesc), I]
+    lib.nrx_packed_weight_bytes.restype = Z
+    lib.nrx_pack_weights.argtypes = [P(ModelDesc), I, P(ctypes.c_void_p), I, V]
+    lib.nrx_workspace_bytes.argtypes = [P(ModelDesc), P(SlotDesc), I, I]
+    lib.nrx_workspace_bytes.restype = Z
+    lib.nrx_forward.argtypes = [P(ModelDesc), P(SlotDesc), I, I, I, V, I, V, I, I, V, V, V, V, I, V, V, Z, V]
+    lib.nrx_forward_launch_count.argtypes = [P(ModelDesc), I, I]
+    lib.nrx_buffer_geometry.argtypes = [P(ModelDesc), P(SlotDesc), I, P(ctypes.c_int32)]
+    lib.nrx_ls_features.argtypes = [P(ModelDesc), P(SlotDesc), I, I, V, I, V, I, I, V, V, V]
+    if lib.nrx_abi_version() != 1:
+        raise NrxLibraryError("libnrx_b200.so ABI version mismatch")
+    _LIB = lib
+    return lib
+
+
+def status_text(code: int) -> str:
+    return load().nrx_status_string(int(code)).decode()
+
+
+def check(code: int, what: str) -> None:
+    if code != 0:
+        raise NrxLibraryError(f"{what} failed: {status_text(code)} (status {code})")
+
+
+def model_desc(config) -> ModelDesc:
+    """NrxConfig (reference or mirror) -> nrx_model_desc."""
+    m = ModelDesc()
+    m.d_s = config.d_s
+    m.hidden = config.hidden_width or config.d_s
+    m.num_iterations = config.num_iterations
+    m.kernel_size = config.kernel_size
+    m.variant = VARIANT_IDS[config.variant]
+    m.m_max = config.m_max
+    orders = tuple(config.io_modulations) if config.variant == "var_io" else (config.m_max,)
+    if len(orders) > NRX_MAX_IO:
+        raise NrxLibraryError(f"at most {NRX_MAX_IO} IO sets are supported, got {len(orders)}")
+    m.n_io = len(orders)
+    for i, o in enumerate(orders):
+        m.io_orders[i] = int(o)
+    m.num_rx_ant = config.num_rx_ant
+    m.include_noise_plane = int(bool(config.include_noise_plane))
+    m.include_freq_encoding = int(bool(config.include_freq_encoding))
+    return m
+
+
+def slot_desc(cfg) -> SlotDesc:
+    """SlotConfig (reference or mirror) -> nrx_slot_desc."""
+    s = SlotDesc()
+    s.num_subcarriers = cfg.num_subcarriers
+    s.num_symbols = cfg.num_symbols
+    s.num_ues = cfg.num_ues
+    s.comb_size = cfg.comb_size
+    ps = tuple(cfg.pilot_symbols)
+    if len(ps) > NRX_MAX_PILOT_SYMBOLS:
+        raise NrxLibraryError(f"at most {NRX_MAX_PILOT_SYMBOLS} pilot symbols are supported")
+    s.num_pilot_symbols = len(ps)
+    for i, p in enumerate(ps):
+        s.pilot_symbols[i] = int(p)
+    return s
+
+
+def weight_names(config) -> list:
+    lib = load()
+    m = model_desc(config)
+    n = lib.nrx_weight_count(ctypes.byref(m))
+    buf = ctypes.create_string_buffer(256)
+    out = []
+    for i in range(n):
+        lib.nrx_weight_name(ctypes.byref(m), i, buf, 256)
+        out.append(buf.value.decode())
+    return out
+
+
+def buffer_geometry(config, cfg, precision: str) -> dict:
+    lib = load()
+    out = (ctypes.c_int32 * 8)()
+    check(lib.nrx_buffer_geometry(ctypes.byref(model_desc(config)), ctypes.byref(slot_desc(cfg)),
+                                  PRECISIONS[precision], out), "nrx_buffer_geometry")
+    return dict(zip(("rows_slab", "Tp", "Cf", "Cs", "Ch", "Ca", "cw", "tiles"), list(out)))

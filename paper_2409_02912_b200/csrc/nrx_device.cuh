@@ -1,0 +1,73 @@
+// Device helpers shared by all kernels.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "nrx_internal.h"
+
+namespace nrx {
+
+// Distance from subcarrier s to the nearest comb subcarrier of UE u
+// (positional_encoding, nrx.py:165-167).
+__device__ __forceinline__ int comb_dist(int s, int u, const Geom& g) {
+  const int o = u % g.comb;
+  if (s <= o) return o - s;
+  const int lo = o + ((s - o) / g.comb) * g.comb;
+  int d = s - lo;
+  const int hi = lo + g.comb;
+  if (hi < g.S && hi - s < d) d = hi - s;
+  return d;
+}
+
+// float32(dist / S) exactly as numpy: int/int true-divide in float64, cast.
+__device__ __forceinline__ float pos_df(int s, int u, const Geom& g) {
+  if (!g.freq_enc) return 0.f;
+  return __double2float_rn(__ddiv_rn((double)comb_dist(s, u, g), (double)g.S));
+}
+
+// Value a producer writes into state channel c >= d (pos encoding / zero).
+__device__ __forceinline__ float state_extra(int c, int s, int t, int u, const Geom& g) {
+  if (c == g.d) return g.dt[t];
+  if (c == g.d + 1) return pos_df(s, u, g);
+  return 0.f;
+}
+
+// Address of the 16-byte chunk (slab, chunk, row) of a chunk-planar buffer.
+template <typename T>
+__device__ __forceinline__ T* chunk_ptr(T* base, int slab, int nchunks, int chunk, int row, const Geom& g) {
+  constexpr int cw = 16 / sizeof(T);
+  return base + (((size_t)slab * nchunks + chunk) * g.rows_slab + row) * cw;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ float2 unpack_bf16x2(uint32_t v) {
+  __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&v);
+  return __bfloat1622float2(b);
+}
+
+// Write 4 (fp32) or 8 (bf16) channel values as one 16-byte chunk.
+__device__ __forceinline__ void store_chunk(float* p, const float* v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void store_chunk(__nv_bfloat16* p, const float* v) {
+  uint4 q;
+  q.x = pack_bf16x2(v[0], v[1]);
+  q.y = pack_bf16x2(v[2], v[3]);
+  q.z = pack_bf16x2(v[4], v[5]);
+  q.w = pack_bf16x2(v[6], v[7]);
+  *reinterpret_cast<uint4*>(p) = q;
+}
+
+__device__ __forceinline__ int io_index(const int32_t* mod_order, int slab, const Geom& g) {
+  if (g.n_io == 1 || mod_order == nullptr) return 0;
+  const int m = mod_order[slab];
+  for (int i = 0; i < g.n_io; ++i)
+    if (g.io_orders[i] == m) return i;
+  return -1;
+}
+
+}  // namespace nrx

@@ -1,0 +1,345 @@
+// Host-side pieces of the C ABI that need no GPU: descriptor validation,
+// geometry, canonical weight naming (expected_shapes, nrx.py:92-120), the
+// packed-weight layout + repacker, and the workspace layout.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "nrx_internal.h"
+
+namespace nrx {
+
+namespace {
+
+struct TensorSpec {
+  std::string name;
+  std::vector<int> shape;
+};
+
+int input_channels(const nrx_model_desc* m) {
+  return 4 * m->num_rx_ant + 2 + (m->include_noise_plane ? 1 : 0);
+}
+
+int llr_width_of(const nrx_model_desc* m, int io) {
+  return m->variant == NRX_VAR_IO ? m->io_orders[io] : m->m_max;
+}
+
+// Canonical tensor list, documented in include/nrx_b200.h.
+std::vector<TensorSpec> canonical(const nrx_model_desc* m) {
+  std::vector<TensorSpec> v;
+  const int k = m->kernel_size, d = m->d_s, h = m->hidden, cin = input_channels(m);
+  auto conv_block = [&](const std::string& p, int c0) {
+    v.push_back({p + ".conv0.w", {k, k, c0, d}});
+    v.push_back({p + ".conv0.b", {d}});
+    v.push_back({p + ".conv1.w", {k, k, d, d}});
+    v.push_back({p + ".conv1.b", {d}});
+  };
+  auto mlp = [&](const std::string& p, int out) {
+    v.push_back({p + ".fc0.w", {d, h}});
+    v.push_back({p + ".fc0.b", {h}});
+    v.push_back({p + ".fc1.w", {h, out}});
+    v.push_back({p + ".fc1.b", {out}});
+  };
+  for (int i = 0; i < m->n_io; ++i) {
+    std::string tag = m->variant == NRX_VAR_IO ? ".m" + std::to_string(m->io_orders[i]) : "";
+    conv_block("state_init" + tag, cin);
+    mlp("readout_llr" + tag, llr_width_of(m, i));
+  }
+  mlp("iteration.msg", d);
+  conv_block("iteration.update", 2 * d + 2);
+  mlp("readout_chest", 2 * m->num_rx_ant);
+  return v;
+}
+
+int64_t numel(const TensorSpec& t) {
+  int64_t n = 1;
+  for (int s : t.shape) n *= s;
+  return n;
+}
+
+}  // namespace
+
+int validate(const nrx_model_desc* m, const nrx_slot_desc* s) {
+  if (!m) return NRX_ERR_INVALID;
+  if (m->d_s < 4 || m->num_iterations < 1 || m->kernel_size < 1 || m->kernel_size % 2 == 0)
+    return NRX_ERR_INVALID;
+  if (m->variant < 0 || m->variant > 2 || m->n_io < 1 || m->n_io > NRX_MAX_IO) return NRX_ERR_INVALID;
+  if (m->variant != NRX_VAR_IO && m->n_io != 1) return NRX_ERR_INVALID;
+  if (m->hidden < 1 || m->num_rx_ant < 1 || m->m_max < 1) return NRX_ERR_INVALID;
+  for (int i = 0; i < m->n_io; ++i)
+    if (m->io_orders[i] < 1 || m->io_orders[i] > m->m_max) return NRX_ERR_INVALID;
+  // implementation limits
+  if (m->d_s > 64 || m->hidden > 256 || m->num_rx_ant > 8 || m->m_max > 8) return NRX_ERR_UNSUPPORTED;
+  if (m->kernel_size > 5) return NRX_ERR_UNSUPPORTED;
+  if (!s) return NRX_OK;
+  if (s->num_subcarriers < 1 || s->num_symbols < 1 || s->num_ues < 1 || s->comb_size < 1) return NRX_ERR_INVALID;
+  if (s->num_ues > s->comb_size) return NRX_ERR_INVALID;
+  if (s->num_pilot_symbols < 1 || s->num_pilot_symbols > NRX_MAX_PILOT_SYMBOLS) return NRX_ERR_INVALID;
+  for (int i = 0; i < s->num_pilot_symbols; ++i)
+    if (s->pilot_symbols[i] < 0 || s->pilot_symbols[i] >= s->num_symbols) return NRX_ERR_INVALID;
+  if (s->num_subcarriers < s->comb_size) return NRX_ERR_UNSUPPORTED;  // every UE needs a pilot
+  if (s->num_symbols > 32 || s->num_ues > 8) return NRX_ERR_UNSUPPORTED;
+  return NRX_OK;
+}
+
+int quantum(int prec) { return prec == NRX_BF16 ? 16 : 4; }
+
+int make_geom(const nrx_model_desc* m, const nrx_slot_desc* s, int n_slots, int prec, Geom* g) {
+  int st = validate(m, s);
+  if (st) return st;
+  if (n_slots < 1) return NRX_ERR_INVALID;
+  if (prec != NRX_FP32 && prec != NRX_BF16) return NRX_ERR_INVALID;
+  std::memset(g, 0, sizeof(*g));
+  g->N = n_slots;
+  g->U = s->num_ues;
+  g->NU = n_slots * s->num_ues;
+  g->S = s->num_subcarriers;
+  g->T = s->num_symbols;
+  g->B = m->num_rx_ant;
+  g->comb = s->comb_size;
+  g->K = s->num_pilot_symbols;
+  for (int i = 0; i < g->K; ++i) g->ps[i] = s->pilot_symbols[i];
+  g->ks = m->kernel_size;
+  g->r = m->kernel_size / 2;
+  g->Tp = g->T + g->r;
+  g->H = g->r * g->Tp + g->r;
+  g->rows_data = g->S * g->Tp;
+  g->rows_slab = rup(g->rows_data, NRX_TILE_M);
+  g->tiles = g->rows_slab / NRX_TILE_M;
+  g->d = m->d_s;
+  g->h = m->hidden;
+  g->prec = prec;
+  g->cw = prec == NRX_BF16 ? 8 : 4;
+  const int q = quantum(prec);
+  g->Cin = input_channels(m);
+  g->Cf = rup(g->Cin, q);
+  g->Cs = rup(g->d + 2, q);
+  g->Ch = rup(g->d, q);
+  g->Ca = rup(g->d, q);
+  g->n_io = m->n_io;
+  int w = 0;
+  for (int i = 0; i < m->n_io; ++i) {
+    g->io_orders[i] = m->io_orders[i];
+    g->io_width[i] = llr_width_of(m, i);
+    if (g->io_width[i] > w) w = g->io_width[i];
+  }
+  g->llr_width = w;
+  g->noise_plane = m->include_noise_plane;
+  g->freq_enc = m->include_freq_encoding;
+  // positional encoding along t (nrx.py:164): float32(min|t - ps| / T)
+  for (int t = 0; t < g->T; ++t) {
+    int best = 1 << 30, arg = 0;
+    for (int k = 0; k < g->K; ++k) {
+      int dd = std::abs(t - g->ps[k]);
+      if (dd < best) { best = dd; arg = k; }  // strict: ties keep the earlier symbol
+    }
+    g->dt[t] = (float)((double)best / (double)g->T);
+    g->nearest[t] = arg;
+  }
+  return NRX_OK;
+}
+
+int dmax_of(int d) { return d <= 16 ? 16 : d <= 32 ? 32 : 64; }
+
+// ---- packed weight layout ------------------------------------------------
+//
+// FP32 (SIMT kernels):
+//   conv  w: [tap][ktap][nw] float, ktap = buffer input channels, nw = output
+//         buffer channels rounded to 8; b: [nw]
+//   mlp   w0: [dmax][h], b0: [h], w1: [h][outp], b1: [outp]
+//         (outp = dmax for msg, 8 for the LLR readout, 16 for the chest)
+// BF16 (tcgen05 kernels) additionally stores bf16 B operands, see k_tc.cu.
+void pack_layout(const nrx_model_desc* m, int prec, PackLayout* L) {
+  Geom g;
+  nrx_slot_desc s{};
+  s.num_subcarriers = 64; s.num_symbols = 14; s.num_ues = 1; s.comb_size = 1;
+  s.num_pilot_symbols = 1; s.pilot_symbols[0] = 0;
+  make_geom(m, &s, 1, prec, &g);
+  std::memset(L, 0, sizeof(*L));
+  const int taps = m->kernel_size * m->kernel_size;
+  const int dmax = dmax_of(m->d_s);
+  L->dmax = dmax;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+  auto conv = [&](ConvOff& c, int ktap, int cdst) {
+    int nw = rup(cdst, 8);
+    c.ktap = ktap;
+    c.w = take((size_t)taps * ktap * nw * 4);
+    c.b = take((size_t)nw * 4);
+  };
+  auto mlp = [&](MlpOff& o, int outp) {
+    o.out = outp;
+    o.w0 = take((size_t)dmax * m->hidden * 4);
+    o.b0 = take((size_t)m->hidden * 4);
+    o.w1 = take((size_t)m->hidden * outp * 4);
+    o.b1 = take((size_t)outp * 4);
+  };
+  for (int i = 0; i < m->n_io; ++i) {
+    conv(L->init0[i], g.Cf, g.Ch);
+    conv(L->init1[i], g.Ch, g.Cs);
+    mlp(L->llr[i], 8);
+  }
+  mlp(L->msg, dmax);
+  conv(L->upd0, g.Cs + g.Ca, g.Ch);
+  conv(L->upd1, g.Ch, g.Cs);
+  mlp(L->chest, 16);
+  L->total = off;
+}
+
+namespace {
+
+// Map a buffer input channel j of a conv to the reference Cin index (-1: zero).
+using ChanMap = int (*)(int j, const Geom& g);
+int map_identity_feats(int j, const Geom& g) { return j < g.Cin ? j : -1; }
+int map_identity_hidden(int j, const Geom& g) { return j < g.d ? j : -1; }
+// update conv0 input = [state (d) | pos (2) | pad][agg (d) | pad]; the
+// reference concat order is [state, agg, pos] (nrx.py:262).
+int map_update(int j, const Geom& g) {
+  if (j < g.d) return j;
+  if (j == g.d) return 2 * g.d;
+  if (j == g.d + 1) return 2 * g.d + 1;
+  if (j < g.Cs) return -1;
+  int a = j - g.Cs;
+  return a < g.d ? g.d + a : -1;
+}
+
+void pack_conv_f32(const Geom& g, int k, const ConvOff& c, int cdst, int cin_ref, const float* w,
+                   const float* b, ChanMap map, uint8_t* base) {
+  const int nw = rup(cdst, 8), taps = k * k, cout = g.d;
+  float* dw = (float*)(base + c.w);
+  float* db = (float*)(base + c.b);
+  for (int tap = 0; tap < taps; ++tap)
+    for (int j = 0; j < c.ktap; ++j) {
+      int src = map(j, g);
+      for (int o = 0; o < nw; ++o)
+        dw[((size_t)tap * c.ktap + j) * nw + o] =
+            (src >= 0 && o < cout) ? w[((size_t)tap * cin_ref + src) * cout + o] : 0.f;
+    }
+  for (int o = 0; o < nw; ++o) db[o] = o < cout ? b[o] : 0.f;
+}
+
+void pack_mlp_f32(int din, int dmax, int h, int out, const MlpOff& o, const float* w0, const float* b0,
+                  const float* w1, const float* b1, uint8_t* base) {
+  float* p0 = (float*)(base + o.w0);
+  for (int i = 0; i < dmax; ++i)
+    for (int j = 0; j < h; ++j) p0[(size_t)i * h + j] = i < din ? w0[(size_t)i * h + j] : 0.f;
+  std::memcpy(base + o.b0, b0, (size_t)h * 4);
+  float* p1 = (float*)(base + o.w1);
+  float* q1 = (float*)(base + o.b1);
+  for (int j = 0; j < h; ++j)
+    for (int c = 0; c < o.out; ++c) p1[(size_t)j * o.out + c] = c < out ? w1[(size_t)j * out + c] : 0.f;
+  for (int c = 0; c < o.out; ++c) q1[c] = c < out ? b1[c] : 0.f;
+}
+
+}  // namespace
+
+int pack_weights_f32(const nrx_model_desc* m, const float* const* t, uint8_t* base) {
+  PackLayout L;
+  pack_layout(m, NRX_FP32, &L);
+  std::memset(base, 0, L.total);
+  Geom g;
+  nrx_slot_desc s{};
+  s.num_subcarriers = 64; s.num_symbols = 14; s.num_ues = 1; s.comb_size = 1;
+  s.num_pilot_symbols = 1;
+  make_geom(m, &s, 1, NRX_FP32, &g);
+  const int k = m->kernel_size, d = m->d_s, h = m->hidden;
+  int i = 0;
+  for (int io = 0; io < m->n_io; ++io) {
+    pack_conv_f32(g, k, L.init0[io], g.Ch, g.Cin, t[i], t[i + 1], map_identity_feats, base);
+    pack_conv_f32(g, k, L.init1[io], g.Cs, d, t[i + 2], t[i + 3], map_identity_hidden, base);
+    pack_mlp_f32(d, L.dmax, h, llr_width_of(m, io), L.llr[io], t[i + 4], t[i + 5], t[i + 6], t[i + 7], base);
+    i += 8;
+  }
+  pack_mlp_f32(d, L.dmax, h, d, L.msg, t[i], t[i + 1], t[i + 2], t[i + 3], base);
+  i += 4;
+  pack_conv_f32(g, k, L.upd0, g.Ch, 2 * d + 2, t[i], t[i + 1], map_update, base);
+  pack_conv_f32(g, k, L.upd1, g.Cs, d, t[i + 2], t[i + 3], map_identity_hidden, base);
+  i += 4;
+  pack_mlp_f32(d, L.dmax, h, 2 * m->num_rx_ant, L.chest, t[i], t[i + 1], t[i + 2], t[i + 3], base);
+  return NRX_OK;
+}
+
+void ws_layout(const Geom& g, WsLayout* w) {
+  const size_t esz = g.prec == NRX_BF16 ? 2 : 4;
+  const size_t plane = (size_t)g.NU * g.rows_slab * esz;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+  w->feats = take(plane * g.Cf);
+  w->h = take(plane * g.Ch);
+  w->state = take(plane * g.Cs);
+  w->agg = take(plane * g.Ca);
+  w->state32 = g.prec == NRX_BF16 ? take((size_t)g.NU * g.rows_slab * 4 * rup(g.d, 4)) : 0;
+  w->total = off;
+}
+
+}  // namespace nrx
+
+using namespace nrx;
+
+extern "C" {
+
+int nrx_abi_version(void) { return NRX_ABI_VERSION; }
+
+const char* nrx_status_string(int s) {
+  switch (s) {
+    case NRX_OK: return "ok";
+    case NRX_ERR_INVALID: return "invalid descriptor or argument";
+    case NRX_ERR_UNSUPPORTED: return "configuration outside the limits of this implementation";
+    case NRX_ERR_WORKSPACE: return "workspace too small";
+    case NRX_ERR_CUDA: return "CUDA launch or driver error";
+    case NRX_ERR_DEPTH: return "inference depth outside [1, N_it]";
+    case NRX_ERR_NO_DEVICE: return "no sm_100 device or kernel image";
+    default: return "unknown status";
+  }
+}
+
+int nrx_validate(const nrx_model_desc* m, const nrx_slot_desc* s) { return validate(m, s); }
+
+int nrx_weight_count(const nrx_model_desc* m) {
+  if (validate(m, nullptr) == NRX_ERR_INVALID) return -1;
+  return (int)canonical(m).size();
+}
+
+int nrx_weight_name(const nrx_model_desc* m, int i, char* buf, size_t len) {
+  if (validate(m, nullptr) == NRX_ERR_INVALID) return -1;
+  auto v = canonical(m);
+  if (i < 0 || i >= (int)v.size() || !buf || len == 0) return -1;
+  std::snprintf(buf, len, "%s", v[i].name.c_str());
+  return (int)v[i].name.size();
+}
+
+int64_t nrx_weight_numel(const nrx_model_desc* m, int i) {
+  if (validate(m, nullptr) == NRX_ERR_INVALID) return -1;
+  auto v = canonical(m);
+  if (i < 0 || i >= (int)v.size()) return -1;
+  return numel(v[i]);
+}
+
+size_t nrx_packed_weight_bytes(const nrx_model_desc* m, int prec) {
+  if (validate(m, nullptr) != NRX_OK) return 0;
+  PackLayout L;
+  pack_layout(m, prec, &L);
+  return L.total;
+}
+
+int nrx_pack_weights(const nrx_model_desc* m, int prec, const float* const* tensors, int n, void* out) {
+  int st = validate(m, nullptr);
+  if (st) return st;
+  if (!tensors || !out || n != (int)canonical(m).size()) return NRX_ERR_INVALID;
+  for (int i = 0; i < n; ++i)
+    if (!tensors[i]) return NRX_ERR_INVALID;
+  if (prec == NRX_FP32) return pack_weights_f32(m, tensors, (uint8_t*)out);
+  return NRX_ERR_UNSUPPORTED;
+}
+
+size_t nrx_workspace_bytes(const nrx_model_desc* m, const nrx_slot_desc* s, int n_slots, int prec) {
+  Geom g;
+  if (make_geom(m, s, n_slots, prec, &g)) return 0;
+  WsLayout w;
+  ws_layout(g, &w);
+  return w.total;
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+// Internal geometry / layout definitions shared by the host orchestrator,
+// the weight packer and the kernels.
+//
+// HBM layout of every activation tensor ("chunk-planar", slab-major):
+//   buf[slab][chunk][row][CW]      CW = 16 bytes / sizeof(element)
+// slab = n*U + u (the reference's N*U flattening, nrx.py:321), chunk =
+// channel / CW, row = s*Tp + t over the (S, T) grid with the symbol axis
+// padded from T to Tp = T + r (r = kernel_size/2).  With that padding the
+// k x k 'same' convolution over (s, t) (autodiff.py:324-350) becomes a 1-D
+// convolution over `row` with tap offsets (a-r)*Tp + (b-r): the zero rows
+// t in [T, Tp) supply the reference's zero padding along T and rows outside
+// [0, rows_slab) (zero-filled by TMA / bounds checks) the padding along S.
+// rows_slab = S*Tp rounded up to the 128-row tile; rows with s >= S or
+// t >= T are kept at zero by every producer.  A 16-byte chunk of one row
+// is the unit every kernel moves, so a warp touching 32 consecutive rows of
+// one chunk issues fully coalesced 512-byte transactions, and a TMA box
+// {CW, rows, chunks} lands as the K-major no-swizzle core-matrix layout
+// tcgen05.mma reads directly.
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/nrx_b200.h"
+
+#define NRX_TILE_M 128
+
+namespace nrx {
+
+inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+inline int rup(int a, int b) { return cdiv(a, b) * b; }
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Geometry + channel bookkeeping, passed by value to kernels.
+struct Geom {
+  int N, U, NU, S, T, B, comb, K;
+  int ps[NRX_MAX_PILOT_SYMBOLS];
+  int ks, r, Tp, H;           // kernel size, radius, padded symbols, halo rows
+  int rows_data, rows_slab, tiles;
+  int d, h;                   // state depth, MLP hidden width
+  int cw;                     // elements per 16-byte chunk
+  int Cin, Cf, Cs, Ch, Ca;    // logical input channels, buffer channel counts
+  int nb;                     // conv output width covered by the SIMT kernel
+  int n_io;
+  int io_orders[NRX_MAX_IO];
+  int io_width[NRX_MAX_IO];   // LLR width produced by io set i
+  int llr_width;              // output row stride of llr_out
+  int noise_plane, freq_enc;
+  int prec;
+  float dt[32];               // positional encoding, symbol axis (float32, nrx.py:164)
+  int nearest[32];            // nearest pilot-symbol index per t (classical.py:71)
+};
+
+// Byte offsets of each weight sub-buffer inside the packed blob.
+struct ConvOff { size_t w, b; int ktap; };
+struct MlpOff { size_t w0, b0, w1, b1; int out; };
+struct PackLayout {
+  ConvOff init0[NRX_MAX_IO], init1[NRX_MAX_IO];
+  MlpOff llr[NRX_MAX_IO];
+  MlpOff msg;
+  ConvOff upd0, upd1;
+  MlpOff chest;
+  size_t total;
+  int dmax;                   // padded state depth for the SIMT MLP kernels
+};
+
+struct WsLayout {
+  size_t feats, h, state, agg, state32, total;
+};
+
+}  // namespace nrx

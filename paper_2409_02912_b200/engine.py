@@ -1,0 +1,196 @@
+"""NrxEngine: one receiver model resident on one B200.
+
+Owns the packed device weights, per-thread CUDA streams, workspaces and
+pinned staging buffers, and calls the C-ABI entry point ``nrx_forward``
+(include/nrx_b200.h).  Two ways in:
+
+* ``forward_device``  device-resident tensors in and out (the paper's
+  "inline acceleration" latency setting), no host copies;
+* ``run``             numpy in, numpy out, with the semantics of the
+  reference ``nrxsim.nrx.nrx_forward`` (nrx.py:345-385); host<->device
+  copies are part of the call.
+
+PyTorch is used for device memory, pinned memory and streams only; all
+arithmetic happens in the CUDA kernels of libnrx_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _lib
+from .config import weight_array
+
+
+def _require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise _lib.NrxLibraryError("no CUDA device: the NRX B200 path has no CPU fallback")
+    return torch
+
+
+def pack_weights(config, weights, precision: str = "fp32") -> np.ndarray:
+    """Host-side repack of a weight dict (reference ``ad.Tensor`` values or
+    arrays) into the kernels' layout via ``nrx_pack_weights`` (no GPU)."""
+    lib = _lib.load()
+    m = _lib.model_desc(config)
+    prec = _lib.PRECISIONS[precision]
+    _lib.check(lib.nrx_validate(ctypes.byref(m), None), "nrx_validate")
+    names = _lib.weight_names(config)
+    if set(names) != set(weights):
+        raise ValueError(f"weights do not match the configuration: {sorted(set(names) ^ set(weights))}")
+    arrays = []
+    for i, name in enumerate(names):
+        a = np.ascontiguousarray(weight_array(weights[name]), dtype=np.float32)
+        if a.size != lib.nrx_weight_numel(ctypes.byref(m), i):
+            raise ValueError(f"tensor '{name}' has {a.size} elements, expected {lib.nrx_weight_numel(ctypes.byref(m), i)}")
+        arrays.append(a)
+    ptrs = (ctypes.c_void_p * len(arrays))(*[a.ctypes.data for a in arrays])
+    nbytes = lib.nrx_packed_weight_bytes(ctypes.byref(m), prec)
+    if nbytes == 0:
+        raise _lib.NrxLibraryError("nrx_packed_weight_bytes returned 0 (unsupported model)")
+    out = np.zeros(nbytes, dtype=np.uint8)
+    _lib.check(lib.nrx_pack_weights(ctypes.byref(m), prec, ptrs, len(arrays), out.ctypes.data),
+               "nrx_pack_weights")
+    return out
+
+
+def pilot_comb_values(book_values: np.ndarray, cfg) -> np.ndarray:
+    """(..., U, S, T) PilotBook values -> (..., U, F, K) values at each UE's
+    comb subcarriers (u % comb + f*comb) and pilot symbols (slot.py:92-93,
+    classical.py:43-44).  Entries past a UE's last comb subcarrier repeat a
+    valid RE and are ignored by the kernel."""
+    S, comb, U = cfg.num_subcarriers, cfg.comb_size, cfg.num_ues
+    F = -(-S // comb)
+    ps = np.asarray(cfg.pilot_symbols)
+    u_idx = np.arange(U)[:, None]
+    s_idx = np.minimum(u_idx % comb + np.arange(F)[None, :] * comb, S - 1)       # (U, F)
+    return np.ascontiguousarray(book_values[..., u_idx[:, :, None], s_idx[:, :, None], ps[None, None, :]])
+
+
+class NrxEngine:
+    """Packed weights of one model on one device; thread-safe ``run``."""
+
+    def __init__(self, config, weights, precision: str = "fp32", device=None):
+        torch = _require_cuda()
+        self.lib = _lib.load()
+        self.config = config
+        self.precision = precision
+        self.prec_id = _lib.PRECISIONS[precision]
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._m = _lib.model_desc(config)
+        packed = pack_weights(config, weights, precision)
+        self.weights_dev = torch.from_numpy(packed).to(self.device)
+        self._tls = threading.local()
+
+    # -- per-thread resources --------------------------------------------------
+
+    def _local(self):
+        tls = self._tls
+        if not hasattr(tls, "stream"):
+            torch = _require_cuda()
+            tls.stream = torch.cuda.Stream(device=self.device)
+            tls.ws = {}
+            tls.bufs = {}
+        return tls
+
+    def workspace(self, cfg, n_slots: int):
+        torch = _require_cuda()
+        s = _lib.slot_desc(cfg)
+        nbytes = self.lib.nrx_workspace_bytes(ctypes.byref(self._m), ctypes.byref(s), n_slots, self.prec_id)
+        if nbytes == 0:
+            code = self.lib.nrx_validate(ctypes.byref(self._m), ctypes.byref(s))
+            _lib.check(code or 1, "nrx_workspace_bytes")
+        tls = self._local()
+        ws = tls.ws.get("ws")
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            tls.ws["ws"] = ws
+        return ws
+
+    def launch_count(self, num_iterations: int) -> int:
+        return self.lib.nrx_forward_launch_count(ctypes.byref(self._m), self.prec_id, int(num_iterations))
+
+    # -- device-resident entry ---------------------------------------------------
+
+    def forward_device(self, cfg, y, pilots, noise_feat, mod_order, num_iterations, llr, chest,
+                       workspace=None, stream=None):
+        """Enqueue one batched forward on device tensors.
+
+        y (N,S,T,B) complex64/complex128; pilots (P,U,F,K) complex with P in
+        {1, N}; noise_feat (N,) float32; mod_order (N*U,) int32; llr
+        (N,U,S,T,W) float32 and chest (N,U,S,T,B) complex64 are written.
+        """
+        torch = _require_cuda()
+        n = y.shape[0]
+        s = _lib.slot_desc(cfg)
+        ws = workspace if workspace is not None else self.workspace(cfg, n)
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        for t in (y, pilots, noise_feat, mod_order, llr, chest):
+            if not t.is_contiguous() or t.device != self.device:
+                raise ValueError("forward_device expects contiguous tensors on the engine's device")
+        code = self.lib.nrx_forward(
+            ctypes.byref(self._m), ctypes.byref(s), n, self.prec_id, int(num_iterations),
+            y.data_ptr(), int(y.dtype == torch.complex128),
+            pilots.data_ptr(), int(pilots.dtype == torch.complex128), pilots.shape[0],
+            noise_feat.data_ptr(), mod_order.data_ptr(), self.weights_dev.data_ptr(),
+            llr.data_ptr(), llr.shape[-1], chest.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)
+        if code == 5:
+            raise ValueError(f"inference depth {num_iterations} outside [1, {self.config.num_iterations}]")
+        _lib.check(code, "nrx_forward")
+
+    # -- numpy entry with the reference's semantics ------------------------------
+
+    def _staging(self, key, shape, dtype, pinned):
+        torch = _require_cuda()
+        tls = self._local()
+        k = (key, tuple(shape), dtype, pinned)
+        buf = tls.bufs.get(k)
+        if buf is None:
+            if pinned:
+                buf = torch.empty(shape, dtype=dtype, pin_memory=True)
+            else:
+                buf = torch.empty(shape, dtype=dtype, device=self.device)
+            tls.bufs[k] = buf
+        return buf
+
+    def run_arrays(self, cfg, y: np.ndarray, pilot_vals: np.ndarray, noise_feat: np.ndarray,
+                   mod_order: np.ndarray, num_iterations: int, llr_width: int, exact_inputs: bool = False):
+        """numpy -> device -> numpy; returns (llr (N,U,S,T,W) f32, chest (N,U,S,T,B) c64).
+
+        y (N,S,T,B) and pilot_vals (P,U,F,K) are shipped as complex64 unless
+        ``exact_inputs`` (then complex128, so the float64 LS sees the same
+        inputs as the reference)."""
+        torch = _require_cuda()
+        cdt_np = np.complex128 if exact_inputs else np.complex64
+        cdt = torch.complex128 if exact_inputs else torch.complex64
+        n = y.shape[0]
+        U, S, T, B = cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, self.config.num_rx_ant
+        tls = self._local()
+        with torch.cuda.stream(tls.stream):
+            h_y = self._staging("y", y.shape, cdt, True)
+            h_y.numpy()[...] = y.astype(cdt_np, copy=False)
+            h_p = self._staging("p", pilot_vals.shape, cdt, True)
+            h_p.numpy()[...] = pilot_vals.astype(cdt_np, copy=False)
+            h_n = self._staging("n", (n,), torch.float32, True)
+            h_n.numpy()[...] = noise_feat
+            h_m = self._staging("m", (n * U,), torch.int32, True)
+            h_m.numpy()[...] = mod_order.reshape(-1)
+            d_y = self._staging("y", y.shape, cdt, False)
+            d_p = self._staging("p", pilot_vals.shape, cdt, False)
+            d_n = self._staging("n", (n,), torch.float32, False)
+            d_m = self._staging("m", (n * U,), torch.int32, False)
+            for d, h in ((d_y, h_y), (d_p, h_p), (d_n, h_n), (d_m, h_m)):
+                d.copy_(h, non_blocking=True)
+            d_llr = self._staging("llr", (n, U, S, T, llr_width), torch.float32, False)
+            d_chest = self._staging("chest", (n, U, S, T, B), torch.complex64, False)
+            self.forward_device(cfg, d_y, d_p, d_n, d_m, num_iterations, d_llr, d_chest, stream=tls.stream)
+            h_llr = self._staging("llr", d_llr.shape, torch.float32, True)
+            h_chest = self._staging("chest", d_chest.shape, torch.complex64, True)
+            h_llr.copy_(d_llr, non_blocking=True)
+            h_chest.copy_(d_chest, non_blocking=True)
+        tls.stream.synchronize()
+        return h_llr.numpy().copy(), h_chest.numpy().copy()

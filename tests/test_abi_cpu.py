@@ -1,0 +1,97 @@
+"""CPU-only checks of the C ABI: the library loads, exports every symbol the
+header declares, names/validates/packs weights without a GPU."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2409_02912_b200 import _lib
+from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, expected_shapes, init_weights
+from paper_2409_02912_b200.engine import pack_weights, pilot_comb_values
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "nrx_b200.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(nrx_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    names = declared_functions()
+    assert len(names) >= 10
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(_lib.EXPORTED)
+    assert lib.nrx_abi_version() == 1
+
+
+@pytest.mark.parametrize("variant,supported,kw", [
+    ("single", (14,), {}),
+    ("masking", (9, 14, 19), dict(d_s=56, num_iterations=2)),
+    ("var_io", (9, 14, 19), dict(d_s=8, hidden_width=20)),
+    ("single", (14,), dict(include_noise_plane=False, kernel_size=5)),
+])
+def test_weight_names_match_expected_shapes(variant, supported, kw):
+    config = NrxConfig.from_table(default_mcs_table(), supported, variant=variant, **kw)
+    names = _lib.weight_names(config)
+    shapes = expected_shapes(config)
+    assert set(names) == set(shapes) and len(names) == len(shapes)
+    lib = _lib.load()
+    m = _lib.model_desc(config)
+    for i, n in enumerate(names):
+        assert lib.nrx_weight_numel(ctypes.byref(m), i) == int(np.prod(shapes[n]))
+
+
+def test_pack_weights_deterministic_and_sized():
+    config = NrxConfig(d_s=56, num_iterations=2)
+    w = init_weights(config, 0)
+    a = pack_weights(config, w, "fp32")
+    b = pack_weights(config, {k: v.copy() for k, v in w.items()}, "fp32")
+    np.testing.assert_array_equal(a, b)
+    # every weight value lands somewhere in the packed blob (no value dropped)
+    packed = a.view(np.float32)
+    for name in ("iteration.update.conv0.w", "readout_chest.fc1.w"):
+        vals = np.unique(w[name])
+        assert np.isin(vals, packed).all()
+    with pytest.raises(ValueError):
+        pack_weights(config, {k: v for k, v in w.items() if k != "readout_chest.fc1.b"})
+
+
+def test_validate_limits():
+    lib = _lib.load()
+    ok = _lib.model_desc(NrxConfig(d_s=56))
+    s = _lib.slot_desc(SlotConfig(num_subcarriers=3276, num_ues=2))
+    assert lib.nrx_validate(ctypes.byref(ok), ctypes.byref(s)) == 0
+    too_deep = _lib.model_desc(NrxConfig(d_s=96))
+    assert lib.nrx_validate(ctypes.byref(too_deep), None) == 2  # unsupported, not invalid
+    bad = _lib.model_desc(NrxConfig(d_s=8))
+    bad.kernel_size = 4
+    assert lib.nrx_validate(ctypes.byref(bad), None) == 1
+    assert "workspace" in _lib.status_text(3)
+
+
+def test_workspace_and_geometry():
+    config = NrxConfig(d_s=56, num_iterations=2)
+    cfg = SlotConfig(num_subcarriers=3276, num_ues=2)
+    geo = _lib.buffer_geometry(config, cfg, "fp32")
+    assert geo["Tp"] == 15 and geo["rows_slab"] % 128 == 0 and geo["rows_slab"] >= 3276 * 15
+    assert geo["Cs"] >= 58 and geo["Cf"] >= 19
+    lib = _lib.load()
+    nb = lib.nrx_workspace_bytes(ctypes.byref(_lib.model_desc(config)), ctypes.byref(_lib.slot_desc(cfg)), 4, 0)
+    assert nb >= 4 * 2 * geo["rows_slab"] * 4 * (geo["Cf"] + geo["Cs"] + geo["Ch"] + geo["Ca"])
+
+
+def test_pilot_comb_values_layout():
+    cfg = SlotConfig(num_subcarriers=25, num_ues=2, comb_size=2, pilot_symbols=(2, 11))
+    vals = np.arange(2 * 25 * 14).reshape(2, 25, 14).astype(np.complex128)
+    p = pilot_comb_values(vals, cfg)
+    assert p.shape == (2, 13, 2)
+    assert p[1, 3, 1] == vals[1, 1 + 3 * 2, 11]
+    assert p[0, 12, 0] == vals[0, 24, 2]
