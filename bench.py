@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 NRX forward pass (the path BASELINE.json names).
+
+Workload (BASELINE.json configs[1] geometry, batched as configs[4]): slots of
+273 PRB (S=3276 subcarriers) x 14 symbols, 2 UEs (16-QAM), 4 RX antennas,
+the real-time NRX (d_s=56, N_it=2, 137,156 random-init weights).  A "step"
+is one batched forward over --slots-per-step independent slots per GPU with
+inputs resident in HBM; ranks shard independent slots (weak scaling, no
+data-path collective).  The JSON line also carries the single-slot latency
+p50/p99 (device-resident, CUDA graph), the end-to-end number through the
+public host API (pinned H2D of inputs + D2H of LLRs/chest inside the timed
+region), the roofline of the dominant kernel, and the reference CPU path
+timed on this host.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+S_C2, U_C2, D_S, N_IT = 3276, 2, 56, 2
+METRIC = "NRX forward slots/s at 273 PRB (2 UE, 4 RX, RT d_s=56 N_it=2); p50/p99 single-slot latency in latency_us"
+
+
+def c2_setup():
+    from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights
+    table = default_mcs_table()
+    cfg = SlotConfig(num_subcarriers=S_C2, num_ues=U_C2, comb_size=2)
+    config = NrxConfig.from_table(table, (14,), variant="single", d_s=D_S, num_iterations=N_IT)
+    return cfg, config, init_weights(config, seed=0), (table[14], table[14])
+
+
+def host_batch(cfg, n_slots: int, pool: int = 8, seed: int = 0):
+    """(y c64 (N,S,T,B), pilots c64 (N,U,F,K), noise (N,), mods (N*U,)) from a
+    pool of distinct synthetic slots (each with its own pilot book)."""
+    from paper_2409_02912_b200.engine import pilot_comb_values
+    from paper_2409_02912_b200.nrx import noise_features
+    from paper_2409_02912_b200.synth import synth_slots
+    y, books, _ = synth_slots(cfg, [4] * cfg.num_ues, min(pool, n_slots), 0.1, seed=seed)
+    idx = np.arange(n_slots) % y.shape[0]
+    vals = np.stack([books[i].values for i in idx])
+    pil = pilot_comb_values(vals, cfg).astype(np.complex64)
+    return (np.ascontiguousarray(y[idx]).astype(np.complex64), pil, noise_features(0.1, n_slots),
+            np.full(n_slots * cfg.num_ues, 4, dtype=np.int32))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+        return False
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 5 + i and s[5 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def conv_update0_flops_per_slab_re(d=D_S, k=3):
+    return 2 * k * k * (2 * d + 2) * d
+
+
+def algorithmic_flops_per_slab_re(d=D_S, h=D_S, n_it=N_IT, m=4, B=4, cin=19, k=3):
+    """MAC = 9 Cin d + 9 d^2 + N_it (2 d h + 9 (2d+2) d + 9 d^2) + (d h + h m) + (d h + h 2B)."""
+    kk = k * k
+    mac = kk * cin * d + kk * d * d + n_it * (2 * d * h + kk * (2 * d + 2) * d + kk * d * d) \
+        + (d * h + h * m) + (d * h + h * 2 * B)
+    return 2 * mac
+
+
+def traffic_from_profiles(kernel: str, precision: str):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+        return t.get(precision, {}).get(kernel)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the unmodified reference nrx_forward on this host's CPUs
+# ---------------------------------------------------------------------------
+
+
+def reference_impl():
+    """(nrx_forward, kind): oracle/_ref (pip-installed reference) or the oracle port."""
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref_dir, "nrxsim")):
+        sys.path.insert(0, ref_dir)
+        from nrxsim.nrx import nrx_forward
+        return nrx_forward, "reference"
+    from oracle.nrx_oracle import nrx_forward
+    return nrx_forward, "port"
+
+
+def run_reference(args, slots: int, warmup: int):
+    """Time the reference CPU path: one slot per call (latency_bench style,
+    evaluation.py:341-349) -> slots/s."""
+    fwd, kind = reference_impl()
+    cfg, config, w, mcs = c2_setup()
+    from paper_2409_02912_b200.synth import synth_slots
+    y, books, _ = synth_slots(cfg, [4, 4], min(slots, 4), 0.1, seed=11)
+    if kind == "reference":
+        # the reference's own types (its isinstance checks need them) and
+        # weights as recorded autodiff tensors, exactly as cli.cmd_bench builds them
+        import dataclasses
+        from nrxsim import autodiff as ad
+        from nrxsim import nrx as rnrx
+        from nrxsim import slot as rslot
+        cfg = rslot.SlotConfig(**{f.name: getattr(cfg, f.name) for f in dataclasses.fields(rslot.SlotConfig)})
+        config = rnrx.NrxConfig(**{f.name: getattr(config, f.name) for f in dataclasses.fields(rnrx.NrxConfig)})
+        mcs = tuple(rslot.McsEntry(m.index, m.modulation_order, m.code_rate) for m in mcs)
+        books = [rslot.PilotBook(values=b.values, config=cfg) for b in books]
+        w = {k: ad.Tensor(v, requires_grad=True) for k, v in w.items()}
+    for i in range(warmup):
+        fwd(y[i % len(y)], books[i % len(y)], cfg, mcs, w, config, 0.1)
+    times = []
+    for i in range(slots):
+        t0 = time.perf_counter()
+        fwd(y[i % len(y)], books[i % len(y)], cfg, mcs, w, config, 0.1)
+        times.append(time.perf_counter() - t0)
+    times = np.asarray(times)
+    return {"value": float(1.0 / times.mean()), "unit": "slots/s", "kind": kind,
+            "cores": int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1)),
+            "p50_ms": float(np.median(times) * 1e3), "p99_ms": float(np.percentile(times, 99) * 1e3),
+            "sample": f"{slots} single-slot nrx_forward calls at C2 (273 PRB, 2 UE, d_s=56, N_it=2) after {warmup} warm-up"}
+
+
+def cpu_baseline_subprocess(slots=3, warmup=1):
+    """Run the reference arm in a child process so OpenBLAS gets all cores."""
+    env = dict(os.environ)
+    env["OPENBLAS_NUM_THREADS"] = str(os.cpu_count() or 1)
+    env.pop("WORLD_SIZE", None); env.pop("RANK", None); env.pop("LOCAL_RANK", None)
+    cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--cpu-json",
+           "--steps", str(slots), "--warmup", str(warmup)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": "slots/s", "kind": "unavailable", "cores": os.cpu_count(),
+                "sample": f"failed: {e!r}"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2409_02912_b200 import _lib
+    from paper_2409_02912_b200.engine import NrxEngine
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    cfg, config, w, mcs = c2_setup()
+    eng = NrxEngine(config, w, precision=args.precision, device=dev)
+    B = args.slots_per_step
+    U, S, T, BR = cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, config.num_rx_ant
+
+    # two device-resident input sets, alternated so consecutive steps never
+    # re-read the same inputs from L2 (per-step activations are GBs anyway)
+    sets = []
+    for s in range(2):
+        y, pil, nf, mods = host_batch(cfg, B, seed=100 * rank + s)
+        sets.append(tuple(torch.from_numpy(a).to(dev) for a in (y, pil, nf, mods)))
+    llr = torch.empty((B, U, S, T, 4), dtype=torch.float32, device=dev)
+    chest = torch.empty((B, U, S, T, BR), dtype=torch.complex64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    ws = eng.workspace(cfg, B)
+
+    def step(i):
+        y, pil, nf, mods = sets[i & 1]
+        eng.forward_device(cfg, y, pil, nf, mods, N_IT, llr, chest, workspace=ws, stream=stream)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler, _lib.KernelTimer(("conv_update0",), max_records=4 * args.steps * N_IT + 16) as kt:
+        e0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        kernel_ms = kt.collect().get("conv_update0", [])
+    elapsed = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        t = torch.tensor([elapsed], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        dist.barrier()
+    torch.cuda.synchronize()
+    slots_total = B * args.steps * world
+    value = slots_total / elapsed
+    ms_per_step = elapsed / args.steps * 1e3
+
+    # roofline of the dominant kernel (conv_update0), device time of each launch
+    peaks, peak_src = load_peaks()
+    flops_launch = conv_update0_flops_per_slab_re() * B * U * S * T
+    kavg = float(np.mean(kernel_ms)) / 1e3 if kernel_ms else float("nan")
+    achieved = flops_launch / kavg / 1e12
+    if args.precision == "bf16":
+        peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+        peak_note = f"bf16 dense, sustained ({peak_src})"
+    else:
+        sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+        peak_note = "fp32 FFMA nominal (148 SM x 128 lanes x 2 x max clock)"
+    traffic = traffic_from_profiles("conv_update0", args.precision)
+
+    # single-slot latency (device resident), CUDA graph of the whole forward
+    lat = latency_single_slot(eng, cfg, dev, args.latency_runs) if rank == 0 else None
+
+    # end to end through the public host API: pinned H2D + D2H inside the region
+    e2e = e2e_throughput(eng, cfg, B, max(2, args.steps // 4), world, dev)
+
+    n_launch = eng.launch_count(N_IT)
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "slots/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.precision, "data": "synthetic (random QAM over Rayleigh multipath, random-init weights)",
+        "config": {"workload": f"C5-style batches of C2 slots: {B} slots/GPU/step of 273 PRB x 14 sym, "
+                               f"2 UE 16-QAM, 4 RX; RT NRX d_s=56 N_it=2 (configs[1] geometry)",
+                   "slots_per_step_per_gpu": B, "precision": args.precision,
+                   "l2": "inputs alternate between two device buffers (188 MB) and per-step activations "
+                         "are > 1 GB, i.e. far larger than the 126 MB L2"},
+        "latency_us": lat,
+        "e2e": e2e,
+        "roofline": {"kernel": "conv_update0 (iteration.update.conv0, 3x3 114->56, implicit GEMM)",
+                     "bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 1),
+                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "peak_source": peak_note,
+                     "algorithmic_flops_per_launch": flops_launch,
+                     "avg_launch_ms": round(kavg * 1e3, 4), "launches_timed": len(kernel_ms),
+                     "share_of_step": round(kavg * 1e3 * N_IT / ms_per_step, 4) if kernel_ms else None},
+        "whole_path": {"algorithmic_tflops": round(algorithmic_flops_per_slab_re() * U * S * T * value / world / 1e12, 2),
+                       "flop_per_slot": algorithmic_flops_per_slab_re() * U * S * T},
+        "gpu_launches": n_launch * args.steps,
+        "launches_per_step": n_launch,
+        "clocks": sampler.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_subprocess()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def latency_single_slot(eng, cfg, dev, runs: int):
+    import torch
+    y, pil, nf, mods = (torch.from_numpy(a).to(dev) for a in host_batch(cfg, 1, pool=1, seed=7))
+    llr = torch.empty((1, cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, 4), dtype=torch.float32, device=dev)
+    chest = torch.empty((1, cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, 4), dtype=torch.complex64, device=dev)
+    ws = torch.empty_like(eng.workspace(cfg, 1))
+    side = torch.cuda.Stream(dev)
+    mode = "cuda_graph"
+    with torch.cuda.stream(side):
+        for _ in range(3):
+            eng.forward_device(cfg, y, pil, nf, mods, N_IT, llr, chest, workspace=ws, stream=side)
+    side.synchronize()
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            eng.forward_device(cfg, y, pil, nf, mods, N_IT, llr, chest, workspace=ws, stream=side)
+        run = g.replay
+    except Exception:
+        mode = "stream"
+
+        def run():
+            eng.forward_device(cfg, y, pil, nf, mods, N_IT, llr, chest, workspace=ws,
+                               stream=torch.cuda.current_stream(dev))
+    for _ in range(20):
+        run()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(runs)]
+    cur = torch.cuda.current_stream(dev)
+    for a, b in ev:
+        a.record(cur)
+        run()
+        b.record(cur)
+    torch.cuda.synchronize()
+    us = np.array([a.elapsed_time(b) * 1e3 for a, b in ev])
+    return {"p50": round(float(np.median(us)), 2), "p99": round(float(np.percentile(us, 99)), 2),
+            "min": round(float(us.min()), 2), "runs": runs, "mode": mode,
+            "note": "one C2 slot, device-resident inputs (no host copies), back-to-back launches"}
+
+
+def e2e_throughput(eng, cfg, B, steps, world, dev):
+    """NrxEngine.run_arrays (numpy in/out): includes staging into pinned
+    memory, H2D of y/pilots/noise/mods and D2H of the LLR + chest grids."""
+    import torch
+    import torch.distributed as dist
+    y, pil, nf, mods = host_batch(cfg, B, seed=3)
+    eng.run_arrays(cfg, y, pil, nf, mods, N_IT, 4)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        llr, chest = eng.run_arrays(cfg, y, pil, nf, mods, N_IT, 4)
+    el = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([el], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    h2d = y.nbytes + pil.nbytes + nf.nbytes + mods.nbytes
+    d2h = llr.nbytes + chest.nbytes
+    return {"value": round(B * steps * world / el, 2), "unit": "slots/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "api": "NrxEngine.run_arrays (numpy in/out, pinned staging, wall clock incl. sync)"}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--precision", choices=("bf16", "fp32"), default=os.environ.get("NRX_BENCH_PRECISION", "fp32"))
+    ap.add_argument("--slots-per-step", type=int, default=32)
+    ap.add_argument("--latency-runs", type=int, default=2000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-json", action="store_true", help=argparse.SUPPRESS)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        world, rank, _ = dist_env()
+        if rank != 0:
+            return
+        res = run_reference(args, slots=max(1, args.steps), warmup=max(1, min(args.warmup, 2)))
+        if args.cpu_json:
+            print(json.dumps(res))
+            return
+        cfg_desc = {"workload": "single C2 slot per step (273 PRB x 14 sym, 2 UE 16-QAM, 4 RX; RT NRX "
+                                "d_s=56 N_it=2), the reference's own nrx_forward on host CPUs",
+                    "slots_per_step": 1}
+        secs = 1.0 / res["value"]
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": round(res["value"], 4), "unit": "slots/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(secs * 1e3, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic (random QAM over Rayleigh multipath, random-init weights)", "config": cfg_desc,
+            "latency_us": {"p50": round(res["p50_ms"] * 1e3, 1), "p99": round(res["p99_ms"] * 1e3, 1)},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "kind", "cores", "sample")},
+            "e2e": {"value": round(res["value"], 4), "unit": "slots/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}), flush=True)
+        return
+    run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

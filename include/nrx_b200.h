@@ -160,6 +160,19 @@ int nrx_ls_features(const nrx_model_desc* model, const nrx_slot_desc* slot, int 
                     int pilots_c128, int n_pilot_sets, const float* noise_feat,
                     void* feats_out, void* stream);
 
+/* Optional per-launch device timing (bench.py's roofline measurement).
+ * While enabled, nrx_forward brackets every launch whose kernel id bit is
+ * set in kernel_mask with CUDA events recorded on the launch stream.
+ * Kernel ids: 0 ls_feat, 1 conv state_init.conv0, 2 conv state_init.conv1,
+ * 3 msg_agg, 4 conv iteration.update.conv0, 5 conv iteration.update.conv1,
+ * 6 readout.  nrx_profile_collect waits for the recorded events, writes up
+ * to cap (kernel id, milliseconds) records, clears them and returns the
+ * count.  Process-wide; not meant for concurrent use. */
+int nrx_profile_enable(uint32_t kernel_mask, int max_records);
+int nrx_profile_collect(int32_t* kernel_ids, float* ms, int cap);
+void nrx_profile_disable(void);
+const char* nrx_kernel_name(int kernel_id);
+
 /* Number of kernel launches one nrx_forward call enqueues. */
 int nrx_forward_launch_count(const nrx_model_desc* model, int precision, int num_iterations);
 

@@ -22,7 +22,10 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnrx_b200
 EXPORTED = ("nrx_abi_version", "nrx_status_string", "nrx_validate", "nrx_weight_count",
             "nrx_weight_name", "nrx_weight_numel", "nrx_packed_weight_bytes", "nrx_pack_weights",
             "nrx_workspace_bytes", "nrx_forward", "nrx_buffer_geometry", "nrx_ls_features",
-            "nrx_forward_launch_count")
+            "nrx_forward_launch_count", "nrx_profile_enable", "nrx_profile_collect",
+            "nrx_profile_disable", "nrx_kernel_name")
+KERNEL_IDS = {"ls_feat": 0, "conv_state_init0": 1, "conv_state_init1": 2, "msg_agg": 3,
+              "conv_update0": 4, "conv_update1": 5, "readout": 6}
 
 
 class ModelDesc(ctypes.Structure):
@@ -73,6 +76,11 @@ def load() -> ctypes.CDLL:
     lib.nrx_forward_launch_count.argtypes = [P(ModelDesc), I, I]
     lib.nrx_buffer_geometry.argtypes = [P(ModelDesc), P(SlotDesc), I, P(ctypes.c_int32)]
     lib.nrx_ls_features.argtypes = [P(ModelDesc), P(SlotDesc), I, I, V, I, V, I, I, V, V, V]
+    lib.nrx_profile_enable.argtypes = [ctypes.c_uint32, I]
+    lib.nrx_profile_collect.argtypes = [P(ctypes.c_int32), P(ctypes.c_float), I]
+    lib.nrx_profile_disable.restype = None
+    lib.nrx_kernel_name.argtypes = [I]
+    lib.nrx_kernel_name.restype = ctypes.c_char_p
     if lib.nrx_abi_version() != 1:
         raise NrxLibraryError("libnrx_b200.so ABI version mismatch")
     _LIB = lib
@@ -143,3 +151,34 @@ def buffer_geometry(config, cfg, precision: str) -> dict:
     check(lib.nrx_buffer_geometry(ctypes.byref(model_desc(config)), ctypes.byref(slot_desc(cfg)),
                                   PRECISIONS[precision], out), "nrx_buffer_geometry")
     return dict(zip(("rows_slab", "Tp", "Cf", "Cs", "Ch", "Ca", "cw", "tiles"), list(out)))
+
+
+class KernelTimer:
+    """Collect per-launch device times of selected kernels (CUDA events
+    recorded by the library around each launch, on the launch stream)."""
+
+    def __init__(self, kernels=("conv_update0",), max_records: int = 4096):
+        self.lib = load()
+        self.mask = 0
+        for k in kernels:
+            self.mask |= 1 << KERNEL_IDS[k]
+        self.max_records = max_records
+
+    def __enter__(self):
+        check(self.lib.nrx_profile_enable(self.mask, self.max_records), "nrx_profile_enable")
+        return self
+
+    def collect(self) -> dict:
+        ids = (ctypes.c_int32 * self.max_records)()
+        ms = (ctypes.c_float * self.max_records)()
+        n = self.lib.nrx_profile_collect(ids, ms, self.max_records)
+        if n < 0:
+            raise NrxLibraryError("nrx_profile_collect failed")
+        out = {}
+        for i in range(n):
+            out.setdefault(self.lib.nrx_kernel_name(ids[i]).decode(), []).append(ms[i])
+        return out
+
+    def __exit__(self, *exc):
+        self.lib.nrx_profile_disable()
+        return False

@@ -13,6 +13,7 @@
 #include <cstring>
 
 #include "nrx_kernels.h"
+#include "nrx_profile.h"
 
 namespace nrx {
 int make_geom(const nrx_model_desc* m, const nrx_slot_desc* s, int n_slots, int prec, Geom* g);
@@ -46,22 +47,23 @@ static int forward_simt(const Geom& g, const PackLayout& L, const WsLayout& W, i
   a.dst = h; a.cdst = g.Ch; a.mode = EPI_RELU;
   a.n_off = g.n_io;
   for (int i = 0; i < g.n_io; ++i) a.off[i] = L.init0[i];
-  NRX_TRY(launch_conv_simt(g, a, st));
+  { ProfScope p(KID_INIT0, st); NRX_TRY(launch_conv_simt(g, a, st)); }
   // state init, conv1: h -> state
   a.src0 = h; a.c0 = g.Ch; a.dst = state; a.cdst = g.Cs; a.mode = EPI_STATE_INIT;
   for (int i = 0; i < g.n_io; ++i) a.off[i] = L.init1[i];
-  NRX_TRY(launch_conv_simt(g, a, st));
+  { ProfScope p(KID_INIT1, st); NRX_TRY(launch_conv_simt(g, a, st)); }
   for (int it = 0; it < n_it; ++it) {
-    NRX_TRY(launch_msg_agg_simt(g, L, wb, state, agg, st));
+    { ProfScope p(KID_MSG, st); NRX_TRY(launch_msg_agg_simt(g, L, wb, state, agg, st)); }
     ConvArgs c{};
     c.wbase = wb; c.n_off = 1;
     c.src0 = state; c.c0 = g.Cs; c.src1 = agg; c.c1 = g.Ca;
     c.dst = h; c.cdst = g.Ch; c.mode = EPI_RELU; c.off[0] = L.upd0;
-    NRX_TRY(launch_conv_simt(g, c, st));
+    { ProfScope p(KID_UPD0, st); NRX_TRY(launch_conv_simt(g, c, st)); }
     c.src0 = h; c.c0 = g.Ch; c.src1 = nullptr; c.c1 = 0;
     c.dst = state; c.cdst = g.Cs; c.mode = EPI_RESIDUAL; c.off[0] = L.upd1;
-    NRX_TRY(launch_conv_simt(g, c, st));
+    { ProfScope p(KID_UPD1, st); NRX_TRY(launch_conv_simt(g, c, st)); }
   }
+  ProfScope p(KID_READOUT, st);
   return launch_readout_simt(g, L, wb, state, mod_order, llr, chest, st);
 }
 
@@ -88,7 +90,10 @@ extern "C" int nrx_forward(const nrx_model_desc* model, const nrx_slot_desc* slo
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   const uint8_t* wb = static_cast<const uint8_t*>(packed_weights);
 
-  NRX_TRY(launch_ls_feat(g, y, y_c128, pilots, pilots_c128, n_pilot_sets, noise_feat, ws + W.feats, st));
+  {
+    ProfScope p(KID_LSFEAT, st);
+    NRX_TRY(launch_ls_feat(g, y, y_c128, pilots, pilots_c128, n_pilot_sets, noise_feat, ws + W.feats, st));
+  }
   if (precision == NRX_FP32)
     return forward_simt(g, L, W, num_iterations, wb, mod_order, ws, llr_out, static_cast<float2*>(chest_out), st);
   return launch_forward_tc(g, L, W, num_iterations, wb, mod_order, ws, llr_out, static_cast<float2*>(chest_out), st);
