@@ -150,7 +150,15 @@ int dmax_of(int d) { return d <= 16 ? 16 : d <= 32 ? 32 : 64; }
 //         buffer channels rounded to 8; b: [nw]
 //   mlp   w0: [dmax][h], b0: [h], w1: [h][outp], b1: [outp]
 //         (outp = dmax for msg, 8 for the LLR readout, 16 for the chest)
-// BF16 (tcgen05 kernels) additionally stores bf16 B operands, see k_tc.cu.
+// BF16 (tcgen05 kernels): every GEMM operand B is stored as W^T in the
+// K-major no-swizzle core-matrix layout the MMA reads from shared memory,
+// [K/8][N][8] bf16 (element (n, k) at ((k/8)*N + n)*8 + k%8); biases fp32.
+//   conv      w: K = taps*ktap (tap-major, then buffer channel), N = np
+//   msg       w0: K = Cs, N = hp;  w1: K = hp, N = np
+//   readout   (per IO set, LLR and chest MLPs fused) w0: K = Cs, N = 2hp
+//             ([llr hidden | chest hidden]);  w1: K = 2hp, N = 32 block
+//             diagonal (outputs 0..7 LLR, 8..8+2B chest)
+// with np = rup(d,16), hp = rup(h,16).
 void pack_layout(const nrx_model_desc* m, int prec, PackLayout* L) {
   Geom g;
   nrx_slot_desc s{};
@@ -163,6 +171,31 @@ void pack_layout(const nrx_model_desc* m, int prec, PackLayout* L) {
   L->dmax = dmax;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+  if (prec == NRX_BF16) {
+    const int np = rup(m->d_s, 16), hp = rup(m->hidden, 16);
+    auto conv = [&](ConvOff& c, int ktap) {
+      c.ktap = ktap;
+      c.w = take((size_t)taps * ktap * np * 2);
+      c.b = take((size_t)np * 4);
+    };
+    auto mlp = [&](MlpOff& o, int k0, int n0, int n1) {
+      o.out = n1;
+      o.w0 = take((size_t)k0 * n0 * 2);
+      o.b0 = take((size_t)n0 * 4);
+      o.w1 = take((size_t)n0 * n1 * 2);
+      o.b1 = take((size_t)n1 * 4);
+    };
+    for (int i = 0; i < m->n_io; ++i) {
+      conv(L->init0[i], g.Cf);
+      conv(L->init1[i], g.Ch);
+      mlp(L->llr[i], g.Cs, 2 * hp, 32);
+    }
+    mlp(L->msg, g.Cs, hp, np);
+    conv(L->upd0, g.Cs + g.Ca);
+    conv(L->upd1, g.Ch);
+    L->total = off;
+    return;
+  }
   auto conv = [&](ConvOff& c, int ktap, int cdst) {
     int nw = rup(cdst, 8);
     c.ktap = ktap;
@@ -233,7 +266,99 @@ void pack_mlp_f32(int din, int dmax, int h, int out, const MlpOff& o, const floa
   for (int c = 0; c < o.out; ++c) q1[c] = c < out ? b1[c] : 0.f;
 }
 
+uint16_t f32_to_bf16(float f) {
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  if ((x & 0x7f800000u) == 0x7f800000u && (x & 0x007fffffu)) return (uint16_t)((x >> 16) | 0x40);  // quiet NaN
+  x += 0x7fffu + ((x >> 16) & 1u);  // round to nearest even
+  return (uint16_t)(x >> 16);
+}
+
+// B operand writer: element (n, k) of a [N][K] K-major matrix.
+struct BOperand {
+  uint16_t* p;
+  int N;
+  void set(int n, int k, float v) { p[((size_t)(k / 8) * N + n) * 8 + (k % 8)] = f32_to_bf16(v); }
+};
+
+void pack_conv_bf16(const Geom& g, int k, const ConvOff& c, int cin_ref, const float* w, const float* b,
+                    ChanMap map, uint8_t* base) {
+  const int np = rup(g.d, 16), taps = k * k, cout = g.d;
+  BOperand B{(uint16_t*)(base + c.w), np};
+  for (int tap = 0; tap < taps; ++tap)
+    for (int j = 0; j < c.ktap; ++j) {
+      const int src = map(j, g);
+      for (int o = 0; o < np; ++o)
+        B.set(o, tap * c.ktap + j, (src >= 0 && o < cout) ? w[((size_t)tap * cin_ref + src) * cout + o] : 0.f);
+    }
+  float* db = (float*)(base + c.b);
+  for (int o = 0; o < np; ++o) db[o] = o < cout ? b[o] : 0.f;
+}
+
 }  // namespace
+
+int pack_weights_bf16(const nrx_model_desc* m, const float* const* t, uint8_t* base) {
+  PackLayout L;
+  pack_layout(m, NRX_BF16, &L);
+  std::memset(base, 0, L.total);
+  Geom g;
+  nrx_slot_desc s{};
+  s.num_subcarriers = 64; s.num_symbols = 14; s.num_ues = 1; s.comb_size = 1;
+  s.num_pilot_symbols = 1;
+  make_geom(m, &s, 1, NRX_BF16, &g);
+  const int k = m->kernel_size, d = m->d_s, h = m->hidden, B2 = 2 * m->num_rx_ant;
+  const int np = rup(d, 16), hp = rup(h, 16);
+  // indices of the shared tensors in the canonical order (include/nrx_b200.h)
+  const int i_msg = 8 * m->n_io, i_upd = i_msg + 4, i_chest = i_upd + 4;
+  for (int io = 0; io < m->n_io; ++io) {
+    const int i = 8 * io;
+    pack_conv_bf16(g, k, L.init0[io], g.Cin, t[i], t[i + 1], map_identity_feats, base);
+    pack_conv_bf16(g, k, L.init1[io], d, t[i + 2], t[i + 3], map_identity_hidden, base);
+    // fused readout: fc0 = [llr fc0 | chest fc0], fc1 block diagonal
+    const MlpOff& o = L.llr[io];
+    const int width = llr_width_of(m, io);
+    const float *lw0 = t[i + 4], *lb0 = t[i + 5], *lw1 = t[i + 6], *lb1 = t[i + 7];
+    const float *cw0 = t[i_chest], *cb0 = t[i_chest + 1], *cw1 = t[i_chest + 2], *cb1 = t[i_chest + 3];
+    BOperand W0{(uint16_t*)(base + o.w0), 2 * hp};
+    float* b0 = (float*)(base + o.b0);
+    for (int n = 0; n < 2 * hp; ++n) {
+      const bool chest = n >= hp;
+      const int nn = chest ? n - hp : n;
+      for (int kk = 0; kk < g.Cs; ++kk)
+        W0.set(n, kk, (kk < d && nn < h) ? (chest ? cw0 : lw0)[(size_t)kk * h + nn] : 0.f);
+      b0[n] = nn < h ? (chest ? cb0 : lb0)[nn] : 0.f;
+    }
+    BOperand W1{(uint16_t*)(base + o.w1), 32};
+    float* b1 = (float*)(base + o.b1);
+    for (int n = 0; n < 32; ++n) {
+      for (int kk = 0; kk < 2 * hp; ++kk) {
+        float v = 0.f;
+        if (n < width && kk < h) v = lw1[(size_t)kk * width + n];
+        if (n >= 8 && n < 8 + B2 && kk >= hp && kk - hp < h) v = cw1[(size_t)(kk - hp) * B2 + (n - 8)];
+        W1.set(n, kk, v);
+      }
+      b1[n] = n < width ? lb1[n] : (n >= 8 && n < 8 + B2) ? cb1[n - 8] : 0.f;
+    }
+  }
+  {
+    const float *w0 = t[i_msg], *b0 = t[i_msg + 1], *w1 = t[i_msg + 2], *b1 = t[i_msg + 3];
+    BOperand W0{(uint16_t*)(base + L.msg.w0), hp};
+    float* pb0 = (float*)(base + L.msg.b0);
+    for (int n = 0; n < hp; ++n) {
+      for (int kk = 0; kk < g.Cs; ++kk) W0.set(n, kk, (kk < d && n < h) ? w0[(size_t)kk * h + n] : 0.f);
+      pb0[n] = n < h ? b0[n] : 0.f;
+    }
+    BOperand W1{(uint16_t*)(base + L.msg.w1), np};
+    float* pb1 = (float*)(base + L.msg.b1);
+    for (int n = 0; n < np; ++n) {
+      for (int kk = 0; kk < hp; ++kk) W1.set(n, kk, (kk < h && n < d) ? w1[(size_t)kk * d + n] : 0.f);
+      pb1[n] = n < d ? b1[n] : 0.f;
+    }
+  }
+  pack_conv_bf16(g, k, L.upd0, 2 * d + 2, t[i_upd], t[i_upd + 1], map_update, base);
+  pack_conv_bf16(g, k, L.upd1, d, t[i_upd + 2], t[i_upd + 3], map_identity_hidden, base);
+  return NRX_OK;
+}
 
 int pack_weights_f32(const nrx_model_desc* m, const float* const* t, uint8_t* base) {
   PackLayout L;
@@ -331,7 +456,11 @@ int nrx_pack_weights(const nrx_model_desc* m, int prec, const float* const* tens
   for (int i = 0; i < n; ++i)
     if (!tensors[i]) return NRX_ERR_INVALID;
   if (prec == NRX_FP32) return pack_weights_f32(m, tensors, (uint8_t*)out);
-  return NRX_ERR_UNSUPPORTED;
+  if (prec == NRX_BF16) {
+    if (m->hidden > 128) return NRX_ERR_UNSUPPORTED;
+    return pack_weights_bf16(m, tensors, (uint8_t*)out);
+  }
+  return NRX_ERR_INVALID;
 }
 
 size_t nrx_workspace_bytes(const nrx_model_desc* m, const nrx_slot_desc* s, int n_slots, int prec) {

@@ -49,7 +49,7 @@ def check_chest(got, ref, precision):
     assert np.abs(got - ref).max() <= gate["max"] * scale
 
 
-@pytest.mark.parametrize("precision", ["fp32"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
 @pytest.mark.parametrize("name", CASES)
 def test_golden_forward(name, precision):
     """Drop-in nrx_forward vs the reference's own outputs on reference inputs."""
@@ -110,7 +110,7 @@ def _c2_setup(d=56, n_it=2, U=2, S=3276, variant="single", supported=(14,), seed
     return cfg, config, w, table
 
 
-@pytest.mark.parametrize("precision", ["fp32"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_c2_rt_slot_vs_oracle(precision):
     """273 PRB / 2 UE / 4 RX / RT model (d=56, N_it=2): the benchmark config."""
     _, gnrx = _gpu()
