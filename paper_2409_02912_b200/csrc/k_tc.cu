@@ -203,8 +203,21 @@ struct ConvTcParams {
   float* dst32;         // fp32 master state (STATE_INIT / RESIDUAL), or null
 };
 
-constexpr int CONV_THREADS = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+// warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue (two warps per
+// TMEM lane quarter, each draining half of the accumulator columns)
+constexpr int CONV_THREADS = 320;
+constexpr int CONV_EPI_THREADS = 256;
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int NP, int MODE>
 __global__ void __launch_bounds__(CONV_THREADS, 1)
     k_conv_tc(const __grid_constant__ ConvTcParams p, const __grid_constant__ CUtensorMap map0,
               const __grid_constant__ CUtensorMap map1) {
@@ -220,6 +233,7 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
   uint64_t* tempty = bars + 18;
   uint64_t* wbar = bars + 20;
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 21);
+  float* sbias = reinterpret_cast<float*>(bars + 22);  // NP floats
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) tmem_alloc(tmem_ptr, p.tmem_cols);
@@ -230,11 +244,13 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], CONV_EPI_THREADS);
     }
     mbar_init(wbar, 1);
     fence_barrier_init();
   }
+  if (threadIdx.x >= 64 && threadIdx.x < 64 + NP)
+    sbias[threadIdx.x - 64] = reinterpret_cast<const float*>(p.wbase + p.b_off[io])[threadIdx.x - 64];
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -259,7 +275,7 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
-      const uint32_t idesc = idesc_bf16(NRX_TILE_M, p.np);
+      constexpr uint32_t idesc = idesc_bf16(NRX_TILE_M, NP);
       const uint32_t wsm = smem_u32(Ws);
       const int kch = p.ktap / 8;  // 16-byte channel chunks per tap
       mbar_wait(wbar, 0);
@@ -292,10 +308,11 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
         ++it;
       }
     }
-  } else {  // ---------------- epilogue: warps 2..5, TMEM lane quarter = warp % 4
-    const int q = warp & 3;
+  } else {  // ---------------- epilogue: warps 2..9
+    constexpr int NC = NP / 2;  // accumulator columns per thread
+    const int q = warp & 3, half = (warp - 2) >> 2;
     const int r = 32 * q + lane;
-    const float* bias = reinterpret_cast<const float*>(p.wbase + p.b_off[io]);
+    const int cbase = half * NC;
     const int nd = p.cdst / 8, n32 = p.d4 / 4;
     WorkIter w(g, g.NU, g.tiles, p.n_io, p.mod_order);
     int slab, tile, it = 0;
@@ -304,13 +321,10 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      float v[80];
+      float v[NC];
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * NP + cbase;
 #pragma unroll
-      for (int i = 0; i < 80; ++i) v[i] = 0.f;
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * p.np;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (c * 16 < p.np) tmem_ld16(taddr + c * 16, v + c * 16);
+      for (int c = 0; c < NC / 8; ++c) tmem_ld8(taddr + 8 * c, v + 8 * c);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -318,47 +332,56 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
       const int row = tile * NRX_TILE_M + r;
       const int s = row / g.Tp, t = row - s * g.Tp;
       const bool valid = row < g.rows_data && t < g.T;
-      const int u = slab % g.U;
-      // fp32 master (residual input / output)
-      if (p.dst32 && p.mode == EPI_RESIDUAL && valid) {
+      float old[NC];
+      if (MODE == EPI_RESIDUAL) {  // fp32 residual stream: issue every load before use
 #pragma unroll
-        for (int c4 = 0; c4 < 16; ++c4) {
-          if (c4 >= n32) break;
-          const float4 o = *reinterpret_cast<const float4*>(chunk_ptr(p.dst32, slab, n32, c4, row, g));
-          const float old[4] = {o.x, o.y, o.z, o.w};
+        for (int c4 = 0; c4 < NC / 4; ++c4) {
+          const int cc = cbase / 4 + c4;
+          float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (valid && cc < n32) o = *reinterpret_cast<const float4*>(chunk_ptr(p.dst32, slab, n32, cc, row, g));
+          old[4 * c4 + 0] = o.x;
+          old[4 * c4 + 1] = o.y;
+          old[4 * c4 + 2] = o.z;
+          old[4 * c4 + 3] = o.w;
+        }
+      }
+      float x[NC];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = 4 * c4 + e;
-            if (c < g.d) v[c] = old[e] + (v[c] + bias[c]);
+      for (int j = 0; j < NC; ++j) {
+        const int c = cbase + j;
+        float y = v[j] + sbias[c];  // conv + bias first, as the reference adds them
+        if (MODE == EPI_RELU) y = fmaxf(y, 0.f);
+        if (MODE == EPI_RESIDUAL) y = old[j] + y;
+        x[j] = (valid && c < g.d) ? y : 0.f;
+      }
+      if (MODE != EPI_RELU) {
+#pragma unroll
+        for (int c4 = 0; c4 < NC / 4; ++c4) {
+          const int cc = cbase / 4 + c4;
+          if (cc < n32) store_chunk(chunk_ptr(p.dst32, slab, n32, cc, row, g), x + 4 * c4);
+        }
+        if (valid) {  // positional channels d, d+1 of the bf16 operand copy
+          const float pdt = g.dt[t], pdf = pos_df(s, slab % g.U, g);
+#pragma unroll
+          for (int j = 0; j < NC; ++j) {
+            const int c = cbase + j;
+            if (c == g.d) x[j] = pdt;
+            if (c == g.d + 1) x[j] = pdf;
           }
         }
-      } else if (valid) {
-#pragma unroll
-        for (int c = 0; c < 64; ++c)
-          if (c < g.d) v[c] = p.mode == EPI_RELU ? fmaxf(v[c] + bias[c], 0.f) : v[c] + bias[c];
       }
 #pragma unroll
-      for (int c8 = 0; c8 < 10; ++c8) {
-        if (c8 >= nd) break;
-        float o[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int c = 8 * c8 + e;
-          o[e] = !valid ? 0.f : c < g.d ? v[c] : (p.mode == EPI_RELU ? 0.f : state_extra(c, s, t, u, g));
-        }
-        store_chunk(chunk_ptr(p.dst, slab, nd, c8, row, g), o);
+      for (int c8 = 0; c8 < NC / 8; ++c8) {
+        const int cc = cbase / 8 + c8;
+        if (cc < nd) store_chunk(chunk_ptr(p.dst, slab, nd, cc, row, g), x + 8 * c8);
       }
-      if (p.dst32 && p.mode != EPI_RELU) {
+      if (half == 1) {  // buffer channels beyond the accumulator: positional / zero only
+        for (int cc = NP / 8; cc < nd; ++cc) {
+          float o[8];
 #pragma unroll
-        for (int c4 = 0; c4 < 16; ++c4) {
-          if (c4 >= n32) break;
-          float o[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = 4 * c4 + e;
-            o[e] = (valid && c < g.d) ? v[c] : 0.f;
-          }
-          store_chunk(chunk_ptr(p.dst32, slab, n32, c4, row, g), o);
+          for (int e = 0; e < 8; ++e)
+            o[e] = (valid && MODE != EPI_RELU) ? state_extra(8 * cc + e, s, t, slab % g.U, g) : 0.f;
+          store_chunk(chunk_ptr(p.dst, slab, nd, cc, row, g), o);
         }
       }
       ++it;
@@ -814,7 +837,7 @@ static int launch_conv(const Geom& g, const PackLayout& L, const ConvOff* offs, 
   p.mod_order = mod_order;
   p.dst = dst;
   p.dst32 = dst32;
-  const size_t fixed = ((p.wbytes + 1023) & ~1023u) + 22 * 8 + 64;
+  const size_t fixed = ((p.wbytes + 1023) & ~1023u) + 22 * 8 + 64 * 4 + 64;
   int stages = 4;
   while (stages > 1 && fixed + (size_t)stages * p.abytes > SMEM_LIMIT) --stages;
   if (fixed + (size_t)stages * p.abytes > SMEM_LIMIT || p.rbox > 256) return NRX_ERR_UNSUPPORTED;
@@ -825,10 +848,18 @@ static int launch_conv(const Geom& g, const PackLayout& L, const ConvOff* offs, 
   if (rc) return rc;
   rc = make_map(&m1, src1 ? src1 : src0, g, c1 ? c1 : c0, p.rbox);
   if (rc) return rc;
-  if (set_smem((const void*)k_conv_tc, SMEM_LIMIT)) return NRX_ERR_CUDA;
+  using KFn = void (*)(const ConvTcParams, const CUtensorMap, const CUtensorMap);
+  static const KFn table[4][3] = {
+      {k_conv_tc<16, 0>, k_conv_tc<16, 1>, k_conv_tc<16, 2>},
+      {k_conv_tc<32, 0>, k_conv_tc<32, 1>, k_conv_tc<32, 2>},
+      {k_conv_tc<48, 0>, k_conv_tc<48, 1>, k_conv_tc<48, 2>},
+      {k_conv_tc<64, 0>, k_conv_tc<64, 1>, k_conv_tc<64, 2>}};
+  if (p.np % 16 || p.np < 16 || p.np > 64 || mode < 0 || mode > 2) return NRX_ERR_UNSUPPORTED;
+  const KFn fn = table[p.np / 16 - 1][mode];
+  if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.NU * g.tiles;
   dim3 grid(total < num_sms() ? total : num_sms(), n_off);
-  k_conv_tc<<<grid, CONV_THREADS, smem, st>>>(p, m0, m1);
+  fn<<<grid, CONV_THREADS, smem, st>>>(p, m0, m1);
   return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
 }
 

@@ -19,10 +19,14 @@ __device__ __forceinline__ int comb_dist(int s, int u, const Geom& g) {
   return d;
 }
 
-// float32(dist / S) exactly as numpy: int/int true-divide in float64, cast.
+// float32(dist / S) as numpy computes it (int/int true-divide in float64,
+// then cast).  For integers below 2^24 the correctly rounded fp32 quotient is
+// identical: the float64 quotient can never fall on (or across) a float32
+// rounding midpoint, since any midpoint differs from a/b by >= 1/(b 2^k)
+// while the float64 error is < 2^-28 / 2^k.
 __device__ __forceinline__ float pos_df(int s, int u, const Geom& g) {
   if (!g.freq_enc) return 0.f;
-  return __double2float_rn(__ddiv_rn((double)comb_dist(s, u, g), (double)g.S));
+  return __fdiv_rn((float)comb_dist(s, u, g), (float)g.S);
 }
 
 // Value a producer writes into state channel c >= d (pos encoding / zero).
