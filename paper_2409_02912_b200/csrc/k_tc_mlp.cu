@@ -1,0 +1,420 @@
+// bf16 tensor-core per-RE MLPs (NRX_BF16 path).
+//
+//  k_msg_tc      message MLP of every UE of a slot on a 128-RE tile followed
+//                by the float64 sum of the other UEs' messages
+//                (cgnn_iteration nrx.py:258-260, sum_others autodiff.py:276-294).
+//  k_readout_tc  LLR and channel-estimate MLPs fused into one N=2h GEMM plus a
+//                block-diagonal N=32 GEMM, writing the user-facing (N,U,S,T,W)
+//                LLRs and the planar-decoded complex64 chest
+//                (readout_llrs/readout_chest nrx.py:266-281, nrx.py:382-384).
+//
+// Both are persistent, warp-specialised two-layer MLPs:
+//   warp 0      TMA producer: state tiles {8, 128, Cs/8, 1} into a 4-stage ring
+//   warp 1      MMA issuer: fc0(j+1) is issued before waiting for the hidden
+//               layer of j, so the tensor core and the hidden epilogue overlap
+//   warps 2-5   hidden epilogue: TMEM -> +bias, ReLU -> bf16 -> shared memory
+//               (the next GEMM's K-major A operand), double buffered
+//   warps 6-9   output epilogue: sum-of-others / LLR + chest stores
+// "use" j enumerates the (work item, UE) pairs a CTA processes.
+#include "tc_common.cuh"
+
+namespace nrx {
+namespace tc {
+
+constexpr int MLP_THREADS = 320;
+constexpr int MSG_MAXU = 4;  // UEs per slot on the tensor-core path
+constexpr int A_STAGES = 4;
+
+struct MlpTcParams {
+  Geom g;
+  int cs, hp, op;          // A channels (state buffer), hidden (padded), output columns
+  int uses_per_item;       // U for the message MLP, 1 for the readout
+  int units;               // work units: slots (msg) or slabs (readout)
+  int n_io;
+  uint32_t w0bytes, w1bytes, abytes, hbytes, tmem_cols;
+  uint32_t col_h, col_o;   // TMEM column of hidden buffer 0 / output region 0
+  const uint8_t* wbase;
+  uint64_t w0[NRX_MAX_IO], b0[NRX_MAX_IO], w1[NRX_MAX_IO], b1[NRX_MAX_IO];
+  const int32_t* mod_order;
+  __nv_bfloat16* agg;      // message MLP output
+  float* llr;              // readout outputs
+  float2* chest;
+};
+
+// Shared-memory carve-up of the MLP kernels.
+struct MlpSmem {
+  uint8_t *W0, *W1, *As, *Hs;
+  uint64_t *afull, *aempty, *hid_full, *h_ready, *hs_free, *out_full, *out_free, *wbar;
+  float *sb0, *sb1;
+  uint32_t* tmem_ptr;
+  __device__ MlpSmem(uint8_t* smem, const MlpTcParams& p) {
+    W0 = smem;
+    W1 = W0 + p.w0bytes;
+    As = W1 + p.w1bytes;
+    Hs = As + A_STAGES * p.abytes;
+    uint64_t* b = reinterpret_cast<uint64_t*>(Hs + 2 * p.hbytes);
+    afull = b;
+    aempty = b + A_STAGES;
+    hid_full = b + 2 * A_STAGES;
+    h_ready = hid_full + 2;
+    hs_free = h_ready + 2;
+    out_full = hs_free + 2;
+    out_free = out_full + 2;
+    wbar = out_free + 2;
+    sb0 = reinterpret_cast<float*>(wbar + 2);
+    sb1 = sb0 + 256;
+    tmem_ptr = reinterpret_cast<uint32_t*>(sb1 + 64);
+  }
+};
+
+__device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int io) {
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc(s.tmem_ptr, p.tmem_cols);
+  if (threadIdx.x == 32) {
+    for (int i = 0; i < A_STAGES; ++i) {
+      mbar_init(&s.afull[i], 1);
+      mbar_init(&s.aempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s.hid_full[i], 1);
+      mbar_init(&s.h_ready[i], 128);
+      mbar_init(&s.hs_free[i], 1);
+      mbar_init(&s.out_full[i], 1);
+      mbar_init(&s.out_free[i], 128);
+    }
+    mbar_init(s.wbar, 1);
+    fence_barrier_init();
+  }
+  const float* b0 = reinterpret_cast<const float*>(p.wbase + p.b0[io]);
+  const float* b1 = reinterpret_cast<const float*>(p.wbase + p.b1[io]);
+  for (int i = threadIdx.x; i < p.hp; i += blockDim.x) s.sb0[i] = b0[i];
+  for (int i = threadIdx.x; i < p.op; i += blockDim.x) s.sb1[i] = b1[i];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+}
+
+// Producer / MMA / hidden-epilogue roles are identical for both MLPs; the
+// output epilogue is passed in as a functor.
+template <typename OutEpilogue>
+__device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int io, const CUtensorMap* amap,
+                                         OutEpilogue&& out_epi) {
+  const Geom& g = p.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t tmem_base = *s.tmem_ptr;
+  const int U = p.uses_per_item;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(s.wbar, p.w0bytes + p.w1bytes);
+      bulk_load(s.W0, p.wbase + p.w0[io], p.w0bytes, s.wbar);
+      bulk_load(s.W1, p.wbase + p.w1[io], p.w1bytes, s.wbar);
+      WorkIter w(g, p.units, g.tiles, p.n_io, p.mod_order);
+      int unit, tile, st = 0;
+      uint32_t ph = 0;
+      while (w.next(unit, tile)) {
+        for (int u = 0; u < U; ++u) {
+          mbar_wait(&s.aempty[st], ph ^ 1);
+          mbar_expect_tx(&s.afull[st], p.abytes);
+          tma_load_4d(s.As + (size_t)st * p.abytes, amap, &s.afull[st], 0, tile * (NRX_TILE_M / 16), 0,
+                      unit * U + u);
+          if (++st == A_STAGES) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {  // MMA issuer: whole warp, elect.sync issues
+    {
+      const uint32_t id0 = idesc_bf16(NRX_TILE_M, p.hp), id1 = idesc_bf16(NRX_TILE_M, p.op);
+      const uint32_t w0s = smem_u32(s.W0), w1s = smem_u32(s.W1);
+      mbar_wait(s.wbar, 0);
+      tc_fence_after();
+      WorkIter w(g, p.units, g.tiles, p.n_io, p.mod_order);
+      int unit, tile;
+      bool have = w.next(unit, tile);
+      int st = 0, j = 0, item = 0;
+      uint32_t ph = 0;
+      auto fc0 = [&](int jj) {  // hidden[jj & 1] = A(stage) x W0
+        mbar_wait(&s.afull[st], ph);
+        tc_fence_after();
+        const uint32_t as = smem_u32(s.As + (size_t)st * p.abytes);
+        const uint32_t d = tmem_base + p.col_h + (jj & 1) * p.hp;
+        uint64_t ad = smem_desc(as, NRX_TILE_M * 16, 128), bd = smem_desc(w0s, p.hp * 16, 128);
+        for (int kc = 0; kc < p.cs / 8; kc += 2) {
+          mma_bf16_warp(d, ad, bd, id0, kc != 0);
+          ad += 2 * NRX_TILE_M;
+          bd += 2 * p.hp;
+        }
+        mma_commit_warp(&s.aempty[st]);
+        mma_commit_warp(&s.hid_full[jj & 1]);
+        if (++st == A_STAGES) { st = 0; ph ^= 1; }
+      };
+      if (have) fc0(0);
+      while (have) {
+        for (int u = 0; u < U; ++u, ++j) {
+          // look ahead: the next use's fc0 overlaps this use's hidden epilogue
+          const bool last_u = u + 1 == U;
+          int nunit = unit, ntile = tile;
+          bool next_exists = true;
+          if (last_u) next_exists = w.next(nunit, ntile);
+          if (next_exists) fc0(j + 1);
+          const int hb = j & 1;
+          mbar_wait(&s.h_ready[hb], (j >> 1) & 1);
+          tc_fence_after();
+          if (u == 0) {  // output region of this item free again?
+            mbar_wait(&s.out_free[item & 1], ((item >> 1) & 1) ^ 1);
+            tc_fence_after();
+          }
+          const uint32_t hs = smem_u32(s.Hs + (size_t)hb * p.hbytes);
+          const uint32_t d = tmem_base + p.col_o + (item & 1) * (U * p.op) + u * p.op;
+          uint64_t ad = smem_desc(hs, NRX_TILE_M * 16, 128), bd = smem_desc(w1s, p.op * 16, 128);
+          for (int kc = 0; kc < p.hp / 8; kc += 2) {
+            mma_bf16_warp(d, ad, bd, id1, kc != 0);
+            ad += 2 * NRX_TILE_M;
+            bd += 2 * p.op;
+          }
+          mma_commit_warp(&s.hs_free[hb]);
+          if (last_u) {
+            mma_commit_warp(&s.out_full[item & 1]);
+            ++item;
+            unit = nunit;
+            tile = ntile;
+            have = next_exists;
+          }
+        }
+      }
+    }
+  } else if (warp < 6) {  // hidden epilogue
+    const int q = warp & 3;
+    const int r = 32 * q + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
+    WorkIter w(g, p.units, g.tiles, p.n_io, p.mod_order);
+    int unit, tile, j = 0;
+    while (w.next(unit, tile)) {
+      for (int u = 0; u < U; ++u, ++j) {
+        const int hb = j & 1;
+        mbar_wait(&s.hid_full[hb], (j >> 1) & 1);
+        tc_fence_after();
+        mbar_wait(&s.hs_free[hb], ((j >> 1) & 1) ^ 1);  // fc1 of use j-2 done with Hs[hb]
+        uint8_t* H = s.Hs + (size_t)hb * p.hbytes;
+        for (int c32 = 0; c32 < p.hp; c32 += 32) {
+          float v[32];
+          tmem_ld16(tmem_base + lane_off + p.col_h + hb * p.hp + c32, v);
+          if (c32 + 16 < p.hp) tmem_ld16(tmem_base + lane_off + p.col_h + hb * p.hp + c32 + 16, v + 16);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c8 = 0; c8 < 4; ++c8) {
+            if (c32 + 8 * c8 >= p.hp) break;
+            float o[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = fmaxf(v[8 * c8 + e] + s.sb0[c32 + 8 * c8 + e], 0.f);
+            store_chunk(reinterpret_cast<__nv_bfloat16*>(H + ((size_t)(c32 / 8 + c8) * NRX_TILE_M + r) * 16), o);
+          }
+        }
+        fence_proxy_async();  // generic-proxy smem writes -> tensor-core reads
+        tc_fence_before();
+        mbar_arrive(&s.h_ready[hb]);
+      }
+    }
+  } else {  // output epilogue (warps 6..9)
+    const int q = warp & 3;
+    const int r = 32 * q + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
+    WorkIter w(g, p.units, g.tiles, p.n_io, p.mod_order);
+    int unit, tile, item = 0;
+    while (w.next(unit, tile)) {
+      mbar_wait(&s.out_full[item & 1], (item >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + lane_off + p.col_o + (item & 1) * (U * p.op);
+      out_epi(unit, tile, r, taddr, &s.out_free[item & 1]);
+      ++item;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+__global__ void __launch_bounds__(MLP_THREADS, 1)
+    k_msg_tc(const __grid_constant__ MlpTcParams p, const __grid_constant__ CUtensorMap smap) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  MlpSmem s(smem, p);
+  mlp_setup(p, s, 0);
+  const Geom& g = p.g;
+  const int U = p.uses_per_item;
+  const int nca = g.Ca / 8;
+  mlp_body(p, s, 0, &smap, [&](int n, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
+    const int row = tile * NRX_TILE_M + r;
+    const int srow = row / g.Tp, t = row - srow * g.Tp;
+    const bool valid = row < g.rows_data && t < g.T;
+    for (int c16 = 0; c16 < p.op; c16 += 16) {
+      float m[MSG_MAXU][16];
+#pragma unroll
+      for (int u = 0; u < MSG_MAXU; ++u)
+        if (u < U) tmem_ld16(taddr + u * p.op + c16, m[u]);
+      tmem_wait_ld();
+      if (c16 + 16 >= p.op) {  // all messages are in registers: release TMEM
+        tc_fence_before();
+        mbar_arrive(free_bar);
+      }
+      double tot[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        tot[e] = 0.0;
+#pragma unroll
+        for (int u = 0; u < MSG_MAXU; ++u)
+          if (u < U) {
+            m[u][e] += s.sb1[c16 + e];
+            tot[e] += (double)m[u][e];
+          }
+      }
+#pragma unroll
+      for (int u = 0; u < MSG_MAXU; ++u) {
+        if (u >= U) break;
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c8 = c16 / 8 + h2;
+          if (c8 >= nca) break;
+          float o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int c = 8 * c8 + e;
+            o[e] = (valid && c < g.d) ? (float)(tot[8 * h2 + e] - (double)m[u][8 * h2 + e]) : 0.f;
+          }
+          store_chunk(chunk_ptr(p.agg, n * U + u, nca, c8, row, g), o);
+        }
+      }
+    }
+  });
+}
+
+__global__ void __launch_bounds__(MLP_THREADS, 1)
+    k_readout_tc(const __grid_constant__ MlpTcParams p, const __grid_constant__ CUtensorMap smap) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  MlpSmem s(smem, p);
+  const int io = p.n_io > 1 ? blockIdx.y : 0;
+  mlp_setup(p, s, io);
+  const Geom& g = p.g;
+  mlp_body(p, s, io, &smap, [&](int slab, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
+    float o[32];
+    tmem_ld16(taddr, o);
+    tmem_ld16(taddr + 16, o + 16);
+    tmem_wait_ld();
+    tc_fence_before();
+    mbar_arrive(free_bar);
+    const int row = tile * NRX_TILE_M + r;
+    const int srow = row / g.Tp, t = row - srow * g.Tp;
+    if (row >= g.rows_data || t >= g.T) return;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) o[c] += s.sb1[c];
+    const int mio = io_index(p.mod_order, slab, g);
+    const int width = mio < 0 ? 0 : g.io_width[mio];
+    const size_t re = ((size_t)slab * g.S + srow) * g.T + t;
+    float* lp = p.llr + re * g.llr_width;
+    if (g.llr_width == 4 && width == 4) {
+      *reinterpret_cast<float4*>(lp) = make_float4(o[0], o[1], o[2], o[3]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < g.llr_width) lp[c] = mio < 0 ? __int_as_float(0x7fc00000) : (c < width ? o[c] : 0.f);
+    }
+    float2* cp = p.chest + re * g.B;
+    if (g.B == 4) {  // planar decode: channel b real, channel B+b imaginary
+      reinterpret_cast<float4*>(cp)[0] = make_float4(o[8], o[12], o[9], o[13]);
+      reinterpret_cast<float4*>(cp)[1] = make_float4(o[10], o[14], o[11], o[15]);
+    } else {
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        if (b >= g.B) break;
+        float im = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k == b) im = o[8 + g.B + k];  // static register indexing
+        cp[b] = make_float2(o[8 + b], im);
+      }
+    }
+  });
+}
+
+}  // namespace tc
+
+using namespace tc;
+
+static int mlp_common(MlpTcParams& p, const Geom& g, int hp, int op, int uses, int units, size_t* smem) {
+  p.g = g;
+  p.cs = g.Cs;
+  p.hp = hp;
+  p.op = op;
+  p.uses_per_item = uses;
+  p.units = units;
+  p.w0bytes = (uint32_t)(p.cs * hp * 2);
+  p.w1bytes = (uint32_t)(hp * op * 2);
+  p.abytes = (uint32_t)(p.cs * NRX_TILE_M * 2);
+  p.hbytes = (uint32_t)(hp * NRX_TILE_M * 2);
+  p.col_h = 0;
+  p.col_o = 2 * hp;
+  const uint32_t cols = 2 * hp + 2 * uses * op;
+  if (cols > 512 || hp > 256) return NRX_ERR_UNSUPPORTED;
+  p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+  *smem = (size_t)p.w0bytes + p.w1bytes + A_STAGES * p.abytes + 2 * p.hbytes + (2 * A_STAGES + 12) * 8 +
+          (256 + 64) * 4 + 16;
+  return *smem > SMEM_LIMIT ? NRX_ERR_UNSUPPORTED : NRX_OK;
+}
+
+int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const __nv_bfloat16* state,
+               __nv_bfloat16* agg, cudaStream_t st) {
+  if (g.U > MSG_MAXU) return NRX_ERR_UNSUPPORTED;
+  MlpTcParams p{};
+  size_t smem = 0;
+  int rc = mlp_common(p, g, rup(g.h, 16), rup(g.d, 16), g.U, g.N, &smem);
+  if (rc) return rc;
+  p.n_io = 1;
+  p.wbase = wb;
+  p.w0[0] = L.msg.w0;
+  p.b0[0] = L.msg.b0;
+  p.w1[0] = L.msg.w1;
+  p.b1[0] = L.msg.b1;
+  p.agg = agg;
+  CUtensorMap m;
+  rc = make_map(&m, state, g, g.Cs, NRX_TILE_M);
+  if (rc) return rc;
+  if (set_smem((const void*)k_msg_tc, SMEM_LIMIT)) return NRX_ERR_CUDA;
+  const int total = g.N * g.tiles;
+  const int per_sm = (512 / p.tmem_cols) < 2 || 2 * smem > SMEM_LIMIT ? 1 : 2;
+  const int cap = num_sms() * per_sm;
+  k_msg_tc<<<total < cap ? total : cap, MLP_THREADS, smem, st>>>(p, m);
+  return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
+}
+
+int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const __nv_bfloat16* state,
+                   const int32_t* mod_order, float* llr, float2* chest, cudaStream_t st) {
+  MlpTcParams p{};
+  size_t smem = 0;
+  int rc = mlp_common(p, g, 2 * rup(g.h, 16), 32, 1, g.NU, &smem);
+  if (rc) return rc;
+  p.n_io = g.n_io;
+  p.wbase = wb;
+  for (int i = 0; i < g.n_io; ++i) {
+    p.w0[i] = L.llr[i].w0;
+    p.b0[i] = L.llr[i].b0;
+    p.w1[i] = L.llr[i].w1;
+    p.b1[i] = L.llr[i].b1;
+  }
+  p.mod_order = mod_order;
+  p.llr = llr;
+  p.chest = chest;
+  CUtensorMap m;
+  rc = make_map(&m, state, g, g.Cs, NRX_TILE_M);
+  if (rc) return rc;
+  if (set_smem((const void*)k_readout_tc, SMEM_LIMIT)) return NRX_ERR_CUDA;
+  const int total = g.NU * g.tiles;
+  const int per_sm = (512 / p.tmem_cols) < 2 || 2 * smem > SMEM_LIMIT ? 1 : 2;
+  const int cap = num_sms() * per_sm;
+  dim3 grid(total < cap ? total : cap, g.n_io);
+  k_readout_tc<<<grid, MLP_THREADS, smem, st>>>(p, m);
+  return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
+}
+
+}  // namespace nrx
