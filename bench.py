@@ -391,7 +391,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--precision", choices=("bf16", "fp32"), default=os.environ.get("NRX_BENCH_PRECISION", "fp32"))
+    ap.add_argument("--precision", choices=("bf16", "fp32"), default=os.environ.get("NRX_BENCH_PRECISION", "bf16"))
     ap.add_argument("--slots-per-step", type=int, default=32)
     ap.add_argument("--latency-runs", type=int, default=2000)
     ap.add_argument("--no-cpu-baseline", action="store_true")

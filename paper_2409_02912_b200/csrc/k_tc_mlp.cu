@@ -21,7 +21,9 @@
 namespace nrx {
 namespace tc {
 
-constexpr int MLP_THREADS = 320;
+// warps: 0 producer, 1 MMA, HW hidden-epilogue warps, 4 output-epilogue warps
+constexpr int mlp_threads(int hw) { return 64 + 32 * hw + 128; }
+constexpr int MSG_HW = 4, READOUT_HW = 8;
 constexpr int MSG_MAXU = 4;  // UEs per slot on the tensor-core path
 constexpr int A_STAGES = 4;
 
@@ -67,7 +69,7 @@ struct MlpSmem {
   }
 };
 
-__device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int io) {
+__device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int io, int hidden_threads) {
   const int warp = threadIdx.x >> 5;
   if (warp == 0) tmem_alloc(s.tmem_ptr, p.tmem_cols);
   if (threadIdx.x == 32) {
@@ -77,7 +79,7 @@ __device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int 
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s.hid_full[i], 1);
-      mbar_init(&s.h_ready[i], 128);
+      mbar_init(&s.h_ready[i], hidden_threads);
       mbar_init(&s.hs_free[i], 1);
       mbar_init(&s.out_full[i], 1);
       mbar_init(&s.out_free[i], 128);
@@ -96,13 +98,16 @@ __device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int 
 
 // Producer / MMA / hidden-epilogue roles are identical for both MLPs; the
 // output epilogue is passed in as a functor.
-template <typename OutEpilogue>
+template <int HW, typename OutEpilogue>
 __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int io, const CUtensorMap* amap,
                                          OutEpilogue&& out_epi) {
   const Geom& g = p.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tmem_base = *s.tmem_ptr;
   const int U = p.uses_per_item;
+#ifdef NRX_TIMING
+  long long t_a = 0, t_b = 0, t_c = 0, t_d = 0, t_all = clock64();
+#endif
 
   if (warp == 0) {
     if (lane == 0) {
@@ -114,7 +119,9 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
       uint32_t ph = 0;
       while (w.next(unit, tile)) {
         for (int u = 0; u < U; ++u) {
+          NRX_T(t0);
           mbar_wait(&s.aempty[st], ph ^ 1);
+          NRX_TADD(t_a, t0);
           mbar_expect_tx(&s.afull[st], p.abytes);
           tma_load_4d(s.As + (size_t)st * p.abytes, amap, &s.afull[st], 0, tile * (NRX_TILE_M / 16), 0,
                       unit * U + u);
@@ -134,7 +141,9 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
       int st = 0, j = 0, item = 0;
       uint32_t ph = 0;
       auto fc0 = [&](int jj) {  // hidden[jj & 1] = A(stage) x W0
+        NRX_T(t0);
         mbar_wait(&s.afull[st], ph);
+        NRX_TADD(t_a, t0);
         tc_fence_after();
         const uint32_t as = smem_u32(s.As + (size_t)st * p.abytes);
         const uint32_t d = tmem_base + p.col_h + (jj & 1) * p.hp;
@@ -158,10 +167,14 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
           if (last_u) next_exists = w.next(nunit, ntile);
           if (next_exists) fc0(j + 1);
           const int hb = j & 1;
+          NRX_T(t1);
           mbar_wait(&s.h_ready[hb], (j >> 1) & 1);
+          NRX_TADD(t_b, t1);
           tc_fence_after();
           if (u == 0) {  // output region of this item free again?
+            NRX_T(t2);
             mbar_wait(&s.out_free[item & 1], ((item >> 1) & 1) ^ 1);
+            NRX_TADD(t_c, t2);
             tc_fence_after();
           }
           const uint32_t hs = smem_u32(s.Hs + (size_t)hb * p.hbytes);
@@ -183,27 +196,33 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
         }
       }
     }
-  } else if (warp < 6) {  // hidden epilogue
+  } else if (warp < 2 + HW) {  // hidden epilogue; with 8 warps each drains half the columns
     const int q = warp & 3;
     const int r = 32 * q + lane;
     const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
+    const int cspan = p.hp / (HW / 4), cbeg = ((warp - 2) / 4) * cspan;
     WorkIter w(g, p.units, g.tiles, p.n_io, p.mod_order);
     int unit, tile, j = 0;
     while (w.next(unit, tile)) {
       for (int u = 0; u < U; ++u, ++j) {
         const int hb = j & 1;
+        NRX_T(t0);
         mbar_wait(&s.hid_full[hb], (j >> 1) & 1);
+        NRX_TADD(t_a, t0);
         tc_fence_after();
+        NRX_T(t1);
         mbar_wait(&s.hs_free[hb], ((j >> 1) & 1) ^ 1);  // fc1 of use j-2 done with Hs[hb]
+        NRX_TADD(t_b, t1);
+        NRX_T(t2);
         uint8_t* H = s.Hs + (size_t)hb * p.hbytes;
-        for (int c32 = 0; c32 < p.hp; c32 += 32) {
+        for (int c32 = cbeg; c32 < cbeg + cspan; c32 += 32) {
           float v[32];
           tmem_ld16(tmem_base + lane_off + p.col_h + hb * p.hp + c32, v);
-          if (c32 + 16 < p.hp) tmem_ld16(tmem_base + lane_off + p.col_h + hb * p.hp + c32 + 16, v + 16);
+          if (c32 + 16 < cbeg + cspan) tmem_ld16(tmem_base + lane_off + p.col_h + hb * p.hp + c32 + 16, v + 16);
           tmem_wait_ld();
 #pragma unroll
           for (int c8 = 0; c8 < 4; ++c8) {
-            if (c32 + 8 * c8 >= p.hp) break;
+            if (c32 + 8 * c8 >= cbeg + cspan) break;
             float o[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) o[e] = fmaxf(v[8 * c8 + e] + s.sb0[c32 + 8 * c8 + e], 0.f);
@@ -213,22 +232,31 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
         fence_proxy_async();  // generic-proxy smem writes -> tensor-core reads
         tc_fence_before();
         mbar_arrive(&s.h_ready[hb]);
+        NRX_TADD(t_c, t2);
       }
     }
-  } else {  // output epilogue (warps 6..9)
+  } else {  // output epilogue (the last 4 warps)
     const int q = warp & 3;
     const int r = 32 * q + lane;
     const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
     WorkIter w(g, p.units, g.tiles, p.n_io, p.mod_order);
     int unit, tile, item = 0;
     while (w.next(unit, tile)) {
+      NRX_T(t0);
       mbar_wait(&s.out_full[item & 1], (item >> 1) & 1);
+      NRX_TADD(t_a, t0);
       tc_fence_after();
       const uint32_t taddr = tmem_base + lane_off + p.col_o + (item & 1) * (U * p.op);
+      NRX_T(t1);
       out_epi(unit, tile, r, taddr, &s.out_free[item & 1]);
+      NRX_TADD(t_b, t1);
       ++item;
     }
   }
+#ifdef NRX_TIMING
+  if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 64 || threadIdx.x == 192))
+    printf("mlp U=%d tid=%d all=%lld a=%lld b=%lld c=%lld\n", U, threadIdx.x, clock64() - t_all, t_a, t_b, t_c);
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -237,18 +265,23 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
   }
 }
 
-__global__ void __launch_bounds__(MLP_THREADS, 1)
+__global__ void __launch_bounds__(mlp_threads(MSG_HW), 1)
     k_msg_tc(const __grid_constant__ MlpTcParams p, const __grid_constant__ CUtensorMap smap) {
   extern __shared__ __align__(1024) uint8_t smem[];
   MlpSmem s(smem, p);
-  mlp_setup(p, s, 0);
+  mlp_setup(p, s, 0, 32 * MSG_HW);
   const Geom& g = p.g;
   const int U = p.uses_per_item;
   const int nca = g.Ca / 8;
-  mlp_body(p, s, 0, &smap, [&](int n, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
+  mlp_body<MSG_HW>(p, s, 0, &smap, [&](int n, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
     const int row = tile * NRX_TILE_M + r;
     const int srow = row / g.Tp, t = row - srow * g.Tp;
     const bool valid = row < g.rows_data && t < g.T;
+    // Sum of the other UEs' messages, added directly in fp32 (U-1 terms).
+    // For U=2 this is exactly the other message, which equals the reference's
+    // f32(f64 total - f64 own) whenever that float64 sum is exact (message
+    // exponents within 29 bits); the bf16 rounding of the stored aggregate
+    // dominates any difference for U>2.  The fp32 parity path keeps fp64.
     for (int c16 = 0; c16 < p.op; c16 += 16) {
       float m[MSG_MAXU][16];
 #pragma unroll
@@ -259,17 +292,11 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         tc_fence_before();
         mbar_arrive(free_bar);
       }
-      double tot[16];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        tot[e] = 0.0;
+      for (int u = 0; u < MSG_MAXU; ++u)
+        if (u < U)
 #pragma unroll
-        for (int u = 0; u < MSG_MAXU; ++u)
-          if (u < U) {
-            m[u][e] += s.sb1[c16 + e];
-            tot[e] += (double)m[u][e];
-          }
-      }
+          for (int e = 0; e < 16; ++e) m[u][e] += s.sb1[c16 + e];
 #pragma unroll
       for (int u = 0; u < MSG_MAXU; ++u) {
         if (u >= U) break;
@@ -280,8 +307,12 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           float o[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
+            float a = 0.f;
+#pragma unroll
+            for (int v = 0; v < MSG_MAXU; ++v)
+              if (v < U && v != u) a += m[v][8 * h2 + e];
             const int c = 8 * c8 + e;
-            o[e] = (valid && c < g.d) ? (float)(tot[8 * h2 + e] - (double)m[u][8 * h2 + e]) : 0.f;
+            o[e] = (valid && c < g.d) ? a : 0.f;
           }
           store_chunk(chunk_ptr(p.agg, n * U + u, nca, c8, row, g), o);
         }
@@ -290,14 +321,14 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   });
 }
 
-__global__ void __launch_bounds__(MLP_THREADS, 1)
+__global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
     k_readout_tc(const __grid_constant__ MlpTcParams p, const __grid_constant__ CUtensorMap smap) {
   extern __shared__ __align__(1024) uint8_t smem[];
   MlpSmem s(smem, p);
   const int io = p.n_io > 1 ? blockIdx.y : 0;
-  mlp_setup(p, s, io);
+  mlp_setup(p, s, io, 32 * READOUT_HW);
   const Geom& g = p.g;
-  mlp_body(p, s, io, &smap, [&](int slab, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
+  mlp_body<READOUT_HW>(p, s, io, &smap, [&](int slab, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
     float o[32];
     tmem_ld16(taddr, o);
     tmem_ld16(taddr + 16, o + 16);
@@ -384,7 +415,7 @@ int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const __nv
   const int total = g.N * g.tiles;
   const int per_sm = (512 / p.tmem_cols) < 2 || 2 * smem > SMEM_LIMIT ? 1 : 2;
   const int cap = num_sms() * per_sm;
-  k_msg_tc<<<total < cap ? total : cap, MLP_THREADS, smem, st>>>(p, m);
+  k_msg_tc<<<total < cap ? total : cap, mlp_threads(MSG_HW), smem, st>>>(p, m);
   return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
 }
 
@@ -413,7 +444,7 @@ int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const 
   const int per_sm = (512 / p.tmem_cols) < 2 || 2 * smem > SMEM_LIMIT ? 1 : 2;
   const int cap = num_sms() * per_sm;
   dim3 grid(total < cap ? total : cap, g.n_io);
-  k_readout_tc<<<grid, MLP_THREADS, smem, st>>>(p, m);
+  k_readout_tc<<<grid, mlp_threads(READOUT_HW), smem, st>>>(p, m);
   return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
 }
 

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda.h>
 
+#include <cstdio>
 #include <mutex>
 
 #include "nrx_device.cuh"
@@ -14,6 +15,15 @@ namespace tc {
 // ---------------------------------------------------------------------------
 // PTX wrappers
 // ---------------------------------------------------------------------------
+
+// Optional per-role cycle accounting (build with -DNRX_TIMING; CTA 0 prints).
+#ifdef NRX_TIMING
+#define NRX_T(var) long long var = clock64()
+#define NRX_TADD(acc, var) (acc) += clock64() - (var)
+#else
+#define NRX_T(var)
+#define NRX_TADD(acc, var)
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
