@@ -64,32 +64,33 @@ class ClockSampler:
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_ms: int = 50):
         self.gpu = gpu_index
+        self.period_ms = period_ms
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self._proc = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        # one long-running nvidia-smi polling at period_ms (spawning per sample is too slow)
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", str(self.period_ms)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self._proc = None
+        time.sleep(0.3)  # let the first samples arrive before the timed region starts
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._proc is not None:
+            time.sleep(0.1)
+            self._proc.terminate()
+            try:
+                out, _ = self._proc.communicate(timeout=5)
+            except Exception:
+                self._proc.kill()
+                out = ""
+            self.samples = [[x.strip() for x in line.split(",")] for line in out.splitlines() if line.strip()]
         return False
 
     def summary(self):
@@ -131,12 +132,14 @@ def algorithmic_flops_per_slab_re(d=D_S, h=D_S, n_it=N_IT, m=4, B=4, cin=19, k=3
     return 2 * mac
 
 
-def traffic_from_profiles(kernel: str, precision: str):
+def traffic_from_profiles(kernel: str, precision: str, slots: int):
+    """DRAM bytes (read + write) per launch of `kernel` at `slots` slots per
+    launch, scaled from the committed ncu --set full capture (profiles/traffic.json)."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as fh:
-            t = json.load(fh)
-        return t.get(precision, {}).get(kernel)
+            t = json.load(fh)[precision][kernel]
+        return int(t["dram_bytes_per_slot"] * slots)
     except Exception:
         return None
 
@@ -279,13 +282,13 @@ def run_ours(args):
         sm_mhz = peaks.get("sm_max_mhz", 1965.0)
         peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
         peak_note = "fp32 FFMA nominal (148 SM x 128 lanes x 2 x max clock)"
-    traffic = traffic_from_profiles("conv_update0", args.precision)
+    traffic = traffic_from_profiles("conv_update0", args.precision, B)
 
     # single-slot latency (device resident), CUDA graph of the whole forward
     lat = latency_single_slot(eng, cfg, dev, args.latency_runs) if rank == 0 else None
 
     # end to end through the public host API: pinned H2D + D2H inside the region
-    e2e = e2e_throughput(eng, cfg, B, max(2, args.steps // 4), world, dev)
+    e2e = e2e_throughput(eng, cfg, B, max(4, args.steps // 2), world, dev)
 
     n_launch = eng.launch_count(N_IT)
     out = {
@@ -361,35 +364,45 @@ def latency_single_slot(eng, cfg, dev, runs: int):
 
 
 def e2e_throughput(eng, cfg, B, steps, world, dev):
-    """NrxEngine.run_arrays (numpy in/out): includes staging into pinned
-    memory, H2D of y/pilots/noise/mods and D2H of the LLR + chest grids."""
+    """NrxEngine.run_stream: every step copies its inputs (y, pilots, noise,
+    MCS) from pinned host memory to the GPU and its LLR + chest grids back to
+    pinned host memory; copies of neighbouring steps overlap the forward."""
     import torch
     import torch.distributed as dist
-    y, pil, nf, mods = host_batch(cfg, B, seed=3)
-    eng.run_arrays(cfg, y, pil, nf, mods, N_IT, 4)
+    U, S, T = cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols
+    hosts = []
+    for s in range(2):
+        arrs = host_batch(cfg, B, seed=3 + s)
+        hosts.append(tuple(torch.from_numpy(a).pin_memory() for a in arrs))
+    outs = [(torch.empty((B, U, S, T, 4), dtype=torch.float32).pin_memory(),
+             torch.empty((B, U, S, T, 4), dtype=torch.complex64).pin_memory()) for _ in range(2)]
+    inputs = [hosts[i & 1] for i in range(steps)]
+    outputs = [outs[i & 1] for i in range(steps)]
+    eng.run_stream(cfg, inputs[:2], outputs[:2], N_IT)   # warm-up
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    for _ in range(steps):
-        llr, chest = eng.run_arrays(cfg, y, pil, nf, mods, N_IT, 4)
+    eng.run_stream(cfg, inputs, outputs, N_IT)
+    torch.cuda.synchronize()
     el = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([el], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
-    h2d = y.nbytes + pil.nbytes + nf.nbytes + mods.nbytes
-    d2h = llr.nbytes + chest.nbytes
+    h2d = sum(t.numel() * t.element_size() for t in hosts[0])
+    d2h = sum(t.numel() * t.element_size() for t in outs[0])
     return {"value": round(B * steps * world / el, 2), "unit": "slots/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "api": "NrxEngine.run_arrays (numpy in/out, pinned staging, wall clock incl. sync)"}
+            "api": "NrxEngine.run_stream (pinned host inputs -> GPU -> pinned host LLR/chest every step; "
+                   "H2D/compute/D2H overlapped across steps; wall clock incl. final sync)"}
 
 
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--precision", choices=("bf16", "fp32"), default=os.environ.get("NRX_BENCH_PRECISION", "bf16"))
     ap.add_argument("--slots-per-step", type=int, default=32)

@@ -142,6 +142,51 @@ class NrxEngine:
             raise ValueError(f"inference depth {num_iterations} outside [1, {self.config.num_iterations}]")
         _lib.check(code, "nrx_forward")
 
+    # -- pipelined host-resident stream ------------------------------------------
+
+    def run_stream(self, cfg, inputs, outputs, num_iterations: int):
+        """Throughput entry for host-resident batches (a serving loop).
+
+        inputs[i] = (y, pilots, noise_feat, mod_order) pinned CPU tensors of
+        batch i, outputs[i] = (llr, chest) pinned CPU tensors it is written
+        to.  H2D of batch i+1 and D2H of batch i-1 run on their own streams
+        and overlap the forward of batch i (double-buffered device inputs and
+        outputs); returns after every output has landed in host memory.
+        """
+        torch = _require_cuda()
+        if not inputs:
+            return
+        dev = self.device
+        s_in, s_cmp, s_out = (torch.cuda.Stream(device=dev) for _ in range(3))
+        d_in = [tuple(torch.empty_like(t, device=dev) for t in inputs[0]) for _ in range(2)]
+        d_out = [tuple(torch.empty_like(t, device=dev) for t in outputs[0]) for _ in range(2)]
+        ws = self.workspace(cfg, inputs[0][0].shape[0])
+        ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "cmp", "out")}
+        started = [False, False]
+        for i, (src, dst) in enumerate(zip(inputs, outputs)):
+            b = i & 1
+            with torch.cuda.stream(s_in):
+                if started[b]:
+                    s_in.wait_event(ev["cmp"][b])          # forward i-2 done reading d_in[b]
+                for d, h in zip(d_in[b], src):
+                    d.copy_(h, non_blocking=True)
+                ev["in"][b].record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ev["in"][b])
+                if started[b]:
+                    s_cmp.wait_event(ev["out"][b])         # D2H i-2 done reading d_out[b]
+                y, pil, nf, mods = d_in[b]
+                self.forward_device(cfg, y, pil, nf, mods, num_iterations, d_out[b][0], d_out[b][1],
+                                    workspace=ws, stream=s_cmp)
+                ev["cmp"][b].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev["cmp"][b])
+                for h, d in zip(dst, d_out[b]):
+                    h.copy_(d, non_blocking=True)
+                ev["out"][b].record(s_out)
+            started[b] = True
+        s_out.synchronize()
+
     # -- numpy entry with the reference's semantics ------------------------------
 
     def _staging(self, key, shape, dtype, pinned):
