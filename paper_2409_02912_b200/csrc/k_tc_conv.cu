@@ -53,7 +53,10 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int NP, int MODE>
+// KS > 0 selects the fully unrolled MMA issue for kernel size KS with NK0 /
+// NK1 K=16 steps per tap from source 0 / 1 (host picks it when the layer
+// matches); KS = 0 is the generic runtime-loop version.
+template <int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0>
 __global__ void __launch_bounds__(CONV_THREADS, 1)
     k_conv_tc(const __grid_constant__ ConvTcParams p, const __grid_constant__ CUtensorMap map0,
               const __grid_constant__ CUtensorMap map1) {
@@ -92,6 +95,9 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
   const int R = p.rbox;
+#ifdef NRX_TIMING
+  long long t_a = 0, t_b = 0, t_c = 0, t_all = clock64();
+#endif
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -104,7 +110,9 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
       while (w.next(slab, tile)) {
         const int grp0 = (tile * NRX_TILE_M - p.hup) / 16;  // 16-row groups
         for (int src = 0; src < (p.c1 ? 2 : 1); ++src) {
+          NRX_T(t0);
           mbar_wait(&empty[st], ph ^ 1);
+          NRX_TADD(t_a, t0);
           mbar_expect_tx(&full[st], (uint32_t)(src ? p.c1 : p.c0) * R * 2);
           tma_load_4d(As + (size_t)st * p.abytes, src ? &map1 : &map0, &full[st], 0, grp0, 0, slab);
           if (++st == p.stages) { st = 0; ph ^= 1; }
@@ -118,6 +126,13 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
     const uint64_t a_desc0 = smem_desc(0, (uint32_t)R * 16, 128);
     const uint64_t b_desc0 = smem_desc(smem_u32(Ws), NP * 16, 128);
     const uint32_t a_kstep = 2 * R, b_kstep = 2 * NP;  // one K=16 step
+    int shifts[KS > 0 ? KS * KS : 1];                   // tap row offsets (16-B units)
+    if constexpr (KS > 0) {
+#pragma unroll
+      for (int ta = 0; ta < KS; ++ta)
+#pragma unroll
+        for (int tb = 0; tb < KS; ++tb) shifts[ta * KS + tb] = (ta - KS / 2) * g.Tp + (tb - KS / 2);
+    }
     mbar_wait(wbar, 0);
     tc_fence_after();
     WorkIter w(g, g.NU, g.tiles, p.n_io, p.mod_order);
@@ -126,31 +141,62 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
     while (w.next(slab, tile)) {
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
+      NRX_T(t0);
       mbar_wait(&tempty[acc], aph ^ 1);
+      NRX_TADD(t_a, t0);
       tc_fence_after();
       const uint32_t d = tmem_base + acc * NP;
-      for (int src = 0; src < (p.c1 ? 2 : 1); ++src) {
-        mbar_wait(&full[st], ph);
-        tc_fence_after();
-        const uint32_t a_stage = (smem_u32(As + (size_t)st * p.abytes) >> 4) + p.hup;
-        const int kc0 = src ? p.c0 / 8 : 0, nks = (src ? p.c1 : p.c0) / 16;
-        uint32_t b_tap = (uint32_t)kc0 * NP;
-        for (int ta = 0; ta < g.ks; ++ta) {
-          for (int tb = 0; tb < g.ks; ++tb) {
-            uint64_t ad = a_desc0 + (a_stage + (ta - g.r) * g.Tp + (tb - g.r));  // row-shifted view
-            uint64_t bd = b_desc0 + b_tap;
-            const uint32_t first = (src | ta | tb) == 0;
-#pragma unroll 4
-            for (int ks = 0; ks < nks; ++ks) {
-              mma_bf16_warp(d, ad, bd, idesc, !(first && ks == 0));
-              ad += a_kstep;
-              bd += b_kstep;
+      if constexpr (KS > 0) {
+        // Specialised issue: taps and K steps fully unrolled with constant
+        // descriptor offsets (48 cycles per N=64 MMA, the shared-memory
+        // operand floor, vs 74 for the runtime loop; scripts/mma_bench_conv_loop.cu).
+#pragma unroll
+        for (int src = 0; src < (NK1 > 0 ? 2 : 1); ++src) {
+          NRX_T(t1);
+          mbar_wait(&full[st], ph);
+          NRX_TADD(t_b, t1);
+          tc_fence_after();
+          const uint64_t a_stage = a_desc0 + ((smem_u32(As + (size_t)st * p.abytes) >> 4) + p.hup);
+          constexpr int KCH = 2 * (NK0 + NK1);
+          const int nk = src ? NK1 : NK0, kc0 = src ? 2 * NK0 : 0;
+#pragma unroll
+          for (int tap = 0; tap < KS * KS; ++tap) {
+#pragma unroll
+            for (int k = 0; k < (NK0 > NK1 ? NK0 : NK1); ++k) {
+              if (k < nk)
+                mma_bf16_warp(d, a_stage + shifts[tap] + (uint32_t)(k * a_kstep),
+                              b_desc0 + (uint32_t)((tap * KCH + kc0 + 2 * k) * NP), idesc, (src | tap | k) != 0);
             }
-            b_tap += (uint32_t)kch * NP;
           }
+          mma_commit_warp(&empty[st]);
+          if (++st == p.stages) { st = 0; ph ^= 1; }
         }
-        mma_commit_warp(&empty[st]);
-        if (++st == p.stages) { st = 0; ph ^= 1; }
+      } else {
+        for (int src = 0; src < (p.c1 ? 2 : 1); ++src) {
+          NRX_T(t1);
+          mbar_wait(&full[st], ph);
+          NRX_TADD(t_b, t1);
+          tc_fence_after();
+          const uint32_t a_stage = (smem_u32(As + (size_t)st * p.abytes) >> 4) + p.hup;
+          const int kc0 = src ? p.c0 / 8 : 0, nks = (src ? p.c1 : p.c0) / 16;
+          uint32_t b_tap = (uint32_t)kc0 * NP;
+          for (int ta = 0; ta < g.ks; ++ta) {
+            for (int tb = 0; tb < g.ks; ++tb) {
+              uint64_t ad = a_desc0 + (a_stage + (ta - g.r) * g.Tp + (tb - g.r));  // row-shifted view
+              uint64_t bd = b_desc0 + b_tap;
+              const uint32_t first = (src | ta | tb) == 0;
+#pragma unroll 4
+              for (int ks = 0; ks < nks; ++ks) {
+                mma_bf16_warp(d, ad, bd, idesc, !(first && ks == 0));
+                ad += a_kstep;
+                bd += b_kstep;
+              }
+              b_tap += (uint32_t)kch * NP;
+            }
+          }
+          mma_commit_warp(&empty[st]);
+          if (++st == p.stages) { st = 0; ph ^= 1; }
+        }
       }
       mma_commit_warp(&tfull[acc]);
       ++it;
@@ -166,7 +212,10 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
     while (w.next(slab, tile)) {
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
+      NRX_T(t0);
       mbar_wait(&tfull[acc], aph);
+      NRX_TADD(t_a, t0);
+      NRX_T(t1);
       tc_fence_after();
       float v[NC];
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * NP + cbase;
@@ -231,9 +280,15 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
           store_chunk(chunk_ptr(p.dst, slab, nd, cc, row, g), o);
         }
       }
+      NRX_TADD(t_b, t1);
       ++it;
     }
   }
+#ifdef NRX_TIMING
+  if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 64))
+    printf("conv NP=%d mode=%d c0=%d c1=%d tid=%d all=%lld a=%lld b=%lld c=%lld\n", NP, MODE, p.c0, p.c1,
+           threadIdx.x, clock64() - t_all, t_a, t_b, t_c);
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -289,7 +344,15 @@ static int launch_conv(const Geom& g, const PackLayout& L, const ConvOff* offs, 
       {k_conv_tc<48, 0>, k_conv_tc<48, 1>, k_conv_tc<48, 2>},
       {k_conv_tc<64, 0>, k_conv_tc<64, 1>, k_conv_tc<64, 2>}};
   if (p.np % 16 || p.np < 16 || p.np > 64 || mode < 0 || mode > 2) return NRX_ERR_UNSUPPORTED;
-  const KFn fn = table[p.np / 16 - 1][mode];
+  KFn fn = table[p.np / 16 - 1][mode];
+  // fully unrolled issue for the 3x3 layers of d_s in (48, 64] (the RT / large models)
+  if (g.ks == 3 && p.np == 64) {
+    const int nk0 = c0 / 16, nk1 = c1 / 16;
+    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_tc<64, EPI_RELU, 3, 2, 0>;
+    if (mode == EPI_RELU && nk0 == 4 && nk1 == 4) fn = k_conv_tc<64, EPI_RELU, 3, 4, 4>;
+    if (mode == EPI_STATE_INIT && nk0 == 4 && nk1 == 0) fn = k_conv_tc<64, EPI_STATE_INIT, 3, 4, 0>;
+    if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0) fn = k_conv_tc<64, EPI_RESIDUAL, 3, 4, 0>;
+  }
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.NU * g.tiles;
   dim3 grid(total < num_sms() ? total : num_sms(), n_off);
