@@ -275,9 +275,9 @@ def run_ours(args):
     flops_launch = conv_update0_flops_per_slab_re() * B * U * S * T
     kavg = float(np.mean(kernel_ms)) / 1e3 if kernel_ms else float("nan")
     achieved = flops_launch / kavg / 1e12
-    if args.precision == "bf16":
+    if args.precision in ("bf16", "fp16"):  # same tcgen05 kind::f16 rate for both
         peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-        peak_note = f"bf16 dense, sustained ({peak_src})"
+        peak_note = f"bf16 dense, sustained ({peak_src}); fp16 runs at the same tensor rate"
     else:
         sm_mhz = peaks.get("sm_max_mhz", 1965.0)
         peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
@@ -404,7 +404,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--precision", choices=("bf16", "fp32"), default=os.environ.get("NRX_BENCH_PRECISION", "bf16"))
+    ap.add_argument("--precision", choices=("bf16", "fp16", "fp32"), default=os.environ.get("NRX_BENCH_PRECISION", "bf16"))
     ap.add_argument("--slots-per-step", type=int, default=32)
     ap.add_argument("--latency-runs", type=int, default=2000)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -61,8 +61,11 @@ typedef enum nrx_status {
 typedef enum nrx_variant { NRX_SINGLE = 0, NRX_MASKING = 1, NRX_VAR_IO = 2 } nrx_variant;
 
 typedef enum nrx_precision {
-  NRX_FP32 = 0,  /* fp32 SIMT arithmetic, parity mode (<=1e-5 rel. of ref) */
-  NRX_BF16 = 1   /* bf16 operands on tcgen05 tensor cores, fp32 accumulate */
+  NRX_FP32 = 0,  /* fp32 SIMT arithmetic, parity mode (<=1e-5 rel. of ref)   */
+  NRX_BF16 = 1,  /* bf16 operands on tcgen05 tensor cores, fp32 accumulate,
+                    fp32 residual state stream                               */
+  NRX_FP16 = 2   /* fp16 operands on tcgen05, fp32 accumulate, fp16 state
+                    (8x finer operand rounding than bf16, no fp32 stream)    */
 } nrx_precision;
 
 /* NrxConfig (nrx.py:37-89). io_orders: var_io -> io_modulations (sorted);

@@ -12,8 +12,8 @@ import os
 
 NRX_MAX_PILOT_SYMBOLS = 16
 NRX_MAX_IO = 4
-NRX_FP32, NRX_BF16 = 0, 1
-PRECISIONS = {"fp32": NRX_FP32, "bf16": NRX_BF16}
+NRX_FP32, NRX_BF16, NRX_FP16 = 0, 1, 2
+PRECISIONS = {"fp32": NRX_FP32, "bf16": NRX_BF16, "fp16": NRX_FP16}
 VARIANT_IDS = {"single": 0, "masking": 1, "var_io": 2}
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnrx_b200.so")

@@ -137,6 +137,8 @@ int launch_ls_feat(const Geom& g, const void* y, int y_c128, const void* pil, in
                    const float* noise, void* feats, cudaStream_t st) {
   if (g.prec == NRX_BF16)
     return launch_ls_feat_t(g, y, y_c128, pil, pil_c128, n_sets, noise, (__nv_bfloat16*)feats, st);
+  if (g.prec == NRX_FP16)
+    return launch_ls_feat_t(g, y, y_c128, pil, pil_c128, n_sets, noise, (__half*)feats, st);
   return launch_ls_feat_t(g, y, y_c128, pil, pil_c128, n_sets, noise, (float*)feats, st);
 }
 

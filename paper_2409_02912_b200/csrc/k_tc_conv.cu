@@ -35,8 +35,8 @@ struct ConvTcParams {
   const uint8_t* wbase;
   uint64_t w_off[NRX_MAX_IO], b_off[NRX_MAX_IO];
   const int32_t* mod_order;
-  __nv_bfloat16* dst;
-  float* dst32;         // fp32 master state (STATE_INIT / RESIDUAL), or null
+  void* dst;            // bf16 / fp16 output buffer (element type = kernel's ET)
+  float* dst32;         // fp32 master state (bf16 STATE_INIT / RESIDUAL), or null
 };
 
 // warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue (two warps per
@@ -56,12 +56,14 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 // KS > 0 selects the fully unrolled MMA issue for kernel size KS with NK0 /
 // NK1 K=16 steps per tap from source 0 / 1 (host picks it when the layer
 // matches); KS = 0 is the generic runtime-loop version.
-template <int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0>
+// ET = __nv_bfloat16 or __half: operand/activation element type.
+template <typename ET, int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0>
 __global__ void __launch_bounds__(CONV_THREADS, 1)
     k_conv_tc(const __grid_constant__ ConvTcParams p, const __grid_constant__ CUtensorMap map0,
               const __grid_constant__ CUtensorMap map1) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const Geom& g = p.g;
+  ET* const dst = static_cast<ET*>(p.dst);
   const int io = p.n_io > 1 ? blockIdx.y : 0;
   uint8_t* Ws = smem;
   uint8_t* As = smem + ((p.wbytes + 1023) & ~1023u);
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
       }
     }
   } else if (warp == 1) {  // ---------------- MMA issuer (whole warp, elect.sync issues)
-    constexpr uint32_t idesc = idesc_bf16(NRX_TILE_M, NP);
+    constexpr uint32_t idesc = idesc_f16kind<ET>(NRX_TILE_M, NP);
     const int kch = p.ktap / 8;  // 16-byte channel chunks per tap
     // descriptors with a zero start address; start fields are added in 16-B units
     const uint64_t a_desc0 = smem_desc(0, (uint32_t)R * 16, 128);
@@ -229,16 +231,28 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
       const int s = row / g.Tp, t = row - s * g.Tp;
       const bool valid = row < g.rows_data && t < g.T;
       float old[NC];
-      if (MODE == EPI_RESIDUAL) {  // fp32 residual stream: issue every load before use
+      if (MODE == EPI_RESIDUAL) {  // residual input: issue every load before use
+        if (p.dst32) {             // bf16 path: fp32 residual stream
 #pragma unroll
-        for (int c4 = 0; c4 < NC / 4; ++c4) {
-          const int cc = cbase / 4 + c4;
-          float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (valid && cc < n32) o = *reinterpret_cast<const float4*>(chunk_ptr(p.dst32, slab, n32, cc, row, g));
-          old[4 * c4 + 0] = o.x;
-          old[4 * c4 + 1] = o.y;
-          old[4 * c4 + 2] = o.z;
-          old[4 * c4 + 3] = o.w;
+          for (int c4 = 0; c4 < NC / 4; ++c4) {
+            const int cc = cbase / 4 + c4;
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid && cc < n32) o = *reinterpret_cast<const float4*>(chunk_ptr(p.dst32, slab, n32, cc, row, g));
+            old[4 * c4 + 0] = o.x;
+            old[4 * c4 + 1] = o.y;
+            old[4 * c4 + 2] = o.z;
+            old[4 * c4 + 3] = o.w;
+          }
+        } else {                   // fp16 path: the state buffer itself
+          uint4 raw[NC / 8];
+#pragma unroll
+          for (int c8 = 0; c8 < NC / 8; ++c8) {
+            const int cc = cbase / 8 + c8;
+            raw[c8] = (valid && cc < nd) ? *reinterpret_cast<const uint4*>(chunk_ptr(dst, slab, nd, cc, row, g))
+                                         : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+          for (int c8 = 0; c8 < NC / 8; ++c8) unpack_chunk(raw[c8], static_cast<const ET*>(nullptr), old + 8 * c8);
         }
       }
       float x[NC];
@@ -251,10 +265,12 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
         x[j] = (valid && c < g.d) ? y : 0.f;
       }
       if (MODE != EPI_RELU) {
+        if (p.dst32) {
 #pragma unroll
-        for (int c4 = 0; c4 < NC / 4; ++c4) {
-          const int cc = cbase / 4 + c4;
-          if (cc < n32) store_chunk(chunk_ptr(p.dst32, slab, n32, cc, row, g), x + 4 * c4);
+          for (int c4 = 0; c4 < NC / 4; ++c4) {
+            const int cc = cbase / 4 + c4;
+            if (cc < n32) store_chunk(chunk_ptr(p.dst32, slab, n32, cc, row, g), x + 4 * c4);
+          }
         }
         if (valid) {  // positional channels d, d+1 of the bf16 operand copy
           const float pdt = g.dt[t], pdf = pos_df(s, slab % g.U, g);
@@ -269,7 +285,7 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
 #pragma unroll
       for (int c8 = 0; c8 < NC / 8; ++c8) {
         const int cc = cbase / 8 + c8;
-        if (cc < nd) store_chunk(chunk_ptr(p.dst, slab, nd, cc, row, g), x + 8 * c8);
+        if (cc < nd) store_chunk(chunk_ptr(dst, slab, nd, cc, row, g), x + 8 * c8);
       }
       if (half == 1) {  // buffer channels beyond the accumulator: positional / zero only
         for (int cc = NP / 8; cc < nd; ++cc) {
@@ -277,7 +293,7 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e)
             o[e] = (valid && MODE != EPI_RELU) ? state_extra(8 * cc + e, s, t, slab % g.U, g) : 0.f;
-          store_chunk(chunk_ptr(p.dst, slab, nd, cc, row, g), o);
+          store_chunk(chunk_ptr(dst, slab, nd, cc, row, g), o);
         }
       }
       NRX_TADD(t_b, t1);
@@ -298,8 +314,29 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
 }
 
 
+using KFn = void (*)(const ConvTcParams, const CUtensorMap, const CUtensorMap);
+
+template <typename ET>
+static KFn select_conv(const Geom& g, int np, int mode, int c0, int c1) {
+  static const KFn table[4][3] = {
+      {k_conv_tc<ET, 16, 0>, k_conv_tc<ET, 16, 1>, k_conv_tc<ET, 16, 2>},
+      {k_conv_tc<ET, 32, 0>, k_conv_tc<ET, 32, 1>, k_conv_tc<ET, 32, 2>},
+      {k_conv_tc<ET, 48, 0>, k_conv_tc<ET, 48, 1>, k_conv_tc<ET, 48, 2>},
+      {k_conv_tc<ET, 64, 0>, k_conv_tc<ET, 64, 1>, k_conv_tc<ET, 64, 2>}};
+  KFn fn = table[np / 16 - 1][mode];
+  // fully unrolled issue for the 3x3 layers of d_s in (48, 64] (the RT / large models)
+  if (g.ks == 3 && np == 64) {
+    const int nk0 = c0 / 16, nk1 = c1 / 16;
+    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_tc<ET, 64, EPI_RELU, 3, 2, 0>;
+    if (mode == EPI_RELU && nk0 == 4 && nk1 == 4) fn = k_conv_tc<ET, 64, EPI_RELU, 3, 4, 4>;
+    if (mode == EPI_STATE_INIT && nk0 == 4 && nk1 == 0) fn = k_conv_tc<ET, 64, EPI_STATE_INIT, 3, 4, 0>;
+    if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0) fn = k_conv_tc<ET, 64, EPI_RESIDUAL, 3, 4, 0>;
+  }
+  return fn;
+}
+
 static int launch_conv(const Geom& g, const PackLayout& L, const ConvOff* offs, int n_off, const void* src0,
-                       int c0, const void* src1, int c1, __nv_bfloat16* dst, int cdst, float* dst32, int mode,
+                       int c0, const void* src1, int c1, void* dst, int cdst, float* dst32, int mode,
                        const uint8_t* wb, const int32_t* mod_order, cudaStream_t st) {
   ConvTcParams p{};
   p.g = g;
@@ -337,22 +374,9 @@ static int launch_conv(const Geom& g, const PackLayout& L, const ConvOff* offs, 
   if (rc) return rc;
   rc = make_map(&m1, src1 ? src1 : src0, g, c1 ? c1 : c0, p.rbox);
   if (rc) return rc;
-  using KFn = void (*)(const ConvTcParams, const CUtensorMap, const CUtensorMap);
-  static const KFn table[4][3] = {
-      {k_conv_tc<16, 0>, k_conv_tc<16, 1>, k_conv_tc<16, 2>},
-      {k_conv_tc<32, 0>, k_conv_tc<32, 1>, k_conv_tc<32, 2>},
-      {k_conv_tc<48, 0>, k_conv_tc<48, 1>, k_conv_tc<48, 2>},
-      {k_conv_tc<64, 0>, k_conv_tc<64, 1>, k_conv_tc<64, 2>}};
   if (p.np % 16 || p.np < 16 || p.np > 64 || mode < 0 || mode > 2) return NRX_ERR_UNSUPPORTED;
-  KFn fn = table[p.np / 16 - 1][mode];
-  // fully unrolled issue for the 3x3 layers of d_s in (48, 64] (the RT / large models)
-  if (g.ks == 3 && p.np == 64) {
-    const int nk0 = c0 / 16, nk1 = c1 / 16;
-    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_tc<64, EPI_RELU, 3, 2, 0>;
-    if (mode == EPI_RELU && nk0 == 4 && nk1 == 4) fn = k_conv_tc<64, EPI_RELU, 3, 4, 4>;
-    if (mode == EPI_STATE_INIT && nk0 == 4 && nk1 == 0) fn = k_conv_tc<64, EPI_STATE_INIT, 3, 4, 0>;
-    if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0) fn = k_conv_tc<64, EPI_RESIDUAL, 3, 4, 0>;
-  }
+  const KFn fn = g.prec == NRX_FP16 ? select_conv<__half>(g, p.np, mode, c0, c1)
+                                    : select_conv<__nv_bfloat16>(g, p.np, mode, c0, c1);
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.NU * g.tiles;
   dim3 grid(total < num_sms() ? total : num_sms(), n_off);
@@ -369,20 +393,21 @@ static int launch_conv(const Geom& g, const PackLayout& L, const ConvOff* offs, 
     if (_s != NRX_OK) return _s; \
   } while (0)
 
-int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const __nv_bfloat16* state,
-               __nv_bfloat16* agg, cudaStream_t st);
-int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const __nv_bfloat16* state,
+int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const void* state, void* agg,
+               cudaStream_t st);
+int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const void* state,
                    const int32_t* mod_order, float* llr, float2* chest, cudaStream_t st);
 
 int launch_forward_tc(const Geom& g, const PackLayout& L, const WsLayout& W, int n_it, const uint8_t* wb,
                       const int32_t* mod_order, uint8_t* ws, float* llr, float2* chest, cudaStream_t st) {
   using namespace tc;
   if (g.d > 64 || g.h > 128) return NRX_ERR_UNSUPPORTED;
-  auto* feats = reinterpret_cast<__nv_bfloat16*>(ws + W.feats);
-  auto* h = reinterpret_cast<__nv_bfloat16*>(ws + W.h);
-  auto* state = reinterpret_cast<__nv_bfloat16*>(ws + W.state);
-  auto* agg = reinterpret_cast<__nv_bfloat16*>(ws + W.agg);
-  auto* state32 = reinterpret_cast<float*>(ws + W.state32);
+  void* feats = ws + W.feats;
+  void* h = ws + W.h;
+  void* state = ws + W.state;
+  void* agg = ws + W.agg;
+  // bf16 keeps an fp32 copy of the residual state stream; fp16 updates the state in place
+  float* state32 = g.prec == NRX_BF16 ? reinterpret_cast<float*>(ws + W.state32) : nullptr;
   {
     ProfScope ps(KID_INIT0, st);
     NRX_TRY_TC(launch_conv(g, L, L.init0, g.n_io, feats, g.Cf, nullptr, 0, h, g.Ch, nullptr, EPI_RELU, wb,

@@ -38,7 +38,7 @@ struct MlpTcParams {
   const uint8_t* wbase;
   uint64_t w0[NRX_MAX_IO], b0[NRX_MAX_IO], w1[NRX_MAX_IO], b1[NRX_MAX_IO];
   const int32_t* mod_order;
-  __nv_bfloat16* agg;      // message MLP output
+  void* agg;               // message MLP output (bf16 / fp16 = kernel's ET)
   float* llr;              // readout outputs
   float2* chest;
 };
@@ -98,7 +98,7 @@ __device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int 
 
 // Producer / MMA / hidden-epilogue roles are identical for both MLPs; the
 // output epilogue is passed in as a functor.
-template <int HW, typename OutEpilogue>
+template <typename ET, int HW, typename OutEpilogue>
 __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int io, const CUtensorMap* amap,
                                          OutEpilogue&& out_epi) {
   const Geom& g = p.g;
@@ -131,7 +131,7 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
     }
   } else if (warp == 1) {  // MMA issuer: whole warp, elect.sync issues
     {
-      const uint32_t id0 = idesc_bf16(NRX_TILE_M, p.hp), id1 = idesc_bf16(NRX_TILE_M, p.op);
+      const uint32_t id0 = idesc_f16kind<ET>(NRX_TILE_M, p.hp), id1 = idesc_f16kind<ET>(NRX_TILE_M, p.op);
       const uint32_t w0s = smem_u32(s.W0), w1s = smem_u32(s.W1);
       mbar_wait(s.wbar, 0);
       tc_fence_after();
@@ -226,7 +226,7 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
             float o[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) o[e] = fmaxf(v[8 * c8 + e] + s.sb0[c32 + 8 * c8 + e], 0.f);
-            store_chunk(reinterpret_cast<__nv_bfloat16*>(H + ((size_t)(c32 / 8 + c8) * NRX_TILE_M + r) * 16), o);
+            store_chunk(reinterpret_cast<ET*>(H + ((size_t)(c32 / 8 + c8) * NRX_TILE_M + r) * 16), o);
           }
         }
         fence_proxy_async();  // generic-proxy smem writes -> tensor-core reads
@@ -265,6 +265,7 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
   }
 }
 
+template <typename ET>
 __global__ void __launch_bounds__(mlp_threads(MSG_HW), 1)
     k_msg_tc(const __grid_constant__ MlpTcParams p, const __grid_constant__ CUtensorMap smap) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -273,7 +274,8 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW), 1)
   const Geom& g = p.g;
   const int U = p.uses_per_item;
   const int nca = g.Ca / 8;
-  mlp_body<MSG_HW>(p, s, 0, &smap, [&](int n, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
+  ET* const agg = static_cast<ET*>(p.agg);
+  mlp_body<ET, MSG_HW>(p, s, 0, &smap, [&](int n, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
     const int row = tile * NRX_TILE_M + r;
     const int srow = row / g.Tp, t = row - srow * g.Tp;
     const bool valid = row < g.rows_data && t < g.T;
@@ -314,13 +316,14 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW), 1)
             const int c = 8 * c8 + e;
             o[e] = (valid && c < g.d) ? a : 0.f;
           }
-          store_chunk(chunk_ptr(p.agg, n * U + u, nca, c8, row, g), o);
+          store_chunk(chunk_ptr(agg, n * U + u, nca, c8, row, g), o);
         }
       }
     }
   });
 }
 
+template <typename ET>
 __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
     k_readout_tc(const __grid_constant__ MlpTcParams p, const __grid_constant__ CUtensorMap smap) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
   const int io = p.n_io > 1 ? blockIdx.y : 0;
   mlp_setup(p, s, io, 32 * READOUT_HW);
   const Geom& g = p.g;
-  mlp_body<READOUT_HW>(p, s, io, &smap, [&](int slab, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
+  mlp_body<ET, READOUT_HW>(p, s, io, &smap, [&](int slab, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
     float o[32];
     tmem_ld16(taddr, o);
     tmem_ld16(taddr + 16, o + 16);
@@ -394,8 +397,8 @@ static int mlp_common(MlpTcParams& p, const Geom& g, int hp, int op, int uses, i
   return *smem > SMEM_LIMIT ? NRX_ERR_UNSUPPORTED : NRX_OK;
 }
 
-int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const __nv_bfloat16* state,
-               __nv_bfloat16* agg, cudaStream_t st) {
+int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const void* state, void* agg,
+               cudaStream_t st) {
   if (g.U > MSG_MAXU) return NRX_ERR_UNSUPPORTED;
   MlpTcParams p{};
   size_t smem = 0;
@@ -411,15 +414,16 @@ int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const __nv
   CUtensorMap m;
   rc = make_map(&m, state, g, g.Cs, NRX_TILE_M);
   if (rc) return rc;
-  if (set_smem((const void*)k_msg_tc, SMEM_LIMIT)) return NRX_ERR_CUDA;
+  const auto fn = g.prec == NRX_FP16 ? k_msg_tc<__half> : k_msg_tc<__nv_bfloat16>;
+  if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.N * g.tiles;
   const int per_sm = (512 / p.tmem_cols) < 2 || 2 * smem > SMEM_LIMIT ? 1 : 2;
   const int cap = num_sms() * per_sm;
-  k_msg_tc<<<total < cap ? total : cap, mlp_threads(MSG_HW), smem, st>>>(p, m);
+  fn<<<total < cap ? total : cap, mlp_threads(MSG_HW), smem, st>>>(p, m);
   return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
 }
 
-int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const __nv_bfloat16* state,
+int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const void* state,
                    const int32_t* mod_order, float* llr, float2* chest, cudaStream_t st) {
   MlpTcParams p{};
   size_t smem = 0;
@@ -439,12 +443,13 @@ int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const 
   CUtensorMap m;
   rc = make_map(&m, state, g, g.Cs, NRX_TILE_M);
   if (rc) return rc;
-  if (set_smem((const void*)k_readout_tc, SMEM_LIMIT)) return NRX_ERR_CUDA;
+  const auto fn = g.prec == NRX_FP16 ? k_readout_tc<__half> : k_readout_tc<__nv_bfloat16>;
+  if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.NU * g.tiles;
   const int per_sm = (512 / p.tmem_cols) < 2 || 2 * smem > SMEM_LIMIT ? 1 : 2;
   const int cap = num_sms() * per_sm;
   dim3 grid(total < cap ? total : cap, g.n_io);
-  k_readout_tc<<<grid, mlp_threads(READOUT_HW), smem, st>>>(p, m);
+  fn<<<grid, mlp_threads(READOUT_HW), smem, st>>>(p, m);
   return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
 }
 

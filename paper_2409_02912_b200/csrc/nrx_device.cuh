@@ -1,6 +1,7 @@
 // Device helpers shared by all kernels.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "nrx_internal.h"
@@ -64,6 +65,38 @@ __device__ __forceinline__ void store_chunk(__nv_bfloat16* p, const float* v) {
   q.z = pack_bf16x2(v[4], v[5]);
   q.w = pack_bf16x2(v[6], v[7]);
   *reinterpret_cast<uint4*>(p) = q;
+}
+
+__device__ __forceinline__ void store_chunk(__half* p, const float* v) {
+  uint4 q;
+  __half2 h0 = __floats2half2_rn(v[0], v[1]), h1 = __floats2half2_rn(v[2], v[3]);
+  __half2 h2 = __floats2half2_rn(v[4], v[5]), h3 = __floats2half2_rn(v[6], v[7]);
+  q.x = *reinterpret_cast<uint32_t*>(&h0);
+  q.y = *reinterpret_cast<uint32_t*>(&h1);
+  q.z = *reinterpret_cast<uint32_t*>(&h2);
+  q.w = *reinterpret_cast<uint32_t*>(&h3);
+  *reinterpret_cast<uint4*>(p) = q;
+}
+
+// Unpack one 16-byte chunk of 8 half-precision channels (type tag selects
+// bf16 or fp16) into floats.
+__device__ __forceinline__ void unpack_chunk(uint4 q, const __nv_bfloat16*, float* v) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = unpack_bf16x2(w[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void unpack_chunk(uint4 q, const __half*, float* v) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
 }
 
 __device__ __forceinline__ int io_index(const int32_t* mod_order, int slab, const Geom& g) {

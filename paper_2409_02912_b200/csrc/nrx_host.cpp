@@ -84,13 +84,13 @@ int validate(const nrx_model_desc* m, const nrx_slot_desc* s) {
   return NRX_OK;
 }
 
-int quantum(int prec) { return prec == NRX_BF16 ? 16 : 4; }
+int quantum(int prec) { return prec == NRX_FP32 ? 4 : 16; }
 
 int make_geom(const nrx_model_desc* m, const nrx_slot_desc* s, int n_slots, int prec, Geom* g) {
   int st = validate(m, s);
   if (st) return st;
   if (n_slots < 1) return NRX_ERR_INVALID;
-  if (prec != NRX_FP32 && prec != NRX_BF16) return NRX_ERR_INVALID;
+  if (prec != NRX_FP32 && prec != NRX_BF16 && prec != NRX_FP16) return NRX_ERR_INVALID;
   std::memset(g, 0, sizeof(*g));
   g->N = n_slots;
   g->U = s->num_ues;
@@ -111,7 +111,7 @@ int make_geom(const nrx_model_desc* m, const nrx_slot_desc* s, int n_slots, int 
   g->d = m->d_s;
   g->h = m->hidden;
   g->prec = prec;
-  g->cw = prec == NRX_BF16 ? 8 : 4;
+  g->cw = prec == NRX_FP32 ? 4 : 8;
   const int q = quantum(prec);
   g->Cin = input_channels(m);
   g->Cf = rup(g->Cin, q);
@@ -171,7 +171,7 @@ void pack_layout(const nrx_model_desc* m, int prec, PackLayout* L) {
   L->dmax = dmax;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
-  if (prec == NRX_BF16) {
+  if (prec != NRX_FP32) {  // bf16 / fp16 tensor-core operands
     const int np = rup(m->d_s, 16), hp = rup(m->hidden, 16);
     auto conv = [&](ConvOff& c, int ktap) {
       c.ktap = ktap;
@@ -274,17 +274,27 @@ uint16_t f32_to_bf16(float f) {
   return (uint16_t)(x >> 16);
 }
 
-// B operand writer: element (n, k) of a [N][K] K-major matrix.
+uint16_t f32_to_f16(float f) {  // IEEE binary16, round to nearest even (GCC _Float16)
+  const _Float16 h = (_Float16)f;
+  uint16_t bits;
+  std::memcpy(&bits, &h, 2);
+  return bits;
+}
+
+// B operand writer: element (n, k) of a [N][K] K-major matrix, bf16 or fp16.
 struct BOperand {
   uint16_t* p;
   int N;
-  void set(int n, int k, float v) { p[((size_t)(k / 8) * N + n) * 8 + (k % 8)] = f32_to_bf16(v); }
+  bool f16;
+  void set(int n, int k, float v) {
+    p[((size_t)(k / 8) * N + n) * 8 + (k % 8)] = f16 ? f32_to_f16(v) : f32_to_bf16(v);
+  }
 };
 
 void pack_conv_bf16(const Geom& g, int k, const ConvOff& c, int cin_ref, const float* w, const float* b,
                     ChanMap map, uint8_t* base) {
   const int np = rup(g.d, 16), taps = k * k, cout = g.d;
-  BOperand B{(uint16_t*)(base + c.w), np};
+  BOperand B{(uint16_t*)(base + c.w), np, g.prec == NRX_FP16};
   for (int tap = 0; tap < taps; ++tap)
     for (int j = 0; j < c.ktap; ++j) {
       const int src = map(j, g);
@@ -297,15 +307,16 @@ void pack_conv_bf16(const Geom& g, int k, const ConvOff& c, int cin_ref, const f
 
 }  // namespace
 
-int pack_weights_bf16(const nrx_model_desc* m, const float* const* t, uint8_t* base) {
+int pack_weights_tc(const nrx_model_desc* m, int prec, const float* const* t, uint8_t* base) {
   PackLayout L;
-  pack_layout(m, NRX_BF16, &L);
+  pack_layout(m, prec, &L);
   std::memset(base, 0, L.total);
   Geom g;
   nrx_slot_desc s{};
   s.num_subcarriers = 64; s.num_symbols = 14; s.num_ues = 1; s.comb_size = 1;
   s.num_pilot_symbols = 1;
-  make_geom(m, &s, 1, NRX_BF16, &g);
+  make_geom(m, &s, 1, prec, &g);
+  const bool f16 = prec == NRX_FP16;
   const int k = m->kernel_size, d = m->d_s, h = m->hidden, B2 = 2 * m->num_rx_ant;
   const int np = rup(d, 16), hp = rup(h, 16);
   // indices of the shared tensors in the canonical order (include/nrx_b200.h)
@@ -319,7 +330,7 @@ int pack_weights_bf16(const nrx_model_desc* m, const float* const* t, uint8_t* b
     const int width = llr_width_of(m, io);
     const float *lw0 = t[i + 4], *lb0 = t[i + 5], *lw1 = t[i + 6], *lb1 = t[i + 7];
     const float *cw0 = t[i_chest], *cb0 = t[i_chest + 1], *cw1 = t[i_chest + 2], *cb1 = t[i_chest + 3];
-    BOperand W0{(uint16_t*)(base + o.w0), 2 * hp};
+    BOperand W0{(uint16_t*)(base + o.w0), 2 * hp, f16};
     float* b0 = (float*)(base + o.b0);
     for (int n = 0; n < 2 * hp; ++n) {
       const bool chest = n >= hp;
@@ -328,7 +339,7 @@ int pack_weights_bf16(const nrx_model_desc* m, const float* const* t, uint8_t* b
         W0.set(n, kk, (kk < d && nn < h) ? (chest ? cw0 : lw0)[(size_t)kk * h + nn] : 0.f);
       b0[n] = nn < h ? (chest ? cb0 : lb0)[nn] : 0.f;
     }
-    BOperand W1{(uint16_t*)(base + o.w1), 32};
+    BOperand W1{(uint16_t*)(base + o.w1), 32, f16};
     float* b1 = (float*)(base + o.b1);
     for (int n = 0; n < 32; ++n) {
       for (int kk = 0; kk < 2 * hp; ++kk) {
@@ -342,13 +353,13 @@ int pack_weights_bf16(const nrx_model_desc* m, const float* const* t, uint8_t* b
   }
   {
     const float *w0 = t[i_msg], *b0 = t[i_msg + 1], *w1 = t[i_msg + 2], *b1 = t[i_msg + 3];
-    BOperand W0{(uint16_t*)(base + L.msg.w0), hp};
+    BOperand W0{(uint16_t*)(base + L.msg.w0), hp, f16};
     float* pb0 = (float*)(base + L.msg.b0);
     for (int n = 0; n < hp; ++n) {
       for (int kk = 0; kk < g.Cs; ++kk) W0.set(n, kk, (kk < d && n < h) ? w0[(size_t)kk * h + n] : 0.f);
       pb0[n] = n < h ? b0[n] : 0.f;
     }
-    BOperand W1{(uint16_t*)(base + L.msg.w1), np};
+    BOperand W1{(uint16_t*)(base + L.msg.w1), np, f16};
     float* pb1 = (float*)(base + L.msg.b1);
     for (int n = 0; n < np; ++n) {
       for (int kk = 0; kk < hp; ++kk) W1.set(n, kk, (kk < h && n < d) ? w1[(size_t)kk * d + n] : 0.f);
@@ -387,7 +398,7 @@ int pack_weights_f32(const nrx_model_desc* m, const float* const* t, uint8_t* ba
 }
 
 void ws_layout(const Geom& g, WsLayout* w) {
-  const size_t esz = g.prec == NRX_BF16 ? 2 : 4;
+  const size_t esz = g.prec == NRX_FP32 ? 4 : 2;
   const size_t plane = (size_t)g.NU * g.rows_slab * esz;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
@@ -456,9 +467,9 @@ int nrx_pack_weights(const nrx_model_desc* m, int prec, const float* const* tens
   for (int i = 0; i < n; ++i)
     if (!tensors[i]) return NRX_ERR_INVALID;
   if (prec == NRX_FP32) return pack_weights_f32(m, tensors, (uint8_t*)out);
-  if (prec == NRX_BF16) {
+  if (prec == NRX_BF16 || prec == NRX_FP16) {
     if (m->hidden > 128) return NRX_ERR_UNSUPPORTED;
-    return pack_weights_bf16(m, tensors, (uint8_t*)out);
+    return pack_weights_tc(m, prec, tensors, (uint8_t*)out);
   }
   return NRX_ERR_INVALID;
 }

@@ -5,6 +5,7 @@
 
 #include <cstdio>
 #include <mutex>
+#include <type_traits>
 
 #include "nrx_device.cuh"
 #include "nrx_kernels.h"
@@ -161,6 +162,13 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
 }
 
 // kind::f16 instruction descriptor: fp32 accumulate, bf16 A/B, K-major A/B.
+// Same for fp16 or bf16 operands by element type (A/B format 0 = F16, 1 = BF16).
+template <typename ET>
+__host__ __device__ constexpr uint32_t idesc_f16kind(int M, int N) {
+  constexpr uint32_t fmt = std::is_same<ET, __half>::value ? 0u : 1u;
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
          (static_cast<uint32_t>(M >> 4) << 24);
