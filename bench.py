@@ -218,6 +218,7 @@ def run_ours(args):
     import torch.distributed as dist
     from paper_2409_02912_b200 import _lib
     from paper_2409_02912_b200.engine import NrxEngine
+    from paper_2409_02912_b200.shard import max_over_ranks
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -290,7 +291,36 @@ def run_ours(args):
     # end to end through the public host API: pinned H2D + D2H inside the region
     e2e = e2e_throughput(eng, cfg, B, max(4, args.steps // 2), world, dev)
 
-    n_launch = eng.launch_count(N_IT)
+    # the other precisions on the same device-resident workload (shorter runs)
+    by_prec = {args.precision: {"slots_per_s": round(value, 2), "ms_per_step": round(ms_per_step, 4)}}
+    if not args.no_precision_sweep:
+        for prec in ("fp32", "bf16", "fp16"):
+            if prec == args.precision:
+                continue
+            other = NrxEngine(config, w, precision=prec, device=dev)
+            ows = other.workspace(cfg, B)
+
+            def ostep(i, other=other, ows=ows):
+                y, pil, nf, mods = sets[i & 1]
+                other.forward_device(cfg, y, pil, nf, mods, N_IT, llr, chest, workspace=ows, stream=stream)
+
+            n_steps = max(3, args.steps // (10 if prec == "fp32" else 4))
+            for i in range(3):
+                ostep(i)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for i in range(n_steps):
+                ostep(i)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = max_over_ranks(a.elapsed_time(b) / 1e3, dev)
+            by_prec[prec] = {"slots_per_s": round(B * n_steps * world / t, 2),
+                             "ms_per_step": round(t / n_steps * 1e3, 4), "steps": n_steps}
+            del other, ows
+            torch.cuda.empty_cache()
+
+    n_launch = eng.launch_count(cfg, N_IT)
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "slots/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
@@ -312,6 +342,7 @@ def run_ours(args):
                      "share_of_step": round(kavg * 1e3 * N_IT / ms_per_step, 4) if kernel_ms else None},
         "whole_path": {"algorithmic_tflops": round(algorithmic_flops_per_slab_re() * U * S * T * value / world / 1e12, 2),
                        "flop_per_slot": algorithmic_flops_per_slab_re() * U * S * T},
+        "by_precision": by_prec,
         "gpu_launches": n_launch * args.steps,
         "launches_per_step": n_launch,
         "clocks": sampler.summary(),
@@ -404,10 +435,12 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--precision", choices=("bf16", "fp16", "fp32"), default=os.environ.get("NRX_BENCH_PRECISION", "bf16"))
+    ap.add_argument("--precision", choices=("bf16", "fp16", "fp32"), default=os.environ.get("NRX_BENCH_PRECISION", "fp16"))
     ap.add_argument("--slots-per-step", type=int, default=32)
     ap.add_argument("--latency-runs", type=int, default=2000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-precision-sweep", action="store_true",
+                    help="skip timing the other precisions (by_precision)")
     ap.add_argument("--cpu-json", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -177,7 +177,8 @@ void nrx_profile_disable(void);
 const char* nrx_kernel_name(int kernel_id);
 
 /* Number of kernel launches one nrx_forward call enqueues. */
-int nrx_forward_launch_count(const nrx_model_desc* model, int precision, int num_iterations);
+int nrx_forward_launch_count(const nrx_model_desc* model, const nrx_slot_desc* slot, int precision,
+                             int num_iterations);
 
 #ifdef __cplusplus
 }

@@ -73,7 +73,7 @@ def load() -> ctypes.CDLL:
     lib.nrx_workspace_bytes.argtypes = [P(ModelDesc), P(SlotDesc), I, I]
     lib.nrx_workspace_bytes.restype = Z
     lib.nrx_forward.argtypes = [P(ModelDesc), P(SlotDesc), I, I, I, V, I, V, I, I, V, V, V, V, I, V, V, Z, V]
-    lib.nrx_forward_launch_count.argtypes = [P(ModelDesc), I, I]
+    lib.nrx_forward_launch_count.argtypes = [P(ModelDesc), P(SlotDesc), I, I]
     lib.nrx_buffer_geometry.argtypes = [P(ModelDesc), P(SlotDesc), I, P(ctypes.c_int32)]
     lib.nrx_ls_features.argtypes = [P(ModelDesc), P(SlotDesc), I, I, V, I, V, I, I, V, V, V]
     lib.nrx_profile_enable.argtypes = [ctypes.c_uint32, I]

@@ -1,29 +1,39 @@
-// bf16 tensor-core convolution (NRX_BF16 path) and the launch sequence of
-// the tensor-core forward pass.
+// Tensor-core (bf16 / fp16) convolution with an optional fused per-RE MLP
+// tail, and the launch sequence of the tensor-core forward pass.
 //
 //  k_conv_tc     k x k 'same' convolution as an implicit GEMM on the
 //                row-linearised grid (nrx_internal.h).  Per 128-row M tile the
 //                producer warp TMA-loads the tile plus +-H halo rows of every
 //                input channel chunk ONCE per input source (4-D box
-//                {8, 128+2H, C/8, 1}, zero filled outside the slab); tap (a,b)
+//                {128, rows/16, C/8, 1}, zero filled outside the slab); tap (a,b)
 //                is the same shared-memory tile viewed at a row offset
 //                (a-r)*Tp + (b-r), which the no-swizzle K-major UMMA descriptor
 //                addresses directly (16-byte granular start address).  The whole
 //                layer's weights stay resident in shared memory (bulk copy once
-//                per CTA).  One thread issues taps * C/16 MMAs (M=128,
+//                per CTA).  The MMA warp issues taps * C/16 MMAs (M=128,
 //                N=rup(d,16), K=16) into one of two TMEM accumulators; eight
 //                epilogue warps drain the other (tcgen05.ld) and apply bias /
-//                ReLU / positional channels / fp32 residual while the next
-//                tile's MMAs run.
+//                ReLU / positional channels / residual while the next tile's
+//                MMAs run.
+//
+//  Fused MLP tail (conv1 of the state init and of the iteration block):
+//  the epilogue also writes the fresh state tile into shared memory as the A
+//  operand of a two-layer per-RE MLP that runs on the same tensor core
+//  between the next tile's conv MMAs:
+//    TAIL_MSG      the message MLP of the next iteration (nrx.py:258); for
+//                  U = 2 the sum of the other UE's messages is exactly that
+//                  UE's message, so the next update conv reads the partner
+//                  slab's messages directly (source-1 slab ^ 1) and the
+//                  separate message kernel disappears;
+//    TAIL_READOUT  the fused LLR + chest readout after the last iteration
+//                  (nrx.py:338-340), writing the user-facing outputs.
 #include "nrx_profile.h"
 #include "tc_common.cuh"
 
 namespace nrx {
 namespace tc {
 
-// ---------------------------------------------------------------------------
-// K2/K3b/K3c: convolution
-// ---------------------------------------------------------------------------
+enum ConvTail { TAIL_NONE = 0, TAIL_MSG = 1, TAIL_READOUT = 2 };
 
 struct ConvTcParams {
   Geom g;
@@ -32,11 +42,19 @@ struct ConvTcParams {
   int n_io, d4;
   uint32_t wbytes, abytes, tmem_cols, rbox;
   int hup;              // halo rows loaded on each side (H rounded up to 16)
+  int src1_xor;         // source-1 slab = slab ^ src1_xor (1: partner UE's messages)
   const uint8_t* wbase;
   uint64_t w_off[NRX_MAX_IO], b_off[NRX_MAX_IO];
   const int32_t* mod_order;
   void* dst;            // bf16 / fp16 output buffer (element type = kernel's ET)
   float* dst32;         // fp32 master state (bf16 STATE_INIT / RESIDUAL), or null
+  // fused MLP tail
+  int thp, top;         // tail hidden (padded) / output columns
+  uint32_t tw0bytes, tw1bytes;
+  uint64_t tw0[NRX_MAX_IO], tb0[NRX_MAX_IO], tw1[NRX_MAX_IO], tb1[NRX_MAX_IO];
+  void* msg;            // TAIL_MSG output: [slab][Ca/8][rows][8] ET
+  float* llr;           // TAIL_READOUT outputs
+  float2* chest;
 };
 
 // warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue (two warps per
@@ -53,11 +71,47 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Shared-memory carve-up (identical on host and device).
+struct ConvSmem {
+  uint32_t w, a, tw0, tw1, ta, th, bars, tmem_ptr, sbias, tb0, tb1, total;
+};
+__host__ __device__ inline ConvSmem conv_smem_layout(const ConvTcParams& p, int tail) {
+  ConvSmem s;
+  uint32_t off = 0;
+  s.w = off;
+  off = (p.wbytes + 1023u) & ~1023u;
+  s.a = off;
+  off += p.stages * p.abytes;
+  s.tw0 = s.tw1 = s.ta = s.th = off;
+  if (tail) {  // tail weights, double-buffered state tile (A), single hidden tile (H)
+    s.tw0 = off;
+    off += p.tw0bytes;
+    s.tw1 = off;
+    off += p.tw1bytes;
+    s.ta = off;
+    off += 2u * p.g.Cs * NRX_TILE_M * 2;
+    s.th = off;
+    off += (uint32_t)p.thp * NRX_TILE_M * 2;
+  }
+  s.bars = off;
+  off += 32 * 8;
+  s.tmem_ptr = off;
+  off += 16;
+  s.sbias = off;
+  off += 64 * 4;
+  s.tb0 = off;
+  off += 256 * 4;
+  s.tb1 = off;
+  off += 64 * 4;
+  s.total = off;
+  return s;
+}
+
 // KS > 0 selects the fully unrolled MMA issue for kernel size KS with NK0 /
 // NK1 K=16 steps per tap from source 0 / 1 (host picks it when the layer
 // matches); KS = 0 is the generic runtime-loop version.
 // ET = __nv_bfloat16 or __half: operand/activation element type.
-template <typename ET, int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0>
+template <typename ET, int NP, int MODE, int TAIL, int KS = 0, int NK0 = 0, int NK1 = 0>
 __global__ void __launch_bounds__(CONV_THREADS, 1)
     k_conv_tc(const __grid_constant__ ConvTcParams p, const __grid_constant__ CUtensorMap map0,
               const __grid_constant__ CUtensorMap map1) {
@@ -65,16 +119,23 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
   const Geom& g = p.g;
   ET* const dst = static_cast<ET*>(p.dst);
   const int io = p.n_io > 1 ? blockIdx.y : 0;
-  uint8_t* Ws = smem;
-  uint8_t* As = smem + ((p.wbytes + 1023) & ~1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(As + (size_t)p.stages * p.abytes);
+  const ConvSmem L = conv_smem_layout(p, TAIL);
+  uint8_t* Ws = smem + L.w;
+  uint8_t* As = smem + L.a;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* full = bars;
   uint64_t* empty = bars + 8;
   uint64_t* tfull = bars + 16;
   uint64_t* tempty = bars + 18;
   uint64_t* wbar = bars + 20;
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 21);
-  float* sbias = reinterpret_cast<float*>(bars + 22);  // NP floats
+  uint64_t* ta_ready = bars + 21;   // [2] tail: state tile in shared memory
+  uint64_t* hid_full = bars + 23;   // [2] tail: fc0 done
+  uint64_t* h_ready = bars + 25;    // [2] tail: hidden layer in shared memory
+  uint64_t* tout_full = bars + 27;  // [2] tail: fc1 done
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L.tmem_ptr);
+  float* sbias = reinterpret_cast<float*>(smem + L.sbias);
+  float* stb0 = reinterpret_cast<float*>(smem + L.tb0);
+  float* stb1 = reinterpret_cast<float*>(smem + L.tb1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) tmem_alloc(tmem_ptr, p.tmem_cols);
@@ -88,14 +149,29 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
       mbar_init(&tempty[a], CONV_EPI_THREADS);
     }
     mbar_init(wbar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ta_ready[b], CONV_EPI_THREADS);
+      mbar_init(&hid_full[b], 1);
+      mbar_init(&h_ready[b], CONV_EPI_THREADS);
+      mbar_init(&tout_full[b], 1);
+    }
     fence_barrier_init();
   }
   if (threadIdx.x >= 64 && threadIdx.x < 64 + NP)
     sbias[threadIdx.x - 64] = reinterpret_cast<const float*>(p.wbase + p.b_off[io])[threadIdx.x - 64];
+  if (TAIL) {
+    const float* b0 = reinterpret_cast<const float*>(p.wbase + p.tb0[io]);
+    const float* b1 = reinterpret_cast<const float*>(p.wbase + p.tb1[io]);
+    for (int i = threadIdx.x; i < p.thp; i += blockDim.x) stb0[i] = b0[i];
+    for (int i = threadIdx.x; i < p.top; i += blockDim.x) stb1[i] = b1[i];
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
+  // tail TMEM regions (double buffered): hidden at col_h + b*thp, outputs at col_o + b*top
+  const uint32_t col_h = 2 * NP, col_o = 2 * NP + 2 * p.thp;
+  const uint32_t ta_bytes = (uint32_t)g.Cs * NRX_TILE_M * 2, th_bytes = (uint32_t)p.thp * NRX_TILE_M * 2;
   const int R = p.rbox;
 #ifdef NRX_TIMING
   long long t_a = 0, t_b = 0, t_c = 0, t_all = clock64();
@@ -103,7 +179,16 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
-      load_weights(Ws, p.wbase + p.w_off[io], p.wbytes, wbar);
+      const uint32_t tbytes = TAIL ? p.tw0bytes + p.tw1bytes : 0;
+      mbar_expect_tx(wbar, p.wbytes + tbytes);
+      for (uint32_t off = 0; off < p.wbytes; off += 32768u) {
+        const uint32_t n = p.wbytes - off < 32768u ? p.wbytes - off : 32768u;
+        bulk_load(Ws + off, p.wbase + p.w_off[io] + off, n, wbar);
+      }
+      if (TAIL) {
+        bulk_load(smem + L.tw0, p.wbase + p.tw0[io], p.tw0bytes, wbar);
+        bulk_load(smem + L.tw1, p.wbase + p.tw1[io], p.tw1bytes, wbar);
+      }
       // one pipeline stage per (tile, input source): finer-grained stages keep
       // more loads in flight next to the resident weights
       WorkIter w(g, g.NU, g.tiles, p.n_io, p.mod_order);
@@ -116,7 +201,8 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
           mbar_wait(&empty[st], ph ^ 1);
           NRX_TADD(t_a, t0);
           mbar_expect_tx(&full[st], (uint32_t)(src ? p.c1 : p.c0) * R * 2);
-          tma_load_4d(As + (size_t)st * p.abytes, src ? &map1 : &map0, &full[st], 0, grp0, 0, slab);
+          tma_load_4d(As + (size_t)st * p.abytes, src ? &map1 : &map0, &full[st], 0, grp0, 0,
+                      src ? (slab ^ p.src1_xor) : slab);
           if (++st == p.stages) { st = 0; ph ^= 1; }
         }
       }
@@ -135,6 +221,37 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
 #pragma unroll
         for (int tb = 0; tb < KS; ++tb) shifts[ta * KS + tb] = (ta - KS / 2) * g.Tp + (tb - KS / 2);
     }
+    // tail MLP, software-pipelined against the epilogue: in loop step i the MMA
+    // warp issues conv(i), fc0(i-1) (hidden = state_tile x W0, N = thp) and
+    // fc1(i-2) (out = relu-hidden x W1, N = top); buffers alternate by tile parity
+    auto issue_fc0 = [&](int j) {
+      const int b = j & 1;
+      const uint32_t id0 = idesc_f16kind<ET>(NRX_TILE_M, p.thp);
+      mbar_wait(&ta_ready[b], (j >> 1) & 1);
+      tc_fence_after();
+      uint64_t ad = smem_desc(smem_u32(smem + L.ta + b * ta_bytes), NRX_TILE_M * 16, 128);
+      uint64_t bd = smem_desc(smem_u32(smem + L.tw0), p.thp * 16, 128);
+      for (int kc = 0; kc < g.Cs / 8; kc += 2) {
+        mma_bf16_warp(tmem_base + col_h + b * p.thp, ad, bd, id0, kc != 0);
+        ad += 2 * NRX_TILE_M;
+        bd += 2 * p.thp;
+      }
+      mma_commit_warp(&hid_full[b]);
+    };
+    auto issue_fc1 = [&](int j) {
+      const int b = j & 1;
+      const uint32_t id1 = idesc_f16kind<ET>(NRX_TILE_M, p.top);
+      mbar_wait(&h_ready[b], (j >> 1) & 1);
+      tc_fence_after();
+      uint64_t ad = smem_desc(smem_u32(smem + L.th), NRX_TILE_M * 16, 128);
+      uint64_t bd = smem_desc(smem_u32(smem + L.tw1), p.top * 16, 128);
+      for (int kc = 0; kc < p.thp / 8; kc += 2) {
+        mma_bf16_warp(tmem_base + col_o + b * p.top, ad, bd, id1, kc != 0);
+        ad += 2 * NRX_TILE_M;
+        bd += 2 * p.top;
+      }
+      mma_commit_warp(&tout_full[b]);
+    };
     mbar_wait(wbar, 0);
     tc_fence_after();
     WorkIter w(g, g.NU, g.tiles, p.n_io, p.mod_order);
@@ -201,7 +318,15 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
         }
       }
       mma_commit_warp(&tfull[acc]);
+      // earlier tiles' MLP tails run while this tile's conv MMAs execute
+      if (TAIL && it >= 1) issue_fc0(it - 1);
+      if (TAIL && it >= 2) issue_fc1(it - 2);
       ++it;
+    }
+    if (TAIL) {  // drain: fc0(n-1), fc1(n-2), fc1(n-1)
+      if (it >= 1) issue_fc0(it - 1);
+      if (it >= 2) issue_fc1(it - 2);
+      if (it >= 1) issue_fc1(it - 1);
     }
   } else {  // ---------------- epilogue: warps 2..9
     constexpr int NC = NP / 2;  // accumulator columns per thread
@@ -209,6 +334,92 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
     const int r = 32 * q + lane;
     const int cbase = half * NC;
     const int nd = p.cdst / 8, n32 = p.d4 / 4;
+    const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
+    int hist_slab[2] = {0, 0}, hist_tile[2] = {0, 0};  // tiles whose tail outputs are pending
+
+    // ---- tail stage 2: hidden layer relu(state x W0 + b0) -> smem (fc1's A operand)
+    auto tail_hidden = [&](int j) {
+      const int b = j & 1;
+      mbar_wait(&hid_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      const int hch = p.thp / 8, hbeg = half * ((hch + 1) / 2), hend = half ? hch : (hch + 1) / 2;
+      uint8_t* H = smem + L.th;  // free: fc1 of the previous tile completed (tail_out ran first)
+      for (int c8 = hbeg; c8 < hend; ++c8) {
+        float hv[8];
+        tmem_ld8(tmem_base + lane_off + col_h + b * p.thp + 8 * c8, hv);
+        tmem_wait_ld();
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = fmaxf(hv[e] + stb0[8 * c8 + e], 0.f);
+        store_chunk(reinterpret_cast<ET*>(H + ((size_t)c8 * NRX_TILE_M + r) * 16), o);
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(&h_ready[b]);
+    };
+    // ---- tail stage 3: outputs of tile j (+b1): messages, or LLRs + chest
+    auto tail_out = [&](int j, int jslab, int jtile) {
+      const int b = j & 1;
+      mbar_wait(&tout_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      const int row = jtile * NRX_TILE_M + r;
+      const int s = row / g.Tp, t = row - s * g.Tp;
+      const bool valid = row < g.rows_data && t < g.T;
+      const uint32_t tcol = tmem_base + lane_off + col_o + b * p.top;
+      if (TAIL == TAIL_MSG) {  // messages of this slab, zero on pad rows/channels
+        ET* const msg = static_cast<ET*>(p.msg);
+        const int och = g.Ca / 8, obeg = half * ((och + 1) / 2), oend = half ? och : (och + 1) / 2;
+        for (int cc = obeg; cc < oend; ++cc) {
+          float mv[8];
+          tmem_ld8(tcol + 8 * cc, mv);
+          tmem_wait_ld();
+          float o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int c = 8 * cc + e;
+            o[e] = (valid && c < g.d) ? mv[e] + stb1[c] : 0.f;
+          }
+          store_chunk(chunk_ptr(msg, jslab, och, cc, row, g), o);
+        }
+      } else if (half == 0) {  // LLRs (masked width) + planar-decoded chest
+        float o[32];
+        tmem_ld16(tcol, o);
+        tmem_ld16(tcol + 16, o + 16);
+        tmem_wait_ld();
+        if (valid) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[c] += stb1[c];
+          const int mio = io_index(p.mod_order, jslab, g);
+          const int width = mio < 0 ? 0 : g.io_width[mio];
+          const size_t re = ((size_t)jslab * g.S + s) * g.T + t;
+          float* lp = p.llr + re * g.llr_width;
+          if (g.llr_width == 4 && width == 4) {
+            *reinterpret_cast<float4*>(lp) = make_float4(o[0], o[1], o[2], o[3]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              if (c < g.llr_width) lp[c] = mio < 0 ? __int_as_float(0x7fc00000) : (c < width ? o[c] : 0.f);
+          }
+          float2* cp = p.chest + re * g.B;
+          if (g.B == 4) {  // planar decode: channel b real, channel B+b imaginary
+            reinterpret_cast<float4*>(cp)[0] = make_float4(o[8], o[12], o[9], o[13]);
+            reinterpret_cast<float4*>(cp)[1] = make_float4(o[10], o[14], o[11], o[15]);
+          } else {
+#pragma unroll
+            for (int bb = 0; bb < 8; ++bb) {
+              if (bb >= g.B) break;
+              float im = 0.f;
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (k == bb) im = o[8 + g.B + k];
+              cp[bb] = make_float2(o[8 + bb], im);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+    };
+
     WorkIter w(g, g.NU, g.tiles, p.n_io, p.mod_order);
     int slab, tile, it = 0;
     while (w.next(slab, tile)) {
@@ -220,7 +431,7 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
       NRX_T(t1);
       tc_fence_after();
       float v[NC];
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * NP + cbase;
+      const uint32_t taddr = tmem_base + lane_off + acc * NP + cbase;
 #pragma unroll
       for (int c = 0; c < NC / 8; ++c) tmem_ld8(taddr + 8 * c, v + 8 * c);
       tmem_wait_ld();
@@ -272,7 +483,7 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
             if (cc < n32) store_chunk(chunk_ptr(p.dst32, slab, n32, cc, row, g), x + 4 * c4);
           }
         }
-        if (valid) {  // positional channels d, d+1 of the bf16 operand copy
+        if (valid) {  // positional channels d, d+1 of the half-precision operand copy
           const float pdt = g.dt[t], pdf = pos_df(s, slab % g.U, g);
 #pragma unroll
           for (int j = 0; j < NC; ++j) {
@@ -285,7 +496,10 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
 #pragma unroll
       for (int c8 = 0; c8 < NC / 8; ++c8) {
         const int cc = cbase / 8 + c8;
-        if (cc < nd) store_chunk(chunk_ptr(dst, slab, nd, cc, row, g), x + 8 * c8);
+        if (cc < nd) {
+          store_chunk(chunk_ptr(dst, slab, nd, cc, row, g), x + 8 * c8);
+          if (TAIL) store_chunk(reinterpret_cast<ET*>(smem + L.ta + (it & 1) * ta_bytes + ((size_t)cc * NRX_TILE_M + r) * 16), x + 8 * c8);
+        }
       }
       if (half == 1) {  // buffer channels beyond the accumulator: positional / zero only
         for (int cc = NP / 8; cc < nd; ++cc) {
@@ -294,16 +508,33 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
           for (int e = 0; e < 8; ++e)
             o[e] = (valid && MODE != EPI_RELU) ? state_extra(8 * cc + e, s, t, slab % g.U, g) : 0.f;
           store_chunk(chunk_ptr(dst, slab, nd, cc, row, g), o);
+          if (TAIL) store_chunk(reinterpret_cast<ET*>(smem + L.ta + (it & 1) * ta_bytes + ((size_t)cc * NRX_TILE_M + r) * 16), o);
         }
+      }
+      if (TAIL) {
+        fence_proxy_async();  // state tile (generic-proxy stores) -> tensor-core reads
+        tc_fence_before();
+        mbar_arrive(&ta_ready[it & 1]);
+        // pipelined tail stages: outputs of tile it-2 (frees the hidden tile),
+        // then the hidden layer of tile it-1
+        if (it >= 2) tail_out(it - 2, hist_slab[it & 1], hist_tile[it & 1]);
+        if (it >= 1) tail_hidden(it - 1);
+        hist_slab[it & 1] = slab;
+        hist_tile[it & 1] = tile;
       }
       NRX_TADD(t_b, t1);
       ++it;
     }
+    if (TAIL) {  // drain, mirroring the MMA warp
+      if (it >= 2) tail_out(it - 2, hist_slab[it & 1], hist_tile[it & 1]);
+      if (it >= 1) tail_hidden(it - 1);
+      if (it >= 1) tail_out(it - 1, hist_slab[(it - 1) & 1], hist_tile[(it - 1) & 1]);
+    }
   }
 #ifdef NRX_TIMING
   if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 64))
-    printf("conv NP=%d mode=%d c0=%d c1=%d tid=%d all=%lld a=%lld b=%lld c=%lld\n", NP, MODE, p.c0, p.c1,
-           threadIdx.x, clock64() - t_all, t_a, t_b, t_c);
+    printf("conv NP=%d mode=%d tail=%d c0=%d c1=%d tid=%d all=%lld a=%lld b=%lld c=%lld\n", NP, MODE, TAIL, p.c0,
+           p.c1, threadIdx.x, clock64() - t_all, t_a, t_b, t_c);
 #endif
   tc_fence_before();
   __syncthreads();
@@ -313,77 +544,123 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
   }
 }
 
-
 using KFn = void (*)(const ConvTcParams, const CUtensorMap, const CUtensorMap);
 
-template <typename ET>
-static KFn select_conv(const Geom& g, int np, int mode, int c0, int c1) {
+template <typename ET, int TAIL>
+static KFn select_conv_tail(const Geom& g, int np, int mode, int c0, int c1) {
   static const KFn table[4][3] = {
-      {k_conv_tc<ET, 16, 0>, k_conv_tc<ET, 16, 1>, k_conv_tc<ET, 16, 2>},
-      {k_conv_tc<ET, 32, 0>, k_conv_tc<ET, 32, 1>, k_conv_tc<ET, 32, 2>},
-      {k_conv_tc<ET, 48, 0>, k_conv_tc<ET, 48, 1>, k_conv_tc<ET, 48, 2>},
-      {k_conv_tc<ET, 64, 0>, k_conv_tc<ET, 64, 1>, k_conv_tc<ET, 64, 2>}};
+      {k_conv_tc<ET, 16, 0, TAIL>, k_conv_tc<ET, 16, 1, TAIL>, k_conv_tc<ET, 16, 2, TAIL>},
+      {k_conv_tc<ET, 32, 0, TAIL>, k_conv_tc<ET, 32, 1, TAIL>, k_conv_tc<ET, 32, 2, TAIL>},
+      {k_conv_tc<ET, 48, 0, TAIL>, k_conv_tc<ET, 48, 1, TAIL>, k_conv_tc<ET, 48, 2, TAIL>},
+      {k_conv_tc<ET, 64, 0, TAIL>, k_conv_tc<ET, 64, 1, TAIL>, k_conv_tc<ET, 64, 2, TAIL>}};
   KFn fn = table[np / 16 - 1][mode];
   // fully unrolled issue for the 3x3 layers of d_s in (48, 64] (the RT / large models)
   if (g.ks == 3 && np == 64) {
     const int nk0 = c0 / 16, nk1 = c1 / 16;
-    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_tc<ET, 64, EPI_RELU, 3, 2, 0>;
-    if (mode == EPI_RELU && nk0 == 4 && nk1 == 4) fn = k_conv_tc<ET, 64, EPI_RELU, 3, 4, 4>;
-    if (mode == EPI_STATE_INIT && nk0 == 4 && nk1 == 0) fn = k_conv_tc<ET, 64, EPI_STATE_INIT, 3, 4, 0>;
-    if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0) fn = k_conv_tc<ET, 64, EPI_RESIDUAL, 3, 4, 0>;
+    if (TAIL == TAIL_NONE && mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_tc<ET, 64, EPI_RELU, TAIL, 3, 2, 0>;
+    if (TAIL == TAIL_NONE && mode == EPI_RELU && nk0 == 4 && nk1 == 4) fn = k_conv_tc<ET, 64, EPI_RELU, TAIL, 3, 4, 4>;
+    if (TAIL != TAIL_READOUT && mode == EPI_STATE_INIT && nk0 == 4 && nk1 == 0)
+      fn = k_conv_tc<ET, 64, EPI_STATE_INIT, TAIL, 3, 4, 0>;
+    if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0) fn = k_conv_tc<ET, 64, EPI_RESIDUAL, TAIL, 3, 4, 0>;
   }
   return fn;
 }
 
-static int launch_conv(const Geom& g, const PackLayout& L, const ConvOff* offs, int n_off, const void* src0,
-                       int c0, const void* src1, int c1, void* dst, int cdst, float* dst32, int mode,
-                       const uint8_t* wb, const int32_t* mod_order, cudaStream_t st) {
+template <typename ET>
+static KFn select_conv(const Geom& g, int np, int mode, int tail, int c0, int c1) {
+  if (tail == TAIL_MSG) return select_conv_tail<ET, TAIL_MSG>(g, np, mode, c0, c1);
+  if (tail == TAIL_READOUT) return select_conv_tail<ET, TAIL_READOUT>(g, np, mode, c0, c1);
+  return select_conv_tail<ET, TAIL_NONE>(g, np, mode, c0, c1);
+}
+
+struct ConvLaunch {
+  const ConvOff* offs;
+  int n_off;
+  const void* src0;
+  int c0;
+  const void* src1;
+  int c1;
+  int src1_xor;
+  void* dst;
+  int cdst;
+  float* dst32;
+  int mode;
+  int tail;             // ConvTail
+  const MlpOff* tail_w;  // per IO set (readout) or one (message MLP)
+  int tail_n;
+  void* msg;
+  float* llr;
+  float2* chest;
+};
+
+static int launch_conv(const Geom& g, const ConvLaunch& c, const uint8_t* wb, const int32_t* mod_order,
+                       cudaStream_t st) {
   ConvTcParams p{};
   p.g = g;
-  p.ktap = c0 + c1;
-  p.c0 = c0;
-  p.c1 = c1;
+  p.ktap = c.c0 + c.c1;
+  p.c0 = c.c0;
+  p.c1 = c.c1;
+  p.src1_xor = c.src1_xor;
   p.np = rup(g.d, 16);
-  p.cdst = cdst;
-  p.mode = mode;
-  p.n_io = n_off;
+  p.cdst = c.cdst;
+  p.mode = c.mode;
+  p.n_io = c.tail == TAIL_READOUT ? c.tail_n : c.n_off;
   p.d4 = rup(g.d, 4);
   // rows per channel chunk in shared memory: the tile plus the halo rounded
   // up to the 16-row TMA granule on both sides (also keeps chunks 256-B aligned)
   p.hup = rup(g.H, 16);
   p.rbox = NRX_TILE_M + 2 * p.hup;
   p.wbytes = (uint32_t)(g.ks * g.ks * p.ktap * p.np * 2);
-  p.abytes = (uint32_t)((c0 > c1 ? c0 : c1) * p.rbox * 2);  // one source per stage
-  p.tmem_cols = p.np * 2 <= 32 ? 32 : p.np * 2 <= 64 ? 64 : p.np * 2 <= 128 ? 128 : 256;
+  p.abytes = (uint32_t)((c.c0 > c.c1 ? c.c0 : c.c1) * p.rbox * 2);  // one source per stage
   p.wbase = wb;
-  for (int i = 0; i < n_off; ++i) {
-    p.w_off[i] = offs[i].w;
-    p.b_off[i] = offs[i].b;
+  for (int i = 0; i < p.n_io; ++i) {
+    const int k = c.n_off > 1 ? i : 0;  // conv weights: per IO set for the var_io state init only
+    p.w_off[i] = c.offs[k].w;
+    p.b_off[i] = c.offs[k].b;
   }
   p.mod_order = mod_order;
-  p.dst = dst;
-  p.dst32 = dst32;
-  const size_t fixed = ((p.wbytes + 1023) & ~1023u) + 22 * 8 + 64 * 4 + 64;
+  p.dst = c.dst;
+  p.dst32 = c.dst32;
+  if (c.tail) {
+    const int hp = rup(g.h, 16);
+    p.thp = c.tail == TAIL_MSG ? hp : 2 * hp;
+    p.top = c.tail == TAIL_MSG ? rup(g.d, 16) : 32;
+    p.tw0bytes = (uint32_t)(g.Cs * p.thp * 2);
+    p.tw1bytes = (uint32_t)(p.thp * p.top * 2);
+    for (int i = 0; i < p.n_io; ++i) {
+      const MlpOff& m = c.tail_w[c.tail_n > 1 ? i : 0];
+      p.tw0[i] = m.w0;
+      p.tb0[i] = m.b0;
+      p.tw1[i] = m.w1;
+      p.tb1[i] = m.b1;
+    }
+    p.msg = c.msg;
+    p.llr = c.llr;
+    p.chest = c.chest;
+    if (p.thp > 256 || p.top > 64) return NRX_ERR_UNSUPPORTED;
+  }
+  const uint32_t cols = 2 * p.np + (c.tail ? 2 * (p.thp + p.top) : 0);
+  p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+  if (cols > 512) return NRX_ERR_UNSUPPORTED;
   int stages = 8;
-  while (stages > 2 && fixed + (size_t)stages * p.abytes > SMEM_LIMIT) --stages;
-  if (fixed + (size_t)stages * p.abytes > SMEM_LIMIT || p.rbox > 256) return NRX_ERR_UNSUPPORTED;
   p.stages = stages;
-  const size_t smem = fixed + (size_t)stages * p.abytes;
+  while (stages > 2 && conv_smem_layout(p, c.tail).total > SMEM_LIMIT) p.stages = --stages;
+  if (conv_smem_layout(p, c.tail).total > SMEM_LIMIT || p.rbox > 256) return NRX_ERR_UNSUPPORTED;
+  const size_t smem = conv_smem_layout(p, c.tail).total;
   CUtensorMap m0, m1;
-  int rc = make_map(&m0, src0, g, c0, p.rbox);
+  int rc = make_map(&m0, c.src0, g, c.c0, p.rbox);
   if (rc) return rc;
-  rc = make_map(&m1, src1 ? src1 : src0, g, c1 ? c1 : c0, p.rbox);
+  rc = make_map(&m1, c.src1 ? c.src1 : c.src0, g, c.c1 ? c.c1 : c.c0, p.rbox);
   if (rc) return rc;
-  if (p.np % 16 || p.np < 16 || p.np > 64 || mode < 0 || mode > 2) return NRX_ERR_UNSUPPORTED;
-  const KFn fn = g.prec == NRX_FP16 ? select_conv<__half>(g, p.np, mode, c0, c1)
-                                    : select_conv<__nv_bfloat16>(g, p.np, mode, c0, c1);
+  if (p.np % 16 || p.np < 16 || p.np > 64 || c.mode < 0 || c.mode > 2) return NRX_ERR_UNSUPPORTED;
+  const KFn fn = g.prec == NRX_FP16 ? select_conv<__half>(g, p.np, c.mode, c.tail, c.c0, c.c1)
+                                    : select_conv<__nv_bfloat16>(g, p.np, c.mode, c.tail, c.c0, c.c1);
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.NU * g.tiles;
-  dim3 grid(total < num_sms() ? total : num_sms(), n_off);
+  dim3 grid(total < num_sms() ? total : num_sms(), p.n_io);
   fn<<<grid, CONV_THREADS, smem, st>>>(p, m0, m1);
   return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
 }
-
 
 }  // namespace tc
 
@@ -398,6 +675,10 @@ int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const void
 int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const void* state,
                    const int32_t* mod_order, float* llr, float2* chest, cudaStream_t st);
 
+// U = 2: message MLP fused into every conv1, partner-slab messages as the
+// update conv's second source; any U: readout fused into the last conv1.
+bool tc_fused_messages(const Geom& g) { return g.U == 2; }
+
 int launch_forward_tc(const Geom& g, const PackLayout& L, const WsLayout& W, int n_it, const uint8_t* wb,
                       const int32_t* mod_order, uint8_t* ws, float* llr, float2* chest, cudaStream_t st) {
   using namespace tc;
@@ -405,39 +686,90 @@ int launch_forward_tc(const Geom& g, const PackLayout& L, const WsLayout& W, int
   void* feats = ws + W.feats;
   void* h = ws + W.h;
   void* state = ws + W.state;
-  void* agg = ws + W.agg;
+  void* agg = ws + W.agg;  // aggregate (U != 2) or own-slab messages (U = 2)
   // bf16 keeps an fp32 copy of the residual state stream; fp16 updates the state in place
   float* state32 = g.prec == NRX_BF16 ? reinterpret_cast<float*>(ws + W.state32) : nullptr;
+  const bool fused = tc_fused_messages(g);
+
+  ConvLaunch c{};
+  c.offs = L.init0;
+  c.n_off = g.n_io;
+  c.src0 = feats;
+  c.c0 = g.Cf;
+  c.dst = h;
+  c.cdst = g.Ch;
+  c.mode = EPI_RELU;
   {
     ProfScope ps(KID_INIT0, st);
-    NRX_TRY_TC(launch_conv(g, L, L.init0, g.n_io, feats, g.Cf, nullptr, 0, h, g.Ch, nullptr, EPI_RELU, wb,
-                           mod_order, st));
+    NRX_TRY_TC(launch_conv(g, c, wb, mod_order, st));
+  }
+  c = ConvLaunch{};
+  c.offs = L.init1;
+  c.n_off = g.n_io;
+  c.src0 = h;
+  c.c0 = g.Ch;
+  c.dst = state;
+  c.cdst = g.Cs;
+  c.dst32 = state32;
+  c.mode = EPI_STATE_INIT;
+  if (fused) {
+    c.tail = TAIL_MSG;
+    c.tail_w = &L.msg;
+    c.tail_n = 1;
+    c.msg = agg;
   }
   {
     ProfScope ps(KID_INIT1, st);
-    NRX_TRY_TC(launch_conv(g, L, L.init1, g.n_io, h, g.Ch, nullptr, 0, state, g.Cs, state32, EPI_STATE_INIT, wb,
-                           mod_order, st));
+    NRX_TRY_TC(launch_conv(g, c, wb, mod_order, st));
   }
   for (int it = 0; it < n_it; ++it) {
-    {
+    if (!fused) {
       ProfScope ps(KID_MSG, st);
       NRX_TRY_TC(launch_msg(g, L, wb, state, agg, st));
     }
+    c = ConvLaunch{};
+    c.offs = &L.upd0;
+    c.n_off = 1;
+    c.src0 = state;
+    c.c0 = g.Cs;
+    c.src1 = agg;
+    c.c1 = g.Ca;
+    c.src1_xor = fused ? 1 : 0;  // U = 2: the partner UE's messages are the aggregate
+    c.dst = h;
+    c.cdst = g.Ch;
+    c.mode = EPI_RELU;
     {
       ProfScope ps(KID_UPD0, st);
-      NRX_TRY_TC(launch_conv(g, L, &L.upd0, 1, state, g.Cs, agg, g.Ca, h, g.Ch, nullptr, EPI_RELU, wb, mod_order,
-                             st));
+      NRX_TRY_TC(launch_conv(g, c, wb, mod_order, st));
     }
-    {
-      ProfScope ps(KID_UPD1, st);
-      NRX_TRY_TC(launch_conv(g, L, &L.upd1, 1, h, g.Ch, nullptr, 0, state, g.Cs, state32, EPI_RESIDUAL, wb,
-                             mod_order, st));
+    const bool last = it + 1 == n_it;
+    c = ConvLaunch{};
+    c.offs = &L.upd1;
+    c.n_off = 1;
+    c.src0 = h;
+    c.c0 = g.Ch;
+    c.dst = state;
+    c.cdst = g.Cs;
+    c.dst32 = state32;
+    c.mode = EPI_RESIDUAL;
+    if (last) {
+      c.tail = TAIL_READOUT;
+      c.tail_w = L.llr;
+      c.tail_n = g.n_io;
+      c.llr = llr;
+      c.chest = chest;
+    } else if (fused) {
+      c.tail = TAIL_MSG;
+      c.tail_w = &L.msg;
+      c.tail_n = 1;
+      c.msg = agg;
     }
+    ProfScope ps(KID_UPD1, st);
+    NRX_TRY_TC(launch_conv(g, c, wb, mod_order, st));
   }
-  ProfScope ps(KID_READOUT, st);
-  return launch_readout(g, L, wb, state, mod_order, llr, chest, st);
+  return NRX_OK;
 }
 
-int tc_launch_count(int n_it) { return 2 + 3 * n_it + 1; }
+int tc_launch_count(int n_it, int num_ues) { return 2 + (num_ues == 2 ? 2 : 3) * n_it; }
 
 }  // namespace nrx

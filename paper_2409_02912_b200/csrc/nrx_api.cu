@@ -21,7 +21,7 @@ void pack_layout(const nrx_model_desc* m, int prec, PackLayout* L);
 void ws_layout(const Geom& g, WsLayout* w);
 int launch_forward_tc(const Geom& g, const PackLayout& L, const WsLayout& W, int n_it, const uint8_t* wb,
                       const int32_t* mod_order, uint8_t* ws, float* llr, float2* chest, cudaStream_t st);
-int tc_launch_count(int n_it);
+int tc_launch_count(int n_it, int num_ues);
 }  // namespace nrx
 
 using namespace nrx;
@@ -99,10 +99,11 @@ extern "C" int nrx_forward(const nrx_model_desc* model, const nrx_slot_desc* slo
   return launch_forward_tc(g, L, W, num_iterations, wb, mod_order, ws, llr_out, static_cast<float2*>(chest_out), st);
 }
 
-extern "C" int nrx_forward_launch_count(const nrx_model_desc* model, int precision, int num_iterations) {
-  if (!model || num_iterations < 1) return -1;
+extern "C" int nrx_forward_launch_count(const nrx_model_desc* model, const nrx_slot_desc* slot, int precision,
+                                        int num_iterations) {
+  if (!model || !slot || num_iterations < 1) return -1;
   if (precision == NRX_FP32) return 1 + 2 + 3 * num_iterations + 1;
-  return 1 + tc_launch_count(num_iterations);
+  return 1 + tc_launch_count(num_iterations, slot->num_ues);
 }
 
 extern "C" int nrx_buffer_geometry(const nrx_model_desc* model, const nrx_slot_desc* slot, int precision,

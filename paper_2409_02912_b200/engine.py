@@ -111,8 +111,10 @@ class NrxEngine:
             tls.ws["ws"] = ws
         return ws
 
-    def launch_count(self, num_iterations: int) -> int:
-        return self.lib.nrx_forward_launch_count(ctypes.byref(self._m), self.prec_id, int(num_iterations))
+    def launch_count(self, cfg, num_iterations: int) -> int:
+        s = _lib.slot_desc(cfg)
+        return self.lib.nrx_forward_launch_count(ctypes.byref(self._m), ctypes.byref(s), self.prec_id,
+                                                 int(num_iterations))
 
     # -- device-resident entry ---------------------------------------------------
 
