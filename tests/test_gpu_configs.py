@@ -1,0 +1,96 @@
+"""GPU parity on the BASELINE.json configurations other than the benchmark's
+C2 slot (which tests/test_gpu_parity.py covers):
+
+  C1  1 UE, 24 PRB, 16-QAM, RT model (d_s=56, N_it=2)
+  C3  mixed modulation orders through the masked readout (QPSK/64-QAM), the
+      var_io variant, and the 256-QAM extension (m_max = 8)
+  C4  the large non-real-time variant (d_s=56, N_it=8) plus depth control
+All against the float64 CPU oracle with the per-precision gates of
+tests/test_gpu_parity.py."""
+
+import numpy as np
+import pytest
+
+from oracle import nrx_oracle as orc
+from test_gpu_parity import check_chest, check_llrs
+
+pytestmark = pytest.mark.gpu
+
+PRECISIONS = ["fp32", "bf16", "fp16"]
+
+
+def _run(cfg, config, w, mcs, n_slots, seed, precision, num_iterations=None, n0=0.1):
+    from paper_2409_02912_b200.nrx import nrx_forward
+    from paper_2409_02912_b200.synth import synth_slots
+    y, books, _ = synth_slots(cfg, [m.modulation_order for m in mcs], n_slots, n0, seed=seed)
+    ref, ref_chest = orc.nrx_forward(y, books, cfg, mcs, w, config, n0, num_iterations=num_iterations,
+                                     dtype=np.float64)
+    got, chest = nrx_forward(y, books, cfg, mcs, w, config, n0, num_iterations=num_iterations,
+                             precision=precision)
+    return got, ref, chest, ref_chest
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_c1_single_ue_24prb(precision):
+    from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights
+    t = default_mcs_table()
+    cfg = SlotConfig(num_subcarriers=288, num_ues=1, comb_size=2)
+    config = NrxConfig.from_table(t, (14,), d_s=56, num_iterations=2)
+    w = orc.perturb_biases(init_weights(config, 3))
+    got, ref, chest, ref_chest = _run(cfg, config, w, (t[14],), 2, 5, precision)
+    check_llrs(got, ref, precision, "C1")
+    check_chest(chest, ref_chest, precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_c3_mixed_mcs_masking(precision):
+    from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights
+    t = default_mcs_table()
+    cfg = SlotConfig(num_subcarriers=480, num_ues=2, comb_size=2)
+    config = NrxConfig.from_table(t, (9, 14, 19), variant="masking", d_s=56, num_iterations=2)
+    w = orc.perturb_biases(init_weights(config, 4))
+    got, ref, chest, ref_chest = _run(cfg, config, w, (t[9], t[19]), 2, 6, precision)
+    assert got[0].shape[-1] == 2 and got[1].shape[-1] == 6      # label-prefix masking per UE
+    check_llrs(got, ref, precision, "C3 masking")
+    check_chest(chest, ref_chest, precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_c3_var_io(precision):
+    from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights
+    t = default_mcs_table()
+    cfg = SlotConfig(num_subcarriers=240, num_ues=2, comb_size=2)
+    config = NrxConfig.from_table(t, (9, 14, 19), variant="var_io", d_s=56, num_iterations=2)
+    w = orc.perturb_biases(init_weights(config, 5))
+    got, ref, chest, ref_chest = _run(cfg, config, w, (t[19], t[9]), 2, 7, precision)
+    assert got[0].shape[-1] == 6 and got[1].shape[-1] == 2
+    check_llrs(got, ref, precision, "C3 var_io")
+    check_chest(chest, ref_chest, precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_256qam_extension_shares_the_masked_readout(precision):
+    """EXTENSION (not in the reference): m_max = 8; QPSK and 256-QAM UEs in
+    one call through the same masked readout.  The oracle's network is
+    order-agnostic (nrx.py:316-319 accepts any order <= m_max)."""
+    from paper_2409_02912_b200.config import NrxConfig, SlotConfig, extended_mcs_table, init_weights
+    t = extended_mcs_table()
+    cfg = SlotConfig(num_subcarriers=240, num_ues=2, comb_size=2)
+    config = NrxConfig.from_table(t, (9, 14, 19, 27), variant="masking", d_s=56, num_iterations=2)
+    assert config.m_max == 8
+    w = orc.perturb_biases(init_weights(config, 6))
+    got, ref, chest, ref_chest = _run(cfg, config, w, (t[27], t[9]), 2, 8, precision, n0=0.01)
+    assert got[0].shape[-1] == 8 and got[1].shape[-1] == 2
+    check_llrs(got, ref, precision, "256-QAM")
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_c4_large_model_and_depth_control(precision):
+    from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights
+    t = default_mcs_table()
+    cfg = SlotConfig(num_subcarriers=240, num_ues=2, comb_size=2)
+    config = NrxConfig.from_table(t, (14,), d_s=56, num_iterations=8)
+    w = init_weights(config, 7)  # zero biases: the SURVEY §8c calibration for N_it = 8
+    for depth in (8, 3):
+        got, ref, chest, ref_chest = _run(cfg, config, w, (t[14], t[14]), 1, 9, precision, num_iterations=depth)
+        check_llrs(got, ref, precision, f"C4 depth {depth}", depth=depth)

@@ -28,8 +28,14 @@ def _gpu():
     return torch, gnrx
 
 
-def check_llrs(got_list, ref_list, precision, label=""):
-    gate = GATES[precision]
+def check_llrs(got_list, ref_list, precision, label="", depth=2):
+    """The p99 gates are calibrated at the RT depth N_it = 2 (SURVEY.md §8c);
+    rounding noise of the half-precision operands accumulates roughly like a
+    random walk over the unrolled iterations, so the p99 gate is scaled by
+    sqrt(depth / 2) for deeper models (bf16 at N_it = 8: 1e-2)."""
+    gate = dict(GATES[precision])
+    if depth > 2:
+        gate["p99"] *= float(np.sqrt(depth / 2))
     scale = max(float(np.abs(r).max()) for r in ref_list)
     for got, ref in zip(got_list, ref_list):
         assert got.shape == ref.shape, (label, got.shape, ref.shape)
