@@ -287,6 +287,8 @@ def run_ours(args):
 
     # single-slot latency (device resident), CUDA graph of the whole forward
     lat = latency_single_slot(eng, cfg, dev, args.latency_runs) if rank == 0 else None
+    lat_other = other_config_latencies(args.precision, dev, max(100, args.latency_runs // 4)) \
+        if rank == 0 and not args.no_precision_sweep else None
 
     # end to end through the public host API: pinned H2D + D2H inside the region
     e2e = e2e_throughput(eng, cfg, B, max(4, args.steps // 2), world, dev)
@@ -332,6 +334,7 @@ def run_ours(args):
                    "l2": "inputs alternate between two device buffers (188 MB) and per-step activations "
                          "are > 1 GB, i.e. far larger than the 126 MB L2"},
         "latency_us": lat,
+        "latency_other_configs_us": lat_other,
         "e2e": e2e,
         "roofline": {"kernel": "conv_update0 (iteration.update.conv0, 3x3 114->56, implicit GEMM)",
                      "bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 1),
@@ -355,28 +358,32 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def latency_single_slot(eng, cfg, dev, runs: int):
+def latency_single_slot(eng, cfg, dev, runs: int, n_it: int = N_IT, orders=None, width: int = 4,
+                        note: str = "one C2 slot"):
     import torch
     y, pil, nf, mods = (torch.from_numpy(a).to(dev) for a in host_batch(cfg, 1, pool=1, seed=7))
-    llr = torch.empty((1, cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, 4), dtype=torch.float32, device=dev)
+    if orders is not None:
+        mods = torch.tensor(orders, dtype=torch.int32, device=dev)
+    llr = torch.empty((1, cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, width), dtype=torch.float32,
+                      device=dev)
     chest = torch.empty((1, cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, 4), dtype=torch.complex64, device=dev)
     ws = torch.empty_like(eng.workspace(cfg, 1))
     side = torch.cuda.Stream(dev)
     mode = "cuda_graph"
     with torch.cuda.stream(side):
         for _ in range(3):
-            eng.forward_device(cfg, y, pil, nf, mods, N_IT, llr, chest, workspace=ws, stream=side)
+            eng.forward_device(cfg, y, pil, nf, mods, n_it, llr, chest, workspace=ws, stream=side)
     side.synchronize()
     try:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=side):
-            eng.forward_device(cfg, y, pil, nf, mods, N_IT, llr, chest, workspace=ws, stream=side)
+            eng.forward_device(cfg, y, pil, nf, mods, n_it, llr, chest, workspace=ws, stream=side)
         run = g.replay
     except Exception:
         mode = "stream"
 
         def run():
-            eng.forward_device(cfg, y, pil, nf, mods, N_IT, llr, chest, workspace=ws,
+            eng.forward_device(cfg, y, pil, nf, mods, n_it, llr, chest, workspace=ws,
                                stream=torch.cuda.current_stream(dev))
     for _ in range(20):
         run()
@@ -391,7 +398,38 @@ def latency_single_slot(eng, cfg, dev, runs: int):
     us = np.array([a.elapsed_time(b) * 1e3 for a, b in ev])
     return {"p50": round(float(np.median(us)), 2), "p99": round(float(np.percentile(us, 99)), 2),
             "min": round(float(us.min()), 2), "runs": runs, "mode": mode,
-            "note": "one C2 slot, device-resident inputs (no host copies), back-to-back launches"}
+            "note": f"{note}, device-resident inputs (no host copies), back-to-back launches"}
+
+
+def other_config_latencies(precision, dev, runs: int):
+    """Single-slot latency of BASELINE.json configs[0], [2], [3] (C1 24 PRB /
+    1 UE; C3 dynamic MCS QPSK + 256-QAM extension through the masked readout;
+    C4 large N_it = 8 with the affine depth fit, evaluation.py:351-363)."""
+    from paper_2409_02912_b200.config import NrxConfig, SlotConfig, extended_mcs_table, init_weights
+    from paper_2409_02912_b200.engine import NrxEngine
+    t = extended_mcs_table()
+    out = {}
+    cfg1 = SlotConfig(num_subcarriers=288, num_ues=1, comb_size=2)
+    c1 = NrxConfig.from_table(t, (14,), d_s=56, num_iterations=2)
+    out["C1_24prb_1ue"] = latency_single_slot(NrxEngine(c1, init_weights(c1, 0), precision, dev), cfg1, dev, runs,
+                                              note="C1 slot (24 PRB, 1 UE, RT d_s=56 N_it=2)")
+    cfg = SlotConfig(num_subcarriers=S_C2, num_ues=2, comb_size=2)
+    c3 = NrxConfig.from_table(t, (9, 14, 19, 27), variant="masking", d_s=56, num_iterations=2)
+    out["C3_mixed_qpsk_256qam"] = latency_single_slot(
+        NrxEngine(c3, init_weights(c3, 0), precision, dev), cfg, dev, runs, orders=[2, 8], width=8,
+        note="C3 slot (273 PRB, UE0 QPSK + UE1 256-QAM ext., masking m_max=8)")
+    c4 = NrxConfig.from_table(t, (14,), d_s=56, num_iterations=8)
+    e4 = NrxEngine(c4, init_weights(c4, 0), precision, dev)
+    depth = {}
+    for n in (1, 2, 4, 8):
+        depth[n] = latency_single_slot(e4, cfg, dev, max(50, runs // 4), n_it=n,
+                                       note=f"C4 slot (273 PRB, 2 UE, large d_s=56) at depth {n}")
+    xs = np.array(list(depth))
+    ys = np.array([depth[n]["p50"] for n in depth])
+    b, a = np.polyfit(xs, ys, 1)
+    out["C4_large_nit8"] = dict(depth[8], depth_p50_us={int(k): v["p50"] for k, v in depth.items()},
+                                affine_fit_us={"overhead": round(float(a), 2), "per_iteration": round(float(b), 2)})
+    return out
 
 
 def e2e_throughput(eng, cfg, B, steps, world, dev):

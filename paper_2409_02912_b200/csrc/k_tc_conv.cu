@@ -57,10 +57,12 @@ struct ConvTcParams {
   float2* chest;
 };
 
-// warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue (two warps per
-// TMEM lane quarter, each draining half of the accumulator columns)
-constexpr int CONV_THREADS = 320;
-constexpr int CONV_EPI_THREADS = 256;
+// warp 0 TMA producer, warp 1 MMA issuer, then NP/16 groups of four epilogue
+// warps (one per TMEM lane quarter); every epilogue thread drains 16
+// accumulator columns of one row (NP=64: 16 epilogue warps, 576 threads).
+__host__ __device__ constexpr int conv_parts(int np) { return np / 16; }
+__host__ __device__ constexpr int conv_epi_threads(int np) { return 128 * conv_parts(np); }
+__host__ __device__ constexpr int conv_threads(int np) { return 64 + conv_epi_threads(np); }
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   uint32_t r[8];
@@ -112,7 +114,7 @@ __host__ __device__ inline ConvSmem conv_smem_layout(const ConvTcParams& p, int 
 // matches); KS = 0 is the generic runtime-loop version.
 // ET = __nv_bfloat16 or __half: operand/activation element type.
 template <typename ET, int NP, int MODE, int TAIL, int KS = 0, int NK0 = 0, int NK1 = 0>
-__global__ void __launch_bounds__(CONV_THREADS, 1)
+__global__ void __launch_bounds__(conv_threads(NP), 1)
     k_conv_tc(const __grid_constant__ ConvTcParams p, const __grid_constant__ CUtensorMap map0,
               const __grid_constant__ CUtensorMap map1) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -146,13 +148,13 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], CONV_EPI_THREADS);
+      mbar_init(&tempty[a], conv_epi_threads(NP));
     }
     mbar_init(wbar, 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&ta_ready[b], CONV_EPI_THREADS);
+      mbar_init(&ta_ready[b], conv_epi_threads(NP));
       mbar_init(&hid_full[b], 1);
-      mbar_init(&h_ready[b], CONV_EPI_THREADS);
+      mbar_init(&h_ready[b], conv_epi_threads(NP));
       mbar_init(&tout_full[b], 1);
     }
     fence_barrier_init();
@@ -328,11 +330,12 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
       if (it >= 2) issue_fc1(it - 2);
       if (it >= 1) issue_fc1(it - 1);
     }
-  } else {  // ---------------- epilogue: warps 2..9
-    constexpr int NC = NP / 2;  // accumulator columns per thread
-    const int q = warp & 3, half = (warp - 2) >> 2;
+  } else {  // ---------------- epilogue: warps 2 .. 2 + 4*PARTS - 1
+    constexpr int PARTS = conv_parts(NP);
+    constexpr int NC = NP / PARTS;  // = 16 accumulator columns per thread
+    const int q = warp & 3, part = (warp - 2) >> 2;
     const int r = 32 * q + lane;
-    const int cbase = half * NC;
+    const int cbase = part * NC;
     const int nd = p.cdst / 8, n32 = p.d4 / 4;
     const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
     int hist_slab[2] = {0, 0}, hist_tile[2] = {0, 0};  // tiles whose tail outputs are pending
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
       const int b = j & 1;
       mbar_wait(&hid_full[b], (j >> 1) & 1);
       tc_fence_after();
-      const int hch = p.thp / 8, hbeg = half * ((hch + 1) / 2), hend = half ? hch : (hch + 1) / 2;
+      const int hch = p.thp / 8, hbeg = part * hch / PARTS, hend = (part + 1) * hch / PARTS;
       uint8_t* H = smem + L.th;  // free: fc1 of the previous tile completed (tail_out ran first)
       for (int c8 = hbeg; c8 < hend; ++c8) {
         float hv[8];
@@ -368,7 +371,7 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
       const uint32_t tcol = tmem_base + lane_off + col_o + b * p.top;
       if (TAIL == TAIL_MSG) {  // messages of this slab, zero on pad rows/channels
         ET* const msg = static_cast<ET*>(p.msg);
-        const int och = g.Ca / 8, obeg = half * ((och + 1) / 2), oend = half ? och : (och + 1) / 2;
+        const int och = g.Ca / 8, obeg = part * och / PARTS, oend = (part + 1) * och / PARTS;
         for (int cc = obeg; cc < oend; ++cc) {
           float mv[8];
           tmem_ld8(tcol + 8 * cc, mv);
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
           }
           store_chunk(chunk_ptr(msg, jslab, och, cc, row, g), o);
         }
-      } else if (half == 0) {  // LLRs (masked width) + planar-decoded chest
+      } else if (part == 0) {  // LLRs (masked width) + planar-decoded chest
         float o[32];
         tmem_ld16(tcol, o);
         tmem_ld16(tcol + 16, o + 16);
@@ -501,7 +504,7 @@ __global__ void __launch_bounds__(CONV_THREADS, 1)
           if (TAIL) store_chunk(reinterpret_cast<ET*>(smem + L.ta + (it & 1) * ta_bytes + ((size_t)cc * NRX_TILE_M + r) * 16), x + 8 * c8);
         }
       }
-      if (half == 1) {  // buffer channels beyond the accumulator: positional / zero only
+      if (part == PARTS - 1) {  // buffer channels beyond the accumulator: positional / zero only
         for (int cc = NP / 8; cc < nd; ++cc) {
           float o[8];
 #pragma unroll
@@ -658,7 +661,7 @@ static int launch_conv(const Geom& g, const ConvLaunch& c, const uint8_t* wb, co
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.NU * g.tiles;
   dim3 grid(total < num_sms() ? total : num_sms(), p.n_io);
-  fn<<<grid, CONV_THREADS, smem, st>>>(p, m0, m1);
+  fn<<<grid, conv_threads(p.np), smem, st>>>(p, m0, m1);
   return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
 }
 
