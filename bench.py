@@ -32,6 +32,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 S_C2, U_C2, D_S, N_IT = 3276, 2, 56, 2
+DATA = ("synthetic: GPU slot generator on the SURVEY §8d recipe (doubletdl TDL-B/TDL-C Jakes fading, Gray "
+        "16-QAM, per-slot QPSK pilots, AWGN n0=0.1); random-init weights")
 METRIC = "NRX forward slots/s at 273 PRB (2 UE, 4 RX, RT d_s=56 N_it=2); p50/p99 single-slot latency in latency_us"
 
 
@@ -43,18 +45,21 @@ def c2_setup():
     return cfg, config, init_weights(config, seed=0), (table[14], table[14])
 
 
-def host_batch(cfg, n_slots: int, pool: int = 8, seed: int = 0):
-    """(y c64 (N,S,T,B), pilots c64 (N,U,F,K), noise (N,), mods (N*U,)) from a
-    pool of distinct synthetic slots (each with its own pilot book)."""
-    from paper_2409_02912_b200.engine import pilot_comb_values
+def gpu_batch(cfg, n_slots: int, dev, seed: int = 0, first_slot: int = 0):
+    """(y c64 (N,S,T,B), pilots c64 (N,U,F,K), noise feature (N,), mods (N*U,))
+    device tensors of n_slots distinct slots from the GPU slot generator, on
+    the SURVEY.md §8d recipe: doubletdl channels (UE0 TDL-B 400 Hz / 100 ns,
+    UE1 TDL-C 100 Hz / 300 ns, 32-sinusoid Jakes fading, 4 RX x 2 TX with the
+    default beams), Gray 16-QAM on every data RE, per-slot QPSK pilots on
+    each UE's comb, AWGN at n0 = 0.1 (SNR 10 dB)."""
+    import torch
     from paper_2409_02912_b200.nrx import noise_features
-    from paper_2409_02912_b200.synth import synth_slots
-    y, books, _ = synth_slots(cfg, [4] * cfg.num_ues, min(pool, n_slots), 0.1, seed=seed)
-    idx = np.arange(n_slots) % y.shape[0]
-    vals = np.stack([books[i].values for i in idx])
-    pil = pilot_comb_values(vals, cfg).astype(np.complex64)
-    return (np.ascontiguousarray(y[idx]).astype(np.complex64), pil, noise_features(0.1, n_slots),
-            np.full(n_slots * cfg.num_ues, 4, dtype=np.int32))
+    from paper_2409_02912_b200.slotgen import GpuSlotSource
+    src = GpuSlotSource(cfg, device=dev)
+    b = src.generate(n_slots, [4] * cfg.num_ues, 0.1, seed=seed, first_slot=first_slot)
+    nf = torch.from_numpy(noise_features(0.1, n_slots)).to(dev)
+    torch.cuda.synchronize(dev)
+    return b.y, b.pilots, nf, b.mod_order
 
 
 class ClockSampler:
@@ -160,13 +165,34 @@ def reference_impl():
     return nrx_forward, "port"
 
 
+def reference_recipe_slots(cfg, n: int, seed: int = 11):
+    """Host slots of the same SURVEY §8d recipe the GPU arm generates
+    (doubletdl, 16-QAM, per-slot pilots, n0 = 0.1), built from the reference
+    recipe's numpy variates by the CPU generator oracle."""
+    from oracle import slotgen_oracle as so
+    from paper_2409_02912_b200.config import PilotBook
+    from paper_2409_02912_b200.slotgen import doubletdl, reference_variates
+    prof = doubletdl()
+    v = reference_variates(cfg, prof, (4, 4), range(n), seed=seed)
+    ys, books = [], []
+    for i in range(n):
+        y, _ = so.synth_slot(cfg, prof, (4, 4), 0.1, v["angles"][i], v["phases"][i], v["labels"][i],
+                             v["noise"][i], v["pilots"][i])
+        vals = np.zeros((cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols), complex)
+        for u in range(cfg.num_ues):
+            sc = np.arange(u % cfg.comb_size, cfg.num_subcarriers, cfg.comb_size)
+            vals[u][np.ix_(sc, list(cfg.pilot_symbols))] = v["pilots"][i, u, :sc.size]
+        ys.append(y)
+        books.append(PilotBook(values=vals, config=cfg))
+    return np.stack(ys), books
+
+
 def run_reference(args, slots: int, warmup: int):
     """Time the reference CPU path: one slot per call (latency_bench style,
     evaluation.py:341-349) -> slots/s."""
     fwd, kind = reference_impl()
     cfg, config, w, mcs = c2_setup()
-    from paper_2409_02912_b200.synth import synth_slots
-    y, books, _ = synth_slots(cfg, [4, 4], min(slots, 4), 0.1, seed=11)
+    y, books = reference_recipe_slots(cfg, min(slots, 2))
     if kind == "reference":
         # the reference's own types (its isinstance checks need them) and
         # weights as recorded autodiff tensors, exactly as cli.cmd_bench builds them
@@ -232,10 +258,7 @@ def run_ours(args):
 
     # two device-resident input sets, alternated so consecutive steps never
     # re-read the same inputs from L2 (per-step activations are GBs anyway)
-    sets = []
-    for s in range(2):
-        y, pil, nf, mods = host_batch(cfg, B, seed=100 * rank + s)
-        sets.append(tuple(torch.from_numpy(a).to(dev) for a in (y, pil, nf, mods)))
+    sets = [gpu_batch(cfg, B, dev, seed=1, first_slot=(2 * rank + s) * B) for s in range(2)]
     llr = torch.empty((B, U, S, T, 4), dtype=torch.float32, device=dev)
     chest = torch.empty((B, U, S, T, BR), dtype=torch.complex64, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -293,6 +316,9 @@ def run_ours(args):
     # end to end through the public host API: pinned H2D + D2H inside the region
     e2e = e2e_throughput(eng, cfg, B, max(4, args.steps // 2), world, dev)
 
+    # Monte-Carlo pipeline: GPU slot generation -> receiver -> bit-error count
+    mc = monte_carlo_pipeline(eng, cfg, B, max(5, args.steps // 4), world, rank, dev)
+
     # the other precisions on the same device-resident workload (shorter runs)
     by_prec = {args.precision: {"slots_per_s": round(value, 2), "ms_per_step": round(ms_per_step, 4)}}
     if not args.no_precision_sweep:
@@ -327,7 +353,7 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 2), "unit": "slots/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": args.precision, "data": "synthetic (random QAM over Rayleigh multipath, random-init weights)",
+        "dtype": args.precision, "data": DATA,
         "config": {"workload": f"C5-style batches of C2 slots: {B} slots/GPU/step of 273 PRB x 14 sym, "
                                f"2 UE 16-QAM, 4 RX; RT NRX d_s=56 N_it=2 (configs[1] geometry)",
                    "slots_per_step_per_gpu": B, "precision": args.precision,
@@ -336,6 +362,7 @@ def run_ours(args):
         "latency_us": lat,
         "latency_other_configs_us": lat_other,
         "e2e": e2e,
+        "monte_carlo": mc,
         "roofline": {"kernel": "conv_update0 (iteration.update.conv0, 3x3 114->56, implicit GEMM)",
                      "bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 1),
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
@@ -361,7 +388,7 @@ def run_ours(args):
 def latency_single_slot(eng, cfg, dev, runs: int, n_it: int = N_IT, orders=None, width: int = 4,
                         note: str = "one C2 slot"):
     import torch
-    y, pil, nf, mods = (torch.from_numpy(a).to(dev) for a in host_batch(cfg, 1, pool=1, seed=7))
+    y, pil, nf, mods = gpu_batch(cfg, 1, dev, seed=7)
     if orders is not None:
         mods = torch.tensor(orders, dtype=torch.int32, device=dev)
     llr = torch.empty((1, cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, width), dtype=torch.float32,
@@ -432,6 +459,59 @@ def other_config_latencies(precision, dev, runs: int):
     return out
 
 
+def monte_carlo_pipeline(eng, cfg, B, steps, world, rank, dev):
+    """Slots/s of (a) the GPU slot generator alone and (b) the uncoded
+    Monte-Carlo step generate -> nrx_forward -> count_bit_errors, all on the
+    device, B distinct slots per step (the reference builds one such slot on
+    the host in 48.6 ms)."""
+    import torch
+    from paper_2409_02912_b200.nrx import noise_features
+    from paper_2409_02912_b200.shard import max_over_ranks
+    from paper_2409_02912_b200.slotgen import GpuSlotSource, count_bit_errors
+    U, S, T = cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols
+    src = GpuSlotSource(cfg, device=dev)
+    mods = torch.full((B * U,), 4, dtype=torch.int32, device=dev)
+    n0 = torch.full((B,), 0.1, dtype=torch.float64, device=dev)
+    nf = torch.from_numpy(noise_features(0.1, B)).to(dev)
+    llr = torch.empty((B, U, S, T, 4), dtype=torch.float32, device=dev)
+    chest = torch.empty((B, U, S, T, 4), dtype=torch.complex64, device=dev)
+    errs = torch.zeros(B * U, dtype=torch.int64, device=dev)
+    ws = eng.workspace(cfg, B)
+    st = torch.cuda.current_stream(dev)
+    box = {}
+
+    def gen(i):
+        box["b"] = src.generate(B, mods, n0, seed=17, first_slot=(i * world + rank) * B, out=box.get("b"))
+
+    def full(i):
+        gen(i)
+        b = box["b"]
+        eng.forward_device(cfg, b.y, b.pilots, nf, b.mod_order, N_IT, llr, chest, workspace=ws, stream=st)
+        count_bit_errors(cfg, llr, b.labels, b.mod_order, out=errs)
+
+    res = {}
+    for name, fn in (("generate", gen), ("pipeline", full)):
+        for i in range(3):
+            fn(i)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for i in range(steps):
+            fn(3 + i)
+        b.record(st)
+        torch.cuda.synchronize()
+        t = max_over_ranks(a.elapsed_time(b) / 1e3, dev)
+        res[name] = {"slots_per_s": round(B * steps * world / t, 1), "ms_per_step": round(t / steps * 1e3, 4)}
+    bits = cfg.num_data_res * 4 * U
+    return {"generate_slots_per_s": res["generate"]["slots_per_s"],
+            "generate_us_per_slot": round(res["generate"]["ms_per_step"] * 1e3 / B, 2),
+            "pipeline_slots_per_s": res["pipeline"]["slots_per_s"], "steps": steps, "slots_per_step": B,
+            "uncoded_ber_last_steps": round(float(errs.sum().item()) / (bits * B * (steps + 3)), 4),
+            "launches_per_step": 2 + eng.launch_count(cfg, N_IT) + 1,
+            "note": "device Philox variates, doubletdl channels, 16-QAM, n0 = 0.1; random-init receiver, so the "
+                    "BER is ~0.5 by construction"}
+
+
 def e2e_throughput(eng, cfg, B, steps, world, dev):
     """NrxEngine.run_stream: every step copies its inputs (y, pilots, noise,
     MCS) from pinned host memory to the GPU and its LLR + chest grids back to
@@ -439,10 +519,9 @@ def e2e_throughput(eng, cfg, B, steps, world, dev):
     import torch
     import torch.distributed as dist
     U, S, T = cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols
-    hosts = []
-    for s in range(2):
-        arrs = host_batch(cfg, B, seed=3 + s)
-        hosts.append(tuple(torch.from_numpy(a).pin_memory() for a in arrs))
+    rank = dist.get_rank() if world > 1 else 0
+    hosts = [tuple(t.cpu().pin_memory() for t in gpu_batch(cfg, B, dev, seed=3, first_slot=(2 * rank + s) * B))
+             for s in range(2)]
     outs = [(torch.empty((B, U, S, T, 4), dtype=torch.float32).pin_memory(),
              torch.empty((B, U, S, T, 4), dtype=torch.complex64).pin_memory()) for _ in range(2)]
     inputs = [hosts[i & 1] for i in range(steps)]
@@ -499,7 +578,7 @@ def main():
             "impl": "reference", "metric": METRIC, "value": round(res["value"], 4), "unit": "slots/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(secs * 1e3, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
-            "data": "synthetic (random QAM over Rayleigh multipath, random-init weights)", "config": cfg_desc,
+            "data": DATA.replace("GPU slot generator", "host generator"), "config": cfg_desc,
             "latency_us": {"p50": round(res["p50_ms"] * 1e3, 1), "p99": round(res["p99_ms"] * 1e3, 1)},
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "kind", "cores", "sample")},
             "e2e": {"value": round(res["value"], 4), "unit": "slots/s", "h2d_bytes_per_step": 0,

@@ -18,12 +18,15 @@ VARIANT_IDS = {"single": 0, "masking": 1, "var_io": 2}
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnrx_b200.so")
 
-# every symbol include/nrx_b200.h declares
+# every symbol include/nrx_b200.h and include/nrx_slotgen.h declare
 EXPORTED = ("nrx_abi_version", "nrx_status_string", "nrx_validate", "nrx_weight_count",
             "nrx_weight_name", "nrx_weight_numel", "nrx_packed_weight_bytes", "nrx_pack_weights",
             "nrx_workspace_bytes", "nrx_forward", "nrx_buffer_geometry", "nrx_ls_features",
             "nrx_forward_launch_count", "nrx_profile_enable", "nrx_profile_collect",
-            "nrx_profile_disable", "nrx_kernel_name")
+            "nrx_profile_disable", "nrx_kernel_name",
+            # include/nrx_slotgen.h
+            "nrx_synth_validate", "nrx_synth_workspace_bytes", "nrx_synth_slots",
+            "nrx_count_bit_errors", "nrx_philox4x32_10")
 KERNEL_IDS = {"ls_feat": 0, "conv_state_init0": 1, "conv_state_init1": 2, "msg_agg": 3,
               "conv_update0": 4, "conv_update1": 5, "readout": 6}
 
@@ -41,6 +44,28 @@ class SlotDesc(ctypes.Structure):
                 ("num_ues", ctypes.c_int32), ("comb_size", ctypes.c_int32),
                 ("num_pilot_symbols", ctypes.c_int32),
                 ("pilot_symbols", ctypes.c_int32 * NRX_MAX_PILOT_SYMBOLS)]
+
+
+NRX_SG_MAX_UES, NRX_SG_MAX_TAPS, NRX_SG_MAX_UE_ANT = 4, 24, 4
+NRX_SG_QAM_POINTS = 4 + 16 + 64 + 256
+
+
+class TdlProfileDesc(ctypes.Structure):
+    _fields_ = [("num_taps", ctypes.c_int32), ("delays_s", ctypes.c_double * NRX_SG_MAX_TAPS),
+                ("powers", ctypes.c_double * NRX_SG_MAX_TAPS), ("doppler_hz", ctypes.c_double)]
+
+
+class ChannelDesc(ctypes.Structure):
+    _fields_ = [("bs_antennas", ctypes.c_int32), ("ue_antennas", ctypes.c_int32),
+                ("num_sinusoids", ctypes.c_int32), ("subcarrier_spacing_hz", ctypes.c_double),
+                ("cp_fraction", ctypes.c_double),
+                ("beams", ((ctypes.c_double * 2) * NRX_SG_MAX_UE_ANT) * NRX_SG_MAX_UES),
+                ("profiles", TdlProfileDesc * NRX_SG_MAX_UES)]
+
+
+class SlotVariates(ctypes.Structure):
+    _fields_ = [("angles", ctypes.c_void_p), ("phases", ctypes.c_void_p), ("labels", ctypes.c_void_p),
+                ("noise", ctypes.c_void_p), ("pilots", ctypes.c_void_p)]
 
 
 class NrxLibraryError(RuntimeError):
@@ -81,6 +106,14 @@ def load() -> ctypes.CDLL:
     lib.nrx_profile_disable.restype = None
     lib.nrx_kernel_name.argtypes = [I]
     lib.nrx_kernel_name.restype = ctypes.c_char_p
+    lib.nrx_synth_validate.argtypes = [P(SlotDesc), P(ChannelDesc)]
+    lib.nrx_synth_workspace_bytes.argtypes = [P(SlotDesc), P(ChannelDesc), I]
+    lib.nrx_synth_workspace_bytes.restype = Z
+    lib.nrx_synth_slots.argtypes = [P(SlotDesc), P(ChannelDesc), I, ctypes.c_uint64, ctypes.c_uint64, V, V,
+                                    P(SlotVariates), V, V, I, V, I, V, V, I, V, Z, V]
+    lib.nrx_count_bit_errors.argtypes = [P(SlotDesc), I, V, I, V, V, V, V]
+    lib.nrx_philox4x32_10.argtypes = [P(ctypes.c_uint32), P(ctypes.c_uint32), P(ctypes.c_uint32)]
+    lib.nrx_philox4x32_10.restype = None
     if lib.nrx_abi_version() != 1:
         raise NrxLibraryError("libnrx_b200.so ABI version mismatch")
     _LIB = lib

@@ -13,11 +13,11 @@ from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_tabl
 from paper_2409_02912_b200.engine import pack_weights, pilot_comb_values
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "nrx_b200.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("nrx_b200.h", "nrx_slotgen.h")]
 
 
 def declared_functions():
-    text = open(HEADER).read()
+    text = "\n".join(open(h).read() for h in HEADERS)
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(nrx_[a-z0-9_]+)\s*\(", text)))
 
