@@ -16,7 +16,8 @@ NRX_FP32, NRX_BF16, NRX_FP16 = 0, 1, 2
 PRECISIONS = {"fp32": NRX_FP32, "bf16": NRX_BF16, "fp16": NRX_FP16}
 VARIANT_IDS = {"single": 0, "masking": 1, "var_io": 2}
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnrx_b200.so")
+LIB_PATH = os.environ.get("NRX_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                           "libnrx_b200.so")
 
 # every symbol include/nrx_b200.h and include/nrx_slotgen.h declare
 EXPORTED = ("nrx_abi_version", "nrx_status_string", "nrx_validate", "nrx_weight_count",

@@ -34,6 +34,10 @@ namespace nrx {
 namespace tc {
 
 enum ConvTail { TAIL_NONE = 0, TAIL_MSG = 1, TAIL_READOUT = 2 };
+#ifndef NRX_TAIL_BATCH
+#define NRX_TAIL_BATCH 1
+#endif
+constexpr int kTailBatch = NRX_TAIL_BATCH;  // TMEM chunk loads in flight per tail-stage wait
 
 struct ConvTcParams {
   Geom g;
@@ -63,7 +67,6 @@ struct ConvTcParams {
 __host__ __device__ constexpr int conv_parts(int np) { return np / 16; }
 __host__ __device__ constexpr int conv_epi_threads(int np) { return 128 * conv_parts(np); }
 __host__ __device__ constexpr int conv_threads(int np) { return 64 + conv_epi_threads(np); }
-
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   uint32_t r[8];
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
@@ -331,6 +334,8 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       if (it >= 1) issue_fc1(it - 1);
     }
   } else {  // ---------------- epilogue: warps 2 .. 2 + 4*PARTS - 1
+    // bf16 keeps an fp32 master of the state (dst32, STATE_INIT / RESIDUAL); fp16 has none
+    constexpr bool MASTER = std::is_same<ET, __nv_bfloat16>::value;
     constexpr int PARTS = conv_parts(NP);
     constexpr int NC = NP / PARTS;  // = 16 accumulator columns per thread
     const int q = warp & 3, part = (warp - 2) >> 2;
@@ -339,6 +344,16 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     const int nd = p.cdst / 8, n32 = p.d4 / 4;
     const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
     int hist_slab[2] = {0, 0}, hist_tile[2] = {0, 0};  // tiles whose tail outputs are pending
+    const uint32_t ta_s = smem_u32(smem + L.ta), th_s = smem_u32(smem + L.th);
+    // chunks holding no state channel (8 cc >= d) are the positional / zero
+    // channels: constant over the iterations, written once by the state init;
+    // the residual update skips them (and their zero rows in the tail's A tile)
+    const int dch = (g.d + 7) / 8;
+    if (TAIL && MODE == EPI_RESIDUAL && part == PARTS - 1) {
+      for (int b = 0; b < 2; ++b)
+        for (int cc = dch; cc < nd; ++cc)
+          st_shared_u4(ta_s + b * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u, make_uint4(0u, 0u, 0u, 0u));
+    }
 
     // ---- tail stage 2: hidden layer relu(state x W0 + b0) -> smem (fc1's A operand)
     auto tail_hidden = [&](int j) {
@@ -346,15 +361,22 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       mbar_wait(&hid_full[b], (j >> 1) & 1);
       tc_fence_after();
       const int hch = p.thp / 8, hbeg = part * hch / PARTS, hend = (part + 1) * hch / PARTS;
-      uint8_t* H = smem + L.th;  // free: fc1 of the previous tile completed (tail_out ran first)
-      for (int c8 = hbeg; c8 < hend; ++c8) {
-        float hv[8];
-        tmem_ld8(tmem_base + lane_off + col_h + b * p.thp + 8 * c8, hv);
-        tmem_wait_ld();
-        float o[8];
+      // TH is free: fc1 of the previous tile completed (tail_out ran first)
+      for (int c0 = hbeg; c0 < hend; c0 += kTailBatch) {  // all TMEM loads of a batch, one wait
+        float hv[kTailBatch][8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = fmaxf(hv[e] + stb0[8 * c8 + e], 0.f);
-        store_chunk(reinterpret_cast<ET*>(H + ((size_t)c8 * NRX_TILE_M + r) * 16), o);
+        for (int k = 0; k < kTailBatch; ++k)
+          if (c0 + k < hend) tmem_ld8(tmem_base + lane_off + col_h + b * p.thp + 8 * (c0 + k), hv[k]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < kTailBatch; ++k) {
+          if (c0 + k >= hend) break;
+          const int c8 = c0 + k;
+          float o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] = fmaxf(hv[k][e] + stb0[8 * c8 + e], 0.f);
+          st_shared_u4(th_s + (uint32_t)(c8 * NRX_TILE_M + r) * 16u, pack_chunk(o, static_cast<const ET*>(nullptr)));
+        }
       }
       fence_proxy_async();
       tc_fence_before();
@@ -372,17 +394,24 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       if (TAIL == TAIL_MSG) {  // messages of this slab, zero on pad rows/channels
         ET* const msg = static_cast<ET*>(p.msg);
         const int och = g.Ca / 8, obeg = part * och / PARTS, oend = (part + 1) * och / PARTS;
-        for (int cc = obeg; cc < oend; ++cc) {
-          float mv[8];
-          tmem_ld8(tcol + 8 * cc, mv);
-          tmem_wait_ld();
-          float o[8];
+        for (int c0 = obeg; c0 < oend; c0 += kTailBatch) {
+          float mv[kTailBatch][8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int c = 8 * cc + e;
-            o[e] = (valid && c < g.d) ? mv[e] + stb1[c] : 0.f;
+          for (int k = 0; k < kTailBatch; ++k)
+            if (c0 + k < oend) tmem_ld8(tcol + 8 * (c0 + k), mv[k]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < kTailBatch; ++k) {
+            if (c0 + k >= oend) break;
+            const int cc = c0 + k;
+            float o[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int c = 8 * cc + e;
+              o[e] = (valid && c < g.d) ? mv[k][e] + stb1[c] : 0.f;
+            }
+            store_chunk(chunk_ptr(msg, jslab, och, cc, row, g), o);
           }
-          store_chunk(chunk_ptr(msg, jslab, och, cc, row, g), o);
         }
       } else if (part == 0) {  // LLRs (masked width) + planar-decoded chest
         float o[32];
@@ -428,25 +457,13 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     while (w.next(slab, tile)) {
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
-      NRX_T(t0);
-      mbar_wait(&tfull[acc], aph);
-      NRX_TADD(t_a, t0);
-      NRX_T(t1);
-      tc_fence_after();
-      float v[NC];
-      const uint32_t taddr = tmem_base + lane_off + acc * NP + cbase;
-#pragma unroll
-      for (int c = 0; c < NC / 8; ++c) tmem_ld8(taddr + 8 * c, v + 8 * c);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
-
       const int row = tile * NRX_TILE_M + r;
       const int s = row / g.Tp, t = row - s * g.Tp;
       const bool valid = row < g.rows_data && t < g.T;
-      float old[NC];
-      if (MODE == EPI_RESIDUAL) {  // residual input: issue every load before use
-        if (p.dst32) {             // bf16 path: fp32 residual stream
+      float old[MASTER ? NC : 1];
+      uint4 raw[MASTER ? 1 : NC / 8];
+      if (MODE == EPI_RESIDUAL) {  // residual input: loads issued before the accumulator wait
+        if (MASTER) {             // bf16 path: fp32 residual stream
 #pragma unroll
           for (int c4 = 0; c4 < NC / 4; ++c4) {
             const int cc = cbase / 4 + c4;
@@ -458,50 +475,74 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
             old[4 * c4 + 3] = o.w;
           }
         } else {                   // fp16 path: the state buffer itself
-          uint4 raw[NC / 8];
 #pragma unroll
           for (int c8 = 0; c8 < NC / 8; ++c8) {
             const int cc = cbase / 8 + c8;
-            raw[c8] = (valid && cc < nd) ? *reinterpret_cast<const uint4*>(chunk_ptr(dst, slab, nd, cc, row, g))
-                                         : make_uint4(0u, 0u, 0u, 0u);
-          }
-#pragma unroll
-          for (int c8 = 0; c8 < NC / 8; ++c8) unpack_chunk(raw[c8], static_cast<const ET*>(nullptr), old + 8 * c8);
-        }
-      }
-      float x[NC];
-#pragma unroll
-      for (int j = 0; j < NC; ++j) {
-        const int c = cbase + j;
-        float y = v[j] + sbias[c];  // conv + bias first, as the reference adds them
-        if (MODE == EPI_RELU) y = fmaxf(y, 0.f);
-        if (MODE == EPI_RESIDUAL) y = old[j] + y;
-        x[j] = (valid && c < g.d) ? y : 0.f;
-      }
-      if (MODE != EPI_RELU) {
-        if (p.dst32) {
-#pragma unroll
-          for (int c4 = 0; c4 < NC / 4; ++c4) {
-            const int cc = cbase / 4 + c4;
-            if (cc < n32) store_chunk(chunk_ptr(p.dst32, slab, n32, cc, row, g), x + 4 * c4);
-          }
-        }
-        if (valid) {  // positional channels d, d+1 of the half-precision operand copy
-          const float pdt = g.dt[t], pdf = pos_df(s, slab % g.U, g);
-#pragma unroll
-          for (int j = 0; j < NC; ++j) {
-            const int c = cbase + j;
-            if (c == g.d) x[j] = pdt;
-            if (c == g.d + 1) x[j] = pdf;
+            raw[c8] = (valid && cc < dch) ? *reinterpret_cast<const uint4*>(chunk_ptr(dst, slab, nd, cc, row, g))
+                                          : make_uint4(0u, 0u, 0u, 0u);
           }
         }
       }
+      NRX_T(t0);
+      mbar_wait(&tfull[acc], aph);
+      NRX_TADD(t_a, t0);
+      NRX_T(t1);
+      tc_fence_after();
+      float v[NC];
+      const uint32_t taddr = tmem_base + lane_off + acc * NP + cbase;
+#ifdef NRX_CONV_LD_EACH
 #pragma unroll
-      for (int c8 = 0; c8 < NC / 8; ++c8) {
+      for (int c = 0; c < NC / 8; ++c) {
+        tmem_ld8(taddr + 8 * c, v + 8 * c);
+        tmem_wait_ld();
+      }
+#else
+#pragma unroll
+      for (int c = 0; c < NC / 8; ++c) tmem_ld8(taddr + 8 * c, v + 8 * c);
+      tmem_wait_ld();
+#endif
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+
+      // positional channels only where a written chunk holds them
+      const int clo = cbase / 8, chi = cbase / 8 + NC / 8;
+      const bool need_pos = MODE != EPI_RELU && valid && (MODE != EPI_RESIDUAL || g.d % 8 != 0) &&
+                            ((g.d / 8 >= clo && g.d / 8 < chi) || ((g.d + 1) / 8 >= clo && (g.d + 1) / 8 < chi));
+      const float pdt = need_pos ? g.dt[t] : 0.f;
+      const float pdf = need_pos ? pos_df(s, slab % g.U, g) : 0.f;
+#pragma unroll
+      for (int c8 = 0; c8 < NC / 8; ++c8) {  // one 8-channel chunk at a time (few live registers)
         const int cc = cbase / 8 + c8;
+        if (MODE == EPI_RESIDUAL && cc >= dch) continue;   // constant positional / zero chunk
+        float o8[8];
+        if (MODE == EPI_RESIDUAL && !MASTER) unpack_chunk(raw[c8], static_cast<const ET*>(nullptr), o8);
+        float* x = v + 8 * c8;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int c = 8 * cc + e;
+          float y = x[e] + sbias[c];  // conv + bias first, as the reference adds them
+          if (MODE == EPI_RELU) y = fmaxf(y, 0.f);
+          if (MODE == EPI_RESIDUAL) y = (MASTER ? old[8 * c8 + e] : o8[e]) + y;
+          x[e] = (valid && c < g.d) ? y : 0.f;
+        }
+        if (MODE != EPI_RELU) {
+          if (MASTER) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (2 * cc + h < n32) store_chunk(chunk_ptr(p.dst32, slab, n32, 2 * cc + h, row, g), x + 4 * h);
+          }
+          // positional channels d, d+1 of the half-precision operand copy
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int c = 8 * cc + e;
+            if (valid && c == g.d) x[e] = pdt;
+            if (valid && c == g.d + 1) x[e] = pdf;
+          }
+        }
         if (cc < nd) {
-          store_chunk(chunk_ptr(dst, slab, nd, cc, row, g), x + 8 * c8);
-          if (TAIL) store_chunk(reinterpret_cast<ET*>(smem + L.ta + (it & 1) * ta_bytes + ((size_t)cc * NRX_TILE_M + r) * 16), x + 8 * c8);
+          const uint4 qx = pack_chunk(x, static_cast<const ET*>(nullptr));
+          *reinterpret_cast<uint4*>(chunk_ptr(dst, slab, nd, cc, row, g)) = qx;
+          if (TAIL) st_shared_u4(ta_s + (it & 1) * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u, qx);
         }
       }
       if (part == PARTS - 1) {  // buffer channels beyond the accumulator: positional / zero only
@@ -511,7 +552,8 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
           for (int e = 0; e < 8; ++e)
             o[e] = (valid && MODE != EPI_RELU) ? state_extra(8 * cc + e, s, t, slab % g.U, g) : 0.f;
           store_chunk(chunk_ptr(dst, slab, nd, cc, row, g), o);
-          if (TAIL) store_chunk(reinterpret_cast<ET*>(smem + L.ta + (it & 1) * ta_bytes + ((size_t)cc * NRX_TILE_M + r) * 16), o);
+          if (TAIL) st_shared_u4(ta_s + (it & 1) * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u,
+                                 pack_chunk(o, static_cast<const ET*>(nullptr)));
         }
       }
       if (TAIL) {

@@ -78,6 +78,23 @@ __device__ __forceinline__ void store_chunk(__half* p, const float* v) {
   *reinterpret_cast<uint4*>(p) = q;
 }
 
+// 8 channel values as one packed 16-byte half-precision chunk, and a store
+// of it to a shared-memory address (no generic-to-shared conversion).
+__device__ __forceinline__ uint4 pack_chunk(const float* v, const __nv_bfloat16*) {
+  return make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                    pack_bf16x2(v[6], v[7]));
+}
+__device__ __forceinline__ uint4 pack_chunk(const float* v, const __half*) {
+  __half2 h[4] = {__floats2half2_rn(v[0], v[1]), __floats2half2_rn(v[2], v[3]), __floats2half2_rn(v[4], v[5]),
+                  __floats2half2_rn(v[6], v[7])};
+  return make_uint4(*reinterpret_cast<uint32_t*>(&h[0]), *reinterpret_cast<uint32_t*>(&h[1]),
+                    *reinterpret_cast<uint32_t*>(&h[2]), *reinterpret_cast<uint32_t*>(&h[3]));
+}
+__device__ __forceinline__ void st_shared_u4(uint32_t addr, uint4 q) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(q.x), "r"(q.y), "r"(q.z), "r"(q.w)
+               : "memory");
+}
+
 // Unpack one 16-byte chunk of 8 half-precision channels (type tag selects
 // bf16 or fp16) into floats.
 __device__ __forceinline__ void unpack_chunk(uint4 q, const __nv_bfloat16*, float* v) {

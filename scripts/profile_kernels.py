@@ -23,7 +23,7 @@ cfg, config, w, _ = bench.c2_setup()
 dev = torch.device("cuda", 0)
 eng = NrxEngine(config, w, precision=args.precision, device=dev)
 B = args.slots
-y, pil, nf, mods = (torch.from_numpy(a).to(dev) for a in bench.host_batch(cfg, B))
+y, pil, nf, mods = bench.gpu_batch(cfg, B, dev)
 U, S, T = cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols
 llr = torch.empty((B, U, S, T, 4), dtype=torch.float32, device=dev)
 chest = torch.empty((B, U, S, T, 4), dtype=torch.complex64, device=dev)
