@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
     int hist_slab[2] = {0, 0}, hist_tile[2] = {0, 0};  // tiles whose tail outputs are pending
     const uint32_t ta_s = smem_u32(smem + L.ta), th_s = smem_u32(smem + L.th);
+    const uint32_t sbias_s = smem_u32(sbias), stb0_s = smem_u32(stb0), stb1_s = smem_u32(stb1);
     // chunks holding no state channel (8 cc >= d) are the positional / zero
     // channels: constant over the iterations, written once by the state init;
     // the residual update skips them (and their zero rows in the tail's A tile)
@@ -362,21 +363,15 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       tc_fence_after();
       const int hch = p.thp / 8, hbeg = part * hch / PARTS, hend = (part + 1) * hch / PARTS;
       // TH is free: fc1 of the previous tile completed (tail_out ran first)
-      for (int c0 = hbeg; c0 < hend; c0 += kTailBatch) {  // all TMEM loads of a batch, one wait
-        float hv[kTailBatch][8];
-#pragma unroll
-        for (int k = 0; k < kTailBatch; ++k)
-          if (c0 + k < hend) tmem_ld8(tmem_base + lane_off + col_h + b * p.thp + 8 * (c0 + k), hv[k]);
+      for (int c8 = hbeg; c8 < hend; ++c8) {
+        float hv[8], bb[8];
+        tmem_ld8(tmem_base + lane_off + col_h + b * p.thp + 8 * c8, hv);
+        ld_shared_f8(stb0_s + 32u * c8, bb);
         tmem_wait_ld();
+        float o[8];
 #pragma unroll
-        for (int k = 0; k < kTailBatch; ++k) {
-          if (c0 + k >= hend) break;
-          const int c8 = c0 + k;
-          float o[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) o[e] = fmaxf(hv[k][e] + stb0[8 * c8 + e], 0.f);
-          st_shared_u4(th_s + (uint32_t)(c8 * NRX_TILE_M + r) * 16u, pack_chunk(o, static_cast<const ET*>(nullptr)));
-        }
+        for (int e = 0; e < 8; ++e) o[e] = fmaxf(hv[e] + bb[e], 0.f);
+        st_shared_u4(th_s + (uint32_t)(c8 * NRX_TILE_M + r) * 16u, pack_chunk(o, static_cast<const ET*>(nullptr)));
       }
       fence_proxy_async();
       tc_fence_before();
@@ -388,30 +383,27 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       mbar_wait(&tout_full[b], (j >> 1) & 1);
       tc_fence_after();
       const int row = jtile * NRX_TILE_M + r;
-      const int s = row / g.Tp, t = row - s * g.Tp;
+      int s, t;
+      row_to_st(row, g, s, t);
       const bool valid = row < g.rows_data && t < g.T;
       const uint32_t tcol = tmem_base + lane_off + col_o + b * p.top;
       if (TAIL == TAIL_MSG) {  // messages of this slab, zero on pad rows/channels
-        ET* const msg = static_cast<ET*>(p.msg);
         const int och = g.Ca / 8, obeg = part * och / PARTS, oend = (part + 1) * och / PARTS;
-        for (int c0 = obeg; c0 < oend; c0 += kTailBatch) {
-          float mv[kTailBatch][8];
-#pragma unroll
-          for (int k = 0; k < kTailBatch; ++k)
-            if (c0 + k < oend) tmem_ld8(tcol + 8 * (c0 + k), mv[k]);
+        ET* const mrow = chunk_ptr(static_cast<ET*>(p.msg), jslab, och, 0, row, g);
+        for (int cc = obeg; cc < oend; ++cc) {
+          float mv[8], bb[8];
+          tmem_ld8(tcol + 8 * cc, mv);
+          ld_shared_f8(stb1_s + 32u * cc, bb);
           tmem_wait_ld();
+          float o[8];
+          if (8 * cc + 8 <= g.d) {  // warp-uniform: every channel of the chunk is a message channel
 #pragma unroll
-          for (int k = 0; k < kTailBatch; ++k) {
-            if (c0 + k >= oend) break;
-            const int cc = c0 + k;
-            float o[8];
+            for (int e = 0; e < 8; ++e) o[e] = valid ? mv[e] + bb[e] : 0.f;
+          } else {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int c = 8 * cc + e;
-              o[e] = (valid && c < g.d) ? mv[k][e] + stb1[c] : 0.f;
-            }
-            store_chunk(chunk_ptr(msg, jslab, och, cc, row, g), o);
+            for (int e = 0; e < 8; ++e) o[e] = (valid && 8 * cc + e < g.d) ? mv[e] + bb[e] : 0.f;
           }
+          *reinterpret_cast<uint4*>(mrow + (size_t)cc * g.rows_slab * 8) = pack_chunk(o, static_cast<const ET*>(nullptr));
         }
       } else if (part == 0) {  // LLRs (masked width) + planar-decoded chest
         float o[32];
@@ -458,7 +450,8 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       const int row = tile * NRX_TILE_M + r;
-      const int s = row / g.Tp, t = row - s * g.Tp;
+      int s, t;
+      row_to_st(row, g, s, t);
       const bool valid = row < g.rows_data && t < g.T;
       float old[MASTER ? NC : 1];
       uint4 raw[MASTER ? 1 : NC / 8];
@@ -478,8 +471,9 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
 #pragma unroll
           for (int c8 = 0; c8 < NC / 8; ++c8) {
             const int cc = cbase / 8 + c8;
-            raw[c8] = (valid && cc < dch) ? *reinterpret_cast<const uint4*>(chunk_ptr(dst, slab, nd, cc, row, g))
-                                          : make_uint4(0u, 0u, 0u, 0u);
+            raw[c8] = (valid && cc < dch)
+                          ? *reinterpret_cast<const uint4*>(chunk_ptr(dst, slab, nd, 0, row, g) + (size_t)cc * g.rows_slab * 8)
+                          : make_uint4(0u, 0u, 0u, 0u);
           }
         }
       }
@@ -510,20 +504,23 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
                             ((g.d / 8 >= clo && g.d / 8 < chi) || ((g.d + 1) / 8 >= clo && (g.d + 1) / 8 < chi));
       const float pdt = need_pos ? g.dt[t] : 0.f;
       const float pdf = need_pos ? pos_df(s, slab % g.U, g) : 0.f;
+      ET* const drow = chunk_ptr(dst, slab, nd, 0, row, g);
+      const size_t dcs = (size_t)g.rows_slab * 8;  // chunk stride of a half-precision buffer
 #pragma unroll
       for (int c8 = 0; c8 < NC / 8; ++c8) {  // one 8-channel chunk at a time (few live registers)
         const int cc = cbase / 8 + c8;
         if (MODE == EPI_RESIDUAL && cc >= dch) continue;   // constant positional / zero chunk
-        float o8[8];
+        float o8[8], bb[8];
         if (MODE == EPI_RESIDUAL && !MASTER) unpack_chunk(raw[c8], static_cast<const ET*>(nullptr), o8);
+        ld_shared_f8(sbias_s + 32u * cc, bb);
         float* x = v + 8 * c8;
+        const bool full = 8 * cc + 8 <= g.d;  // warp-uniform
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int c = 8 * cc + e;
-          float y = x[e] + sbias[c];  // conv + bias first, as the reference adds them
+          float y = x[e] + bb[e];  // conv + bias first, as the reference adds them
           if (MODE == EPI_RELU) y = fmaxf(y, 0.f);
           if (MODE == EPI_RESIDUAL) y = (MASTER ? old[8 * c8 + e] : o8[e]) + y;
-          x[e] = (valid && c < g.d) ? y : 0.f;
+          x[e] = (valid && (full || 8 * cc + e < g.d)) ? y : 0.f;
         }
         if (MODE != EPI_RELU) {
           if (MASTER) {
@@ -531,17 +528,18 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
             for (int h = 0; h < 2; ++h)
               if (2 * cc + h < n32) store_chunk(chunk_ptr(p.dst32, slab, n32, 2 * cc + h, row, g), x + 4 * h);
           }
-          // positional channels d, d+1 of the half-precision operand copy
+          if (!full) {  // positional channels d, d+1 of the half-precision operand copy
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int c = 8 * cc + e;
-            if (valid && c == g.d) x[e] = pdt;
-            if (valid && c == g.d + 1) x[e] = pdf;
+            for (int e = 0; e < 8; ++e) {
+              const int c = 8 * cc + e;
+              if (valid && c == g.d) x[e] = pdt;
+              if (valid && c == g.d + 1) x[e] = pdf;
+            }
           }
         }
         if (cc < nd) {
           const uint4 qx = pack_chunk(x, static_cast<const ET*>(nullptr));
-          *reinterpret_cast<uint4*>(chunk_ptr(dst, slab, nd, cc, row, g)) = qx;
+          *reinterpret_cast<uint4*>(drow + cc * dcs) = qx;
           if (TAIL) st_shared_u4(ta_s + (it & 1) * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u, qx);
         }
       }

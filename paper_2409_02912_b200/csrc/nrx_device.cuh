@@ -37,6 +37,15 @@ __device__ __forceinline__ float state_extra(int c, int s, int t, int u, const G
   return 0.f;
 }
 
+// Grid row -> (subcarrier s, padded symbol t).  floor((row + 1/2) / Tp) by
+// one float multiply: the fractional part of (row + 1/2) / Tp stays >= 1/(2 Tp)
+// from an integer and the product's error is below row / Tp * 2^-22, so the
+// result is exact for rows < 2^21 (make_geom enforces it).
+__device__ __forceinline__ void row_to_st(int row, const Geom& g, int& s, int& t) {
+  s = __float2int_rz((static_cast<float>(row) + 0.5f) * g.inv_Tp);
+  t = row - s * g.Tp;
+}
+
 // Address of the 16-byte chunk (slab, chunk, row) of a chunk-planar buffer.
 template <typename T>
 __device__ __forceinline__ T* chunk_ptr(T* base, int slab, int nchunks, int chunk, int row, const Geom& g) {

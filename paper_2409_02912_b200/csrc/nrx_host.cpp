@@ -104,10 +104,12 @@ int make_geom(const nrx_model_desc* m, const nrx_slot_desc* s, int n_slots, int 
   g->ks = m->kernel_size;
   g->r = m->kernel_size / 2;
   g->Tp = g->T + g->r;
+  g->inv_Tp = 1.0f / (float)g->Tp;
   g->H = g->r * g->Tp + g->r;
   g->rows_data = g->S * g->Tp;
   g->rows_slab = rup(g->rows_data, NRX_TILE_M);
   g->tiles = g->rows_slab / NRX_TILE_M;
+  if (g->rows_slab >= (1 << 21)) return NRX_ERR_UNSUPPORTED;   // row_to_st exactness bound
   g->d = m->d_s;
   g->h = m->hidden;
   g->prec = prec;

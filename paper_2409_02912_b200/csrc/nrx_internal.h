@@ -35,6 +35,7 @@ struct Geom {
   int N, U, NU, S, T, B, comb, K;
   int ps[NRX_MAX_PILOT_SYMBOLS];
   int ks, r, Tp, H;           // kernel size, radius, padded symbols, halo rows
+  float inv_Tp;               // 1 / Tp: row -> (s, t) by one multiply (rows < 2^21)
   int rows_data, rows_slab, tiles;
   int d, h;                   // state depth, MLP hidden width
   int cw;                     // elements per 16-byte chunk

@@ -33,6 +33,17 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+// 8 consecutive fp32 values (e.g. a bias chunk) from a 16-B aligned shared address
+__device__ __forceinline__ void ld_shared_f8(uint32_t addr, float* b) {
+  const float4 lo = ld_shared_f4(addr), hi = ld_shared_f4(addr + 16);
+  b[0] = lo.x; b[1] = lo.y; b[2] = lo.z; b[3] = lo.w;
+  b[4] = hi.x; b[5] = hi.y; b[6] = hi.z; b[7] = hi.w;
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -40,6 +51,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef NRX_MBAR_SUSPEND_NS
+#define NRX_MBAR_SUSPEND_NS 0
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -51,10 +65,28 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps in the barrier
+// unit instead of spinning (issue slots stay with the working warps).
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(NRX_MBAR_SUSPEND_NS)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+#if NRX_MBAR_SUSPEND_NS > 0
+  while (!mbar_try_wait_sleep(a, parity)) {
+  }
+#else
   while (!mbar_try_wait(a, parity)) {
   }
+#endif
 }
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -185,23 +217,34 @@ __device__ __forceinline__ uint32_t tmem_cols_pow2(uint32_t n) {
 // ---------------------------------------------------------------------------
 
 struct WorkIter {
-  int t, stride, total, tps, n_io, io;
+  int u, tl, stride, units, tps, n_io, io;
+  bool first;
   const int32_t* mod;
   const Geom* g;
-  __device__ WorkIter(const Geom& geo, int units, int tiles_per_unit, int n_io_sets, const int32_t* mods)
-      : t(blockIdx.x), stride(gridDim.x), total(units * tiles_per_unit), tps(tiles_per_unit), n_io(n_io_sets),
-        io(blockIdx.y), mod(mods), g(&geo) {}
-  // next (unit, tile) owned by this CTA; units are slabs (or slots)
+  __device__ WorkIter(const Geom& geo, int n_units, int tiles_per_unit, int n_io_sets, const int32_t* mods)
+      : u(0), tl(0), stride(gridDim.x), units(n_units), tps(tiles_per_unit), n_io(n_io_sets), io(blockIdx.y),
+        first(true), mod(mods), g(&geo) {}
+  // next (unit, tile) owned by this CTA (flat index blockIdx.x + k * gridDim.x);
+  // units are slabs (or slots).  Incremental: one division on the first call.
   __device__ bool next(int& unit, int& tile) {
-    while (t < total) {
-      const int u = t / tps, tl = t - u * tps;
-      t += stride;
+    while (true) {
+      if (first) {
+        first = false;
+        u = blockIdx.x / tps;
+        tl = blockIdx.x - u * tps;
+      } else {
+        tl += stride;
+        while (tl >= tps) {
+          tl -= tps;
+          ++u;
+        }
+      }
+      if (u >= units) return false;
       if (n_io > 1 && io_index(mod, u, *g) != io) continue;
       unit = u;
       tile = tl;
       return true;
     }
-    return false;
   }
 };
 
