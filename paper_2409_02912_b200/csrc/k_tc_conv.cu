@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   const ConvSmem L = conv_smem_layout(p, TAIL);
   uint8_t* Ws = smem + L.w;
   uint8_t* As = smem + L.a;
+  const uint32_t As_s = smem_u32(As);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* full = bars;
   uint64_t* empty = bars + 8;
@@ -138,6 +139,10 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   uint64_t* h_ready = bars + 25;    // [2] tail: hidden layer in shared memory
   uint64_t* tout_full = bars + 27;  // [2] tail: fc1 done
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L.tmem_ptr);
+  // shared-space addresses of the barriers (8 B each)
+  const uint32_t B_full = smem_u32(full), B_empty = smem_u32(empty), B_tfull = smem_u32(tfull),
+                 B_tempty = smem_u32(tempty), B_wbar = smem_u32(wbar), B_ta_ready = smem_u32(ta_ready),
+                 B_hid_full = smem_u32(hid_full), B_h_ready = smem_u32(h_ready), B_tout_full = smem_u32(tout_full);
   float* sbias = reinterpret_cast<float*>(smem + L.sbias);
   float* stb0 = reinterpret_cast<float*>(smem + L.tb0);
   float* stb1 = reinterpret_cast<float*>(smem + L.tb1);
@@ -203,10 +208,10 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         const int grp0 = (tile * NRX_TILE_M - p.hup) / 16;  // 16-row groups
         for (int src = 0; src < (p.c1 ? 2 : 1); ++src) {
           NRX_T(t0);
-          mbar_wait(&empty[st], ph ^ 1);
+          mbar_wait(B_empty + 8u * (st), ph ^ 1);
           NRX_TADD(t_a, t0);
-          mbar_expect_tx(&full[st], (uint32_t)(src ? p.c1 : p.c0) * R * 2);
-          tma_load_4d(As + (size_t)st * p.abytes, src ? &map1 : &map0, &full[st], 0, grp0, 0,
+          mbar_expect_tx(B_full + 8u * (st), (uint32_t)(src ? p.c1 : p.c0) * R * 2);
+          tma_load_4d(As_s + st * p.abytes, src ? &map1 : &map0, B_full + 8u * (st), 0, grp0, 0,
                       src ? (slab ^ p.src1_xor) : slab);
           if (++st == p.stages) { st = 0; ph ^= 1; }
         }
@@ -232,7 +237,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     auto issue_fc0 = [&](int j) {
       const int b = j & 1;
       const uint32_t id0 = idesc_f16kind<ET>(NRX_TILE_M, p.thp);
-      mbar_wait(&ta_ready[b], (j >> 1) & 1);
+      mbar_wait(B_ta_ready + 8u * (b), (j >> 1) & 1);
       tc_fence_after();
       uint64_t ad = smem_desc(smem_u32(smem + L.ta + b * ta_bytes), NRX_TILE_M * 16, 128);
       uint64_t bd = smem_desc(smem_u32(smem + L.tw0), p.thp * 16, 128);
@@ -241,12 +246,12 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         ad += 2 * NRX_TILE_M;
         bd += 2 * p.thp;
       }
-      mma_commit_warp(&hid_full[b]);
+      mma_commit_warp(B_hid_full + 8u * (b));
     };
     auto issue_fc1 = [&](int j) {
       const int b = j & 1;
       const uint32_t id1 = idesc_f16kind<ET>(NRX_TILE_M, p.top);
-      mbar_wait(&h_ready[b], (j >> 1) & 1);
+      mbar_wait(B_h_ready + 8u * (b), (j >> 1) & 1);
       tc_fence_after();
       uint64_t ad = smem_desc(smem_u32(smem + L.th), NRX_TILE_M * 16, 128);
       uint64_t bd = smem_desc(smem_u32(smem + L.tw1), p.top * 16, 128);
@@ -255,9 +260,9 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         ad += 2 * NRX_TILE_M;
         bd += 2 * p.top;
       }
-      mma_commit_warp(&tout_full[b]);
+      mma_commit_warp(B_tout_full + 8u * (b));
     };
-    mbar_wait(wbar, 0);
+    mbar_wait(B_wbar, 0);
     tc_fence_after();
     WorkIter w(g, g.NU, g.tiles, p.n_io, p.mod_order);
     int slab, tile, st = 0, it = 0;
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       NRX_T(t0);
-      mbar_wait(&tempty[acc], aph ^ 1);
+      mbar_wait(B_tempty + 8u * (acc), aph ^ 1);
       NRX_TADD(t_a, t0);
       tc_fence_after();
       const uint32_t d = tmem_base + acc * NP;
@@ -277,10 +282,10 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
 #pragma unroll
         for (int src = 0; src < (NK1 > 0 ? 2 : 1); ++src) {
           NRX_T(t1);
-          mbar_wait(&full[st], ph);
+          mbar_wait(B_full + 8u * (st), ph);
           NRX_TADD(t_b, t1);
           tc_fence_after();
-          const uint64_t a_stage = a_desc0 + ((smem_u32(As + (size_t)st * p.abytes) >> 4) + p.hup);
+          const uint64_t a_stage = a_desc0 + (((As_s + st * p.abytes) >> 4) + p.hup);
           constexpr int KCH = 2 * (NK0 + NK1);
           const int nk = src ? NK1 : NK0, kc0 = src ? 2 * NK0 : 0;
 #pragma unroll
@@ -292,16 +297,16 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
                               b_desc0 + (uint32_t)((tap * KCH + kc0 + 2 * k) * NP), idesc, (src | tap | k) != 0);
             }
           }
-          mma_commit_warp(&empty[st]);
+          mma_commit_warp(B_empty + 8u * (st));
           if (++st == p.stages) { st = 0; ph ^= 1; }
         }
       } else {
         for (int src = 0; src < (p.c1 ? 2 : 1); ++src) {
           NRX_T(t1);
-          mbar_wait(&full[st], ph);
+          mbar_wait(B_full + 8u * (st), ph);
           NRX_TADD(t_b, t1);
           tc_fence_after();
-          const uint32_t a_stage = (smem_u32(As + (size_t)st * p.abytes) >> 4) + p.hup;
+          const uint32_t a_stage = ((As_s + st * p.abytes) >> 4) + p.hup;
           const int kc0 = src ? p.c0 / 8 : 0, nks = (src ? p.c1 : p.c0) / 16;
           uint32_t b_tap = (uint32_t)kc0 * NP;
           for (int ta = 0; ta < g.ks; ++ta) {
@@ -318,11 +323,11 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
               b_tap += (uint32_t)kch * NP;
             }
           }
-          mma_commit_warp(&empty[st]);
+          mma_commit_warp(B_empty + 8u * (st));
           if (++st == p.stages) { st = 0; ph ^= 1; }
         }
       }
-      mma_commit_warp(&tfull[acc]);
+      mma_commit_warp(B_tfull + 8u * (acc));
       // earlier tiles' MLP tails run while this tile's conv MMAs execute
       if (TAIL && it >= 1) issue_fc0(it - 1);
       if (TAIL && it >= 2) issue_fc1(it - 2);
@@ -359,7 +364,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     // ---- tail stage 2: hidden layer relu(state x W0 + b0) -> smem (fc1's A operand)
     auto tail_hidden = [&](int j) {
       const int b = j & 1;
-      mbar_wait(&hid_full[b], (j >> 1) & 1);
+      mbar_wait(B_hid_full + 8u * (b), (j >> 1) & 1);
       tc_fence_after();
       const int hch = p.thp / 8, hbeg = part * hch / PARTS, hend = (part + 1) * hch / PARTS;
       // TH is free: fc1 of the previous tile completed (tail_out ran first)
@@ -375,12 +380,12 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       }
       fence_proxy_async();
       tc_fence_before();
-      mbar_arrive(&h_ready[b]);
+      mbar_arrive(B_h_ready + 8u * (b));
     };
     // ---- tail stage 3: outputs of tile j (+b1): messages, or LLRs + chest
     auto tail_out = [&](int j, int jslab, int jtile) {
       const int b = j & 1;
-      mbar_wait(&tout_full[b], (j >> 1) & 1);
+      mbar_wait(B_tout_full + 8u * (b), (j >> 1) & 1);
       tc_fence_after();
       const int row = jtile * NRX_TILE_M + r;
       int s, t;
@@ -478,7 +483,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         }
       }
       NRX_T(t0);
-      mbar_wait(&tfull[acc], aph);
+      mbar_wait(B_tfull + 8u * (acc), aph);
       NRX_TADD(t_a, t0);
       NRX_T(t1);
       tc_fence_after();
@@ -496,7 +501,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       tmem_wait_ld();
 #endif
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      mbar_arrive(B_tempty + 8u * (acc));
 
       // positional channels only where a written chunk holds them
       const int clo = cbase / 8, chi = cbase / 8 + NC / 8;
@@ -557,7 +562,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       if (TAIL) {
         fence_proxy_async();  // state tile (generic-proxy stores) -> tensor-core reads
         tc_fence_before();
-        mbar_arrive(&ta_ready[it & 1]);
+        mbar_arrive(B_ta_ready + 8u * (it & 1));
         // pipelined tail stages: outputs of tile it-2 (frees the hidden tile),
         // then the hidden layer of tile it-1
         if (it >= 2) tail_out(it - 2, hist_slab[it & 1], hist_tile[it & 1]);
