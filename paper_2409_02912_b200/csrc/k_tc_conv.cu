@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   const uint32_t ta_bytes = (uint32_t)g.Cs * NRX_TILE_M * 2, th_bytes = (uint32_t)p.thp * NRX_TILE_M * 2;
   const int R = p.rbox;
 #ifdef NRX_TIMING
-  long long t_a = 0, t_b = 0, t_c = 0, t_all = clock64();
+  long long t_a = 0, t_b = 0, t_c = 0, t_d = 0, t_all = clock64();
 #endif
 
   if (warp == 0) {
@@ -237,7 +237,9 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     auto issue_fc0 = [&](int j) {
       const int b = j & 1;
       const uint32_t id0 = idesc_f16kind<ET>(NRX_TILE_M, p.thp);
+      NRX_T(tw);
       mbar_wait(B_ta_ready + 8u * (b), (j >> 1) & 1);
+      NRX_TADD(t_c, tw);
       tc_fence_after();
       uint64_t ad = smem_desc(smem_u32(smem + L.ta + b * ta_bytes), NRX_TILE_M * 16, 128);
       uint64_t bd = smem_desc(smem_u32(smem + L.tw0), p.thp * 16, 128);
@@ -251,7 +253,9 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     auto issue_fc1 = [&](int j) {
       const int b = j & 1;
       const uint32_t id1 = idesc_f16kind<ET>(NRX_TILE_M, p.top);
+      NRX_T(tw);
       mbar_wait(B_h_ready + 8u * (b), (j >> 1) & 1);
+      NRX_TADD(t_d, tw);
       tc_fence_after();
       uint64_t ad = smem_desc(smem_u32(smem + L.th), NRX_TILE_M * 16, 128);
       uint64_t bd = smem_desc(smem_u32(smem + L.tw1), p.top * 16, 128);
@@ -364,7 +368,9 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     // ---- tail stage 2: hidden layer relu(state x W0 + b0) -> smem (fc1's A operand)
     auto tail_hidden = [&](int j) {
       const int b = j & 1;
+      NRX_T(tw);
       mbar_wait(B_hid_full + 8u * (b), (j >> 1) & 1);
+      NRX_TADD(t_d, tw);
       tc_fence_after();
       const int hch = p.thp / 8, hbeg = part * hch / PARTS, hend = (part + 1) * hch / PARTS;
       // TH is free: fc1 of the previous tile completed (tail_out ran first)
@@ -373,10 +379,10 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         tmem_ld8(tmem_base + lane_off + col_h + b * p.thp + 8 * c8, hv);
         ld_shared_f8(stb0_s + 32u * c8, bb);
         tmem_wait_ld();
-        float o[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = fmaxf(hv[e] + bb[e], 0.f);
-        st_shared_u4(th_s + (uint32_t)(c8 * NRX_TILE_M + r) * 16u, pack_chunk(o, static_cast<const ET*>(nullptr)));
+        for (int e = 0; e < 8; ++e) hv[e] += bb[e];
+        st_shared_u4(th_s + (uint32_t)(c8 * NRX_TILE_M + r) * 16u,
+                     relu_chunk(pack_chunk(hv, static_cast<const ET*>(nullptr)), static_cast<const ET*>(nullptr)));
       }
       fence_proxy_async();
       tc_fence_before();
@@ -385,13 +391,16 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     // ---- tail stage 3: outputs of tile j (+b1): messages, or LLRs + chest
     auto tail_out = [&](int j, int jslab, int jtile) {
       const int b = j & 1;
+      NRX_T(tw);
       mbar_wait(B_tout_full + 8u * (b), (j >> 1) & 1);
+      NRX_TADD(t_c, tw);
       tc_fence_after();
       const int row = jtile * NRX_TILE_M + r;
       int s, t;
       row_to_st(row, g, s, t);
       const bool valid = row < g.rows_data && t < g.T;
       const uint32_t tcol = tmem_base + lane_off + col_o + b * p.top;
+      const uint32_t vmask = valid ? 0xffffffffu : 0u;
       if (TAIL == TAIL_MSG) {  // messages of this slab, zero on pad rows/channels
         const int och = g.Ca / 8, obeg = part * och / PARTS, oend = (part + 1) * och / PARTS;
         ET* const mrow = chunk_ptr(static_cast<ET*>(p.msg), jslab, och, 0, row, g);
@@ -400,15 +409,10 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
           tmem_ld8(tcol + 8 * cc, mv);
           ld_shared_f8(stb1_s + 32u * cc, bb);
           tmem_wait_ld();
-          float o[8];
-          if (8 * cc + 8 <= g.d) {  // warp-uniform: every channel of the chunk is a message channel
 #pragma unroll
-            for (int e = 0; e < 8; ++e) o[e] = valid ? mv[e] + bb[e] : 0.f;
-          } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) o[e] = (valid && 8 * cc + e < g.d) ? mv[e] + bb[e] : 0.f;
-          }
-          *reinterpret_cast<uint4*>(mrow + (size_t)cc * g.rows_slab * 8) = pack_chunk(o, static_cast<const ET*>(nullptr));
+          for (int e = 0; e < 8; ++e) mv[e] = 8 * cc + 8 <= g.d || 8 * cc + e < g.d ? mv[e] + bb[e] : 0.f;
+          *reinterpret_cast<uint4*>(mrow + (size_t)cc * g.rows_slab * 8) =
+              mask_chunk(pack_chunk(mv, static_cast<const ET*>(nullptr)), vmask);
         }
       } else if (part == 0) {  // LLRs (masked width) + planar-decoded chest
         float o[32];
@@ -510,6 +514,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       const float pdt = need_pos ? g.dt[t] : 0.f;
       const float pdf = need_pos ? pos_df(s, slab % g.U, g) : 0.f;
       ET* const drow = chunk_ptr(dst, slab, nd, 0, row, g);
+      const uint32_t vmask = valid ? 0xffffffffu : 0u;
       const size_t dcs = (size_t)g.rows_slab * 8;  // chunk stride of a half-precision buffer
 #pragma unroll
       for (int c8 = 0; c8 < NC / 8; ++c8) {  // one 8-channel chunk at a time (few live registers)
@@ -520,6 +525,16 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         ld_shared_f8(sbias_s + 32u * cc, bb);
         float* x = v + 8 * c8;
         const bool full = 8 * cc + 8 <= g.d;  // warp-uniform
+        if (!MASTER && full) {  // fast path: pack, then ReLU / pad-row mask on the packed words
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] = MODE == EPI_RESIDUAL ? o8[e] + (x[e] + bb[e]) : x[e] + bb[e];
+          uint4 qx = pack_chunk(x, static_cast<const ET*>(nullptr));
+          if (MODE == EPI_RELU) qx = relu_chunk(qx, static_cast<const ET*>(nullptr));
+          qx = mask_chunk(qx, vmask);
+          *reinterpret_cast<uint4*>(drow + cc * dcs) = qx;
+          if (TAIL) st_shared_u4(ta_s + (it & 1) * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u, qx);
+          continue;
+        }
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           float y = x[e] + bb[e];  // conv + bias first, as the reference adds them
@@ -581,8 +596,8 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   }
 #ifdef NRX_TIMING
   if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 64))
-    printf("conv NP=%d mode=%d tail=%d c0=%d c1=%d tid=%d all=%lld a=%lld b=%lld c=%lld\n", NP, MODE, TAIL, p.c0,
-           p.c1, threadIdx.x, clock64() - t_all, t_a, t_b, t_c);
+    printf("conv NP=%d mode=%d tail=%d c0=%d c1=%d tid=%d all=%lld a=%lld b=%lld c=%lld d=%lld\n", NP, MODE, TAIL,
+           p.c0, p.c1, threadIdx.x, clock64() - t_all, t_a, t_b, t_c, t_d);
 #endif
   tc_fence_before();
   __syncthreads();

@@ -99,6 +99,29 @@ __device__ __forceinline__ uint4 pack_chunk(const float* v, const __half*) {
   return make_uint4(*reinterpret_cast<uint32_t*>(&h[0]), *reinterpret_cast<uint32_t*>(&h[1]),
                     *reinterpret_cast<uint32_t*>(&h[2]), *reinterpret_cast<uint32_t*>(&h[3]));
 }
+// max(x, 0) on a packed chunk (exact: rounding commutes with the clamp)
+__device__ __forceinline__ uint4 relu_chunk(uint4 q, const __half*) {
+  uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __half2 h = __hmax2(*reinterpret_cast<__half2*>(&w[i]), __float2half2_rn(0.f));
+    w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+__device__ __forceinline__ uint4 relu_chunk(uint4 q, const __nv_bfloat16*) {
+  uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 h = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&w[i]), __float2bfloat162_rn(0.f));
+    w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+// zero a packed chunk on invalid (pad) rows: mask = 0 or ~0
+__device__ __forceinline__ uint4 mask_chunk(uint4 q, uint32_t m) {
+  return make_uint4(q.x & m, q.y & m, q.z & m, q.w & m);
+}
 __device__ __forceinline__ void st_shared_u4(uint32_t addr, uint4 q) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(q.x), "r"(q.y), "r"(q.z), "r"(q.w)
                : "memory");
