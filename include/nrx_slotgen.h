@@ -27,9 +27,10 @@
  * stream keyed by (seed, global slot index), so a slot's content never
  * depends on the batch it was generated in or on the rank that made it.
  *
- * Arithmetic: float64 (like the reference) whenever variates are supplied
- * or a complex128 output is requested; device-drawn slots with complex64
- * outputs are synthesised in float32 from the same variates.
+ * Arithmetic: float64 (like the reference) whenever channel or noise
+ * variates are supplied or a complex128 output is requested; otherwise
+ * (device variates, possibly caller labels / pilots, complex64 outputs) the
+ * slot is synthesised in float32 from the same variates.
  *
  * Like nrx_forward: no allocation, no host synchronisation; work is
  * enqueued on `stream` (void* = cudaStream_t) and an nrx_status returned.

@@ -27,7 +27,11 @@ EXPORTED = ("nrx_abi_version", "nrx_status_string", "nrx_validate", "nrx_weight_
             "nrx_profile_disable", "nrx_kernel_name",
             # include/nrx_slotgen.h
             "nrx_synth_validate", "nrx_synth_workspace_bytes", "nrx_synth_slots",
-            "nrx_count_bit_errors", "nrx_philox4x32_10")
+            "nrx_count_bit_errors", "nrx_philox4x32_10",
+            # include/nrx_ldpc.h
+            "nrx_ldpc_create", "nrx_ldpc_destroy", "nrx_ldpc_dims", "nrx_ldpc_workspace_bytes",
+            "nrx_ldpc_decode", "nrx_ldpc_encode", "nrx_random_bits", "nrx_bits_to_labels",
+            "nrx_extract_llrs", "nrx_count_mismatches")
 KERNEL_IDS = {"ls_feat": 0, "conv_state_init0": 1, "conv_state_init1": 2, "msg_agg": 3,
               "conv_update0": 4, "conv_update1": 5, "readout": 6}
 
@@ -67,6 +71,14 @@ class ChannelDesc(ctypes.Structure):
 class SlotVariates(ctypes.Structure):
     _fields_ = [("angles", ctypes.c_void_p), ("phases", ctypes.c_void_p), ("labels", ctypes.c_void_p),
                 ("noise", ctypes.c_void_p), ("pilots", ctypes.c_void_p)]
+
+
+class LdpcDesc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("m", ctypes.c_int32), ("k", ctypes.c_int32), ("dmax", ctypes.c_int32),
+                ("cdeg", ctypes.c_int32), ("row_cols", ctypes.c_void_p), ("col_rows", ctypes.c_void_p),
+                ("col_slots", ctypes.c_void_p), ("info_positions", ctypes.c_void_p),
+                ("n_punctured", ctypes.c_int32), ("punctured", ctypes.c_void_p),
+                ("n_shortened", ctypes.c_int32), ("shortened", ctypes.c_void_p), ("chain_cols", ctypes.c_void_p)]
 
 
 class NrxLibraryError(RuntimeError):
@@ -115,6 +127,18 @@ def load() -> ctypes.CDLL:
     lib.nrx_count_bit_errors.argtypes = [P(SlotDesc), I, V, I, V, V, V, V]
     lib.nrx_philox4x32_10.argtypes = [P(ctypes.c_uint32), P(ctypes.c_uint32), P(ctypes.c_uint32)]
     lib.nrx_philox4x32_10.restype = None
+    lib.nrx_ldpc_create.argtypes = [P(LdpcDesc), P(ctypes.c_void_p)]
+    lib.nrx_ldpc_destroy.argtypes = [V]
+    lib.nrx_ldpc_destroy.restype = None
+    lib.nrx_ldpc_dims.argtypes = [V, P(ctypes.c_int32)]
+    lib.nrx_ldpc_workspace_bytes.argtypes = [V, I]
+    lib.nrx_ldpc_workspace_bytes.restype = Z
+    lib.nrx_ldpc_decode.argtypes = [V, I, V, I, V, V, V, Z, V]
+    lib.nrx_ldpc_encode.argtypes = [V, I, V, V, V, Z, V]
+    lib.nrx_random_bits.argtypes = [ctypes.c_uint64, ctypes.c_uint64, I, I, V, V]
+    lib.nrx_bits_to_labels.argtypes = [P(SlotDesc), I, I, I, V, V, V]
+    lib.nrx_extract_llrs.argtypes = [P(SlotDesc), I, I, I, V, I, ctypes.c_float, V, V]
+    lib.nrx_count_mismatches.argtypes = [I, I, V, V, V, V]
     if lib.nrx_abi_version() != 1:
         raise NrxLibraryError("libnrx_b200.so ABI version mismatch")
     _LIB = lib

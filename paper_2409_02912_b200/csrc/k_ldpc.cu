@@ -1,0 +1,582 @@
+// k_ldpc.cu — GPU LDPC decoding (flooding min-sum, early exit on parity) and
+// staircase (IRA) encoding.  C ABI in include/nrx_ldpc.h.
+//
+// Reference (/root/reference/pkg/src/nrxsim/ldpc.py): LdpcCode.decode
+// ldpc.py:99-178, check_parity :91-97, encode :88-90, rate matching
+// :303-330.  The decoder keeps the reference's float32 operation order, so
+// the decoded bits and success flags are bit-identical
+// (tests/test_gpu_ldpc.py against tests/golden/ldpc_*.npz):
+//   total_j = chan_j + ((c2v_0 + c2v_1) + c2v_2)      variable update
+//   v2c     = total_col - c2v                          check update
+//   c2v     = (row_sign * sgn) * (s == argmin ? min2 : min1)
+//
+// Per iteration three launches over all codewords of the batch (grid.y =
+// codeword): k_ldpc_var (thread per variable: totals + hard bits),
+// k_ldpc_check (thread per check: syndrome, then min-sum messages from
+// two passes over the row so no per-row arrays live in registers) and
+// k_ldpc_flag (a codeword whose checks are all satisfied freezes: later
+// launches return at once for it, exactly the reference's per-codeword
+// early exit).  A final variable pass gives the hard bits of codewords that
+// never converged (the reference's for-else branch).
+//
+// Encoder (codes with a staircase parity part): information bits placed,
+// per-check information syndromes s_i, then the parity chain
+// p_i = s_i ^ p_{i-1} as one block-wide XOR prefix scan per codeword, and
+// the transmitted positions gathered.
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "../../include/nrx_ldpc.h"
+
+struct nrx_ldpc_code {
+  int n, m, k, dmax, cdeg, k_eff, ntx, has_chain;
+  int32_t* row_cols;   // (m, dmax)
+  int32_t* col_rows;   // (n, cdeg)
+  int32_t* col_slots;  // (n, cdeg)
+  int32_t* chan_src;   // (n): transmitted index, -1 punctured, -2 shortened
+  int32_t* keep_pos;   // (k_eff): mother positions of the kept info bits
+  int32_t* tx_pos;     // (ntx)
+  int32_t* info_slot;  // (n): payload index of an info position, -1 shortened, -2 parity
+  int32_t* chain_cols; // (m) or null
+};
+
+namespace nrx_ldpc {
+
+constexpr float kShortenedLlr = 60.0f;   // ldpc.py:25
+constexpr int kThreads = 256;
+constexpr int kScanThreads = 1024;
+
+struct Flags {
+  int done;
+  int unsat;
+};
+
+struct DecWs {
+  float* chan;
+  float* total;
+  float* c2v;
+  uint8_t* hard;
+  Flags* flags;
+};
+
+size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+DecWs dec_layout(const nrx_ldpc_code& c, int n_cw, uint8_t* base, size_t* total_bytes) {
+  DecWs w{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align256(off + bytes);
+    return o;
+  };
+  const size_t o_chan = take(sizeof(float) * c.n * (size_t)n_cw);
+  const size_t o_total = take(sizeof(float) * c.n * (size_t)n_cw);
+  const size_t o_c2v = take(sizeof(float) * (size_t)c.m * c.dmax * n_cw);
+  const size_t o_hard = take((size_t)c.n * n_cw);
+  const size_t o_flags = take(sizeof(Flags) * (size_t)n_cw);
+  if (total_bytes) *total_bytes = off;
+  if (base) {
+    w.chan = reinterpret_cast<float*>(base + o_chan);
+    w.total = reinterpret_cast<float*>(base + o_total);
+    w.c2v = reinterpret_cast<float*>(base + o_c2v);
+    w.hard = base + o_hard;
+    w.flags = reinterpret_cast<Flags*>(base + o_flags);
+  }
+  return w;
+}
+
+struct EncWs {
+  uint8_t* cw;
+  uint8_t* syn;
+};
+
+EncWs enc_layout(const nrx_ldpc_code& c, int n_cw, uint8_t* base, size_t* total_bytes) {
+  EncWs w{};
+  const size_t o_cw = 0;
+  const size_t o_syn = align256((size_t)c.n * n_cw);
+  const size_t end = align256(o_syn + (size_t)c.m * n_cw);
+  if (total_bytes) *total_bytes = end;
+  if (base) {
+    w.cw = base + o_cw;
+    w.syn = base + o_syn;
+  }
+  return w;
+}
+
+// ---------------------------------------------------------------------------
+// decoder kernels
+// ---------------------------------------------------------------------------
+
+__global__ void k_ldpc_init(nrx_ldpc_code c, const float* llr, DecWs w) {
+  const int cw = blockIdx.y;
+  const size_t ne = (size_t)c.m * c.dmax;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ne || i < (size_t)c.n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    if (i < (size_t)c.n) {
+      const int src = c.chan_src[i];
+      // ln(p0/p1) convention: the channel value is the negated logit LLR
+      w.chan[(size_t)cw * c.n + i] =
+          src >= 0 ? -llr[(size_t)cw * c.ntx + src] : (src == -2 ? kShortenedLlr : 0.f);
+    }
+    if (i < ne) w.c2v[(size_t)cw * ne + i] = 0.f;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) w.flags[cw] = Flags{0, 0};
+}
+
+// Variable update: total = chan + ((c2v_0 + c2v_1) + c2v_2); hard bits.
+__global__ void __launch_bounds__(kThreads) k_ldpc_var(nrx_ldpc_code c, DecWs w, int only_open) {
+  const int cw = blockIdx.y;
+  if (w.flags[cw].done) return;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= c.n) return;
+  const float* c2v = w.c2v + (size_t)cw * c.m * c.dmax;
+  float s = 0.f;
+  for (int t = 0; t < c.cdeg; ++t) {
+    const int r = c.col_rows[(size_t)j * c.cdeg + t];
+    if (r < 0) break;
+    const float v = c2v[(size_t)r * c.dmax + c.col_slots[(size_t)j * c.cdeg + t]];
+    s = t == 0 ? v : __fadd_rn(s, v);
+  }
+  const float tot = __fadd_rn(w.chan[(size_t)cw * c.n + j], s);
+  if (!only_open) w.total[(size_t)cw * c.n + j] = tot;
+  w.hard[(size_t)cw * c.n + j] = tot < 0.f ? 1 : 0;
+}
+
+// Check update (two passes over the row) + syndrome of this iteration's hard bits.
+__global__ void __launch_bounds__(kThreads) k_ldpc_check(nrx_ldpc_code c, DecWs w) {
+  const int cw = blockIdx.y;
+  if (w.flags[cw].done) return;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  int syn = 0;
+  if (r < c.m) {
+    const int32_t* cols = c.row_cols + (size_t)r * c.dmax;
+    float* msg = w.c2v + ((size_t)cw * c.m + r) * c.dmax;
+    const float* tot = w.total + (size_t)cw * c.n;
+    float min1 = INFINITY, min2 = INFINITY;
+    int amin = 0, neg = 0;
+    bool first = true;
+    for (int s = 0; s < c.dmax; ++s) {
+      const int col = cols[s];
+      float mag = INFINITY;
+      if (col >= 0) {
+        const float v = tot[col];
+        syn ^= v < 0.f ? 1 : 0;
+        const float x = __fsub_rn(v, msg[s]);
+        mag = fabsf(x);
+        neg ^= x < 0.f ? 1 : 0;
+      }
+      // np.argmin: first index of the smallest magnitude (invalid slots are +inf)
+      if (first || mag < min1) {
+        if (!first) min2 = min1;
+        min1 = mag;
+        amin = s;
+        first = false;
+      } else if (mag < min2) {
+        min2 = mag;
+      }
+    }
+    const float rs = neg ? -1.f : 1.f;
+    for (int s = 0; s < c.dmax; ++s) {
+      const int col = cols[s];
+      if (col < 0) {
+        msg[s] = 0.f;
+        continue;
+      }
+      const float x = __fsub_rn(tot[col], msg[s]);
+      const float sg = x < 0.f ? -1.f : 1.f;
+      msg[s] = __fmul_rn(rs * sg, s == amin ? min2 : min1);
+    }
+  }
+  if (__syncthreads_or(syn) && threadIdx.x == 0) atomicOr(&w.flags[cw].unsat, 1);
+}
+
+// A codeword whose checks were all satisfied by this iteration's hard bits is done.
+__global__ void k_ldpc_flag(DecWs w, int n_cw) {
+  const int cw = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cw >= n_cw) return;
+  Flags f = w.flags[cw];
+  if (!f.done && !f.unsat) f.done = 1;
+  f.unsat = 0;
+  w.flags[cw] = f;
+}
+
+__global__ void k_ldpc_extract(nrx_ldpc_code c, DecWs w, uint8_t* info, uint8_t* success, int n_cw) {
+  const int cw = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c.k_eff; i += gridDim.x * blockDim.x)
+    info[(size_t)cw * c.k_eff + i] = w.hard[(size_t)cw * c.n + c.keep_pos[i]];
+  if (blockIdx.x == 0 && threadIdx.x == 0) success[cw] = static_cast<uint8_t>(w.flags[cw].done);
+}
+
+// ---------------------------------------------------------------------------
+// staircase encoder kernels
+// ---------------------------------------------------------------------------
+
+__global__ void k_enc_place(nrx_ldpc_code c, const uint8_t* info, EncWs w) {
+  const int cw = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= c.n) return;
+  const int slot = c.info_slot[j];
+  w.cw[(size_t)cw * c.n + j] = slot >= 0 ? (info[(size_t)cw * c.k_eff + slot] & 1) : 0;
+}
+
+__global__ void k_enc_syn(nrx_ldpc_code c, EncWs w) {
+  const int cw = blockIdx.y;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= c.m) return;
+  const uint8_t* bits = w.cw + (size_t)cw * c.n;
+  int s = 0;
+  for (int k = 0; k < c.dmax; ++k) {
+    const int col = c.row_cols[(size_t)r * c.dmax + k];
+    if (col >= 0 && c.info_slot[col] != -2) s ^= bits[col];
+  }
+  w.syn[(size_t)cw * c.m + r] = static_cast<uint8_t>(s);
+}
+
+// p_i = s_0 ^ ... ^ s_i written to the chain's parity column, one block per codeword.
+__global__ void __launch_bounds__(kScanThreads) k_enc_chain(nrx_ldpc_code c, EncWs w) {
+  __shared__ int warp_x[kScanThreads / 32];
+  const int cw = blockIdx.x;
+  const uint8_t* syn = w.syn + (size_t)cw * c.m;
+  uint8_t* bits = w.cw + (size_t)cw * c.n;
+  const int per = (c.m + kScanThreads - 1) / kScanThreads;
+  const int beg = threadIdx.x * per, end = min(c.m, beg + per);
+  int x = 0;
+  for (int i = beg; i < end; ++i) x ^= syn[i];
+  // exclusive XOR scan of the per-thread segment parities
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl ^= y;
+  }
+  if (lane == 31) warp_x[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int v = lane < kScanThreads / 32 ? warp_x[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v ^= y;
+    }
+    if (lane < kScanThreads / 32) warp_x[lane] = v;   // inclusive over warps
+  }
+  __syncthreads();
+  int acc = (incl ^ x) ^ (wid > 0 ? warp_x[wid - 1] : 0);   // exclusive prefix of this segment
+  for (int i = beg; i < end; ++i) {
+    acc ^= syn[i];
+    bits[c.chain_cols[i]] = static_cast<uint8_t>(acc);
+  }
+}
+
+__global__ void k_enc_tx(nrx_ldpc_code c, EncWs w, uint8_t* tx) {
+  const int cw = blockIdx.y;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= c.ntx) return;
+  tx[(size_t)cw * c.ntx + e] = w.cw[(size_t)cw * c.n + c.tx_pos[e]];
+}
+
+// ---------------------------------------------------------------------------
+// coded Monte-Carlo glue
+// ---------------------------------------------------------------------------
+
+__device__ inline uint4 philox10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// one Philox block -> 128 bits of one row
+__global__ void k_random_bits(uint32_t k0, uint32_t k1, unsigned long long first, int cols, uint8_t* out) {
+  const int row = blockIdx.y;
+  const int blk = blockIdx.x * blockDim.x + threadIdx.x;   // 128-bit block of the row
+  if (blk * 128 >= cols) return;
+  const unsigned long long g = first + (unsigned long long)row;
+  const uint4 r = philox10(make_uint4((uint32_t)blk, (uint32_t)g, (uint32_t)(g >> 32), 0x5A17u), k0, k1);
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+  uint8_t* o = out + (size_t)row * cols + (size_t)blk * 128;
+  const int nb = min(128, cols - blk * 128);
+  for (int i = 0; i < nb; ++i) o[i] = (w[i >> 5] >> (i & 31)) & 1u;
+}
+
+struct SlotGeo {
+  int S, T, U, nsym;      // nsym: data symbols per subcarrier
+  int data_t[32];         // the data symbols, ascending
+};
+
+__global__ void k_bits_to_labels(SlotGeo g, int ue, int m, const uint8_t* bits, uint8_t* labels) {
+  const int n = blockIdx.y;
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;     // data RE, subcarrier-major
+  const int nd = g.S * g.nsym;
+  if (d >= nd) return;
+  const int s = d / g.nsym, t = g.data_t[d - s * g.nsym];
+  const uint8_t* b = bits + ((size_t)n * nd + d) * m;
+  int lab = 0;
+  for (int j = 0; j < m; ++j) lab = (lab << 1) | (b[j] & 1);
+  labels[(((size_t)n * g.U + ue) * g.S + s) * g.T + t] = static_cast<uint8_t>(lab);
+}
+
+__global__ void k_extract_llrs(SlotGeo g, int ue, int m, const float* llr, int W, float clip, float* out) {
+  const int n = blockIdx.y;
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nd = g.S * g.nsym;
+  if (d >= nd) return;
+  const int s = d / g.nsym, t = g.data_t[d - s * g.nsym];
+  const float* src = llr + ((((size_t)n * g.U + ue) * g.S + s) * g.T + t) * W;
+  float* dst = out + ((size_t)n * nd + d) * m;
+  for (int j = 0; j < m; ++j) dst[j] = fminf(fmaxf(src[j], -clip), clip);
+}
+
+__global__ void k_mismatches(int cols, const uint8_t* a, const uint8_t* b, unsigned long long* errors) {
+  const int row = blockIdx.y;
+  int e = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cols; i += gridDim.x * blockDim.x)
+    e += (a[(size_t)row * cols + i] & 1) != (b[(size_t)row * cols + i] & 1);
+  const int tot = __reduce_add_sync(0xffffffffu, e);
+  if ((threadIdx.x & 31) == 0 && tot) atomicAdd(errors + row, (unsigned long long)tot);
+}
+
+int slot_geo(const nrx_slot_desc* s, SlotGeo* g) {
+  if (!s || s->num_subcarriers < 1 || s->num_symbols < 1 || s->num_symbols > 32 || s->num_ues < 1 ||
+      s->num_pilot_symbols < 1 || s->num_pilot_symbols > NRX_MAX_PILOT_SYMBOLS)
+    return NRX_ERR_INVALID;
+  g->S = s->num_subcarriers;
+  g->T = s->num_symbols;
+  g->U = s->num_ues;
+  bool pilot[32] = {};
+  for (int k = 0; k < s->num_pilot_symbols; ++k) {
+    if (s->pilot_symbols[k] < 0 || s->pilot_symbols[k] >= g->T) return NRX_ERR_INVALID;
+    pilot[s->pilot_symbols[k]] = true;
+  }
+  g->nsym = 0;
+  for (int t = 0; t < g->T; ++t)
+    if (!pilot[t]) g->data_t[g->nsym++] = t;
+  return g->nsym > 0 ? NRX_OK : NRX_ERR_INVALID;
+}
+
+int launch_status() {
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e == cudaErrorNoKernelImageForDevice || e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+    return NRX_ERR_NO_DEVICE;
+  return e == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
+}
+
+template <typename T>
+int upload(T** dst, const std::vector<T>& v) {
+  *dst = nullptr;
+  if (v.empty()) return NRX_OK;
+  if (cudaMalloc(reinterpret_cast<void**>(dst), v.size() * sizeof(T)) != cudaSuccess) return NRX_ERR_CUDA;
+  return cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess ? NRX_OK
+                                                                                              : NRX_ERR_CUDA;
+}
+
+}  // namespace nrx_ldpc
+
+using namespace nrx_ldpc;
+
+extern "C" int nrx_ldpc_create(const nrx_ldpc_desc* d, nrx_ldpc_code** out) {
+  if (!d || !out) return NRX_ERR_INVALID;
+  *out = nullptr;
+  if (d->n < 2 || d->m < 1 || d->k < 1 || d->k >= d->n || d->dmax < 1 || d->cdeg < 1) return NRX_ERR_INVALID;
+  if (d->cdeg > NRX_LDPC_MAX_COL_DEG || d->dmax > NRX_LDPC_MAX_ROW_DEG) return NRX_ERR_UNSUPPORTED;
+  if (!d->row_cols || !d->col_rows || !d->col_slots || !d->info_positions) return NRX_ERR_INVALID;
+  if (d->n_punctured < 0 || d->n_shortened < 0 || (d->n_punctured && !d->punctured) ||
+      (d->n_shortened && !d->shortened))
+    return NRX_ERR_INVALID;
+  const int n = d->n, m = d->m, k = d->k;
+  for (size_t i = 0; i < (size_t)m * d->dmax; ++i)
+    if (d->row_cols[i] < -1 || d->row_cols[i] >= n) return NRX_ERR_INVALID;
+  for (size_t i = 0; i < (size_t)n * d->cdeg; ++i) {
+    if (d->col_rows[i] < -1 || d->col_rows[i] >= m) return NRX_ERR_INVALID;
+    if (d->col_rows[i] >= 0 && (d->col_slots[i] < 0 || d->col_slots[i] >= d->dmax)) return NRX_ERR_INVALID;
+  }
+  std::vector<int32_t> info_slot(n, -2), chan_src(n, 0);
+  std::vector<char> skip(n, 0), is_short(n, 0);
+  for (int i = 0; i < d->n_punctured; ++i) {
+    const int p = d->punctured[i];
+    if (p < 0 || p >= n) return NRX_ERR_INVALID;
+    skip[p] = 1;
+  }
+  for (int i = 0; i < d->n_shortened; ++i) {
+    const int p = d->shortened[i];
+    if (p < 0 || p >= n) return NRX_ERR_INVALID;
+    skip[p] = 1;
+    is_short[p] = 1;
+  }
+  std::vector<int32_t> keep_pos;
+  for (int i = 0; i < k; ++i) {
+    const int p = d->info_positions[i];
+    if (p < 0 || p >= n || (i && p <= d->info_positions[i - 1])) return NRX_ERR_INVALID;
+    if (is_short[p]) {
+      info_slot[p] = -1;
+    } else {
+      info_slot[p] = static_cast<int32_t>(keep_pos.size());
+      keep_pos.push_back(p);
+    }
+  }
+  std::vector<int32_t> tx_pos;
+  for (int j = 0; j < n; ++j) {
+    if (!skip[j]) {
+      chan_src[j] = static_cast<int32_t>(tx_pos.size());
+      tx_pos.push_back(j);
+    } else {
+      chan_src[j] = is_short[j] ? -2 : -1;   // shortened: known zero; punctured: erased
+    }
+  }
+  if (keep_pos.empty() || tx_pos.empty()) return NRX_ERR_INVALID;
+  if (d->chain_cols) {
+    for (int i = 0; i < m; ++i)
+      if (d->chain_cols[i] < 0 || d->chain_cols[i] >= n || info_slot[d->chain_cols[i]] != -2) return NRX_ERR_INVALID;
+  }
+  nrx_ldpc_code* c = new nrx_ldpc_code{};
+  c->n = n;
+  c->m = m;
+  c->k = k;
+  c->dmax = d->dmax;
+  c->cdeg = d->cdeg;
+  c->k_eff = static_cast<int>(keep_pos.size());
+  c->ntx = static_cast<int>(tx_pos.size());
+  c->has_chain = d->chain_cols != nullptr;
+  int rc = NRX_OK;
+  rc = rc ? rc : upload(&c->row_cols, std::vector<int32_t>(d->row_cols, d->row_cols + (size_t)m * d->dmax));
+  rc = rc ? rc : upload(&c->col_rows, std::vector<int32_t>(d->col_rows, d->col_rows + (size_t)n * d->cdeg));
+  rc = rc ? rc : upload(&c->col_slots, std::vector<int32_t>(d->col_slots, d->col_slots + (size_t)n * d->cdeg));
+  rc = rc ? rc : upload(&c->chan_src, chan_src);
+  rc = rc ? rc : upload(&c->keep_pos, keep_pos);
+  rc = rc ? rc : upload(&c->tx_pos, tx_pos);
+  rc = rc ? rc : upload(&c->info_slot, info_slot);
+  if (!rc && d->chain_cols) rc = upload(&c->chain_cols, std::vector<int32_t>(d->chain_cols, d->chain_cols + m));
+  if (rc) {
+    nrx_ldpc_destroy(c);
+    return rc == NRX_ERR_CUDA && cudaGetLastError() == cudaErrorNoDevice ? NRX_ERR_NO_DEVICE : rc;
+  }
+  *out = c;
+  return NRX_OK;
+}
+
+extern "C" void nrx_ldpc_destroy(nrx_ldpc_code* c) {
+  if (!c) return;
+  int32_t* ptrs[] = {c->row_cols, c->col_rows, c->col_slots, c->chan_src, c->keep_pos, c->tx_pos,
+                     c->info_slot, c->chain_cols};
+  for (int32_t* p : ptrs)
+    if (p) cudaFree(p);
+  delete c;
+}
+
+extern "C" int nrx_ldpc_dims(const nrx_ldpc_code* c, int32_t* out4) {
+  if (!c || !out4) return NRX_ERR_INVALID;
+  out4[0] = c->n;
+  out4[1] = c->k_eff;
+  out4[2] = c->ntx;
+  out4[3] = c->m;
+  return NRX_OK;
+}
+
+extern "C" size_t nrx_ldpc_workspace_bytes(const nrx_ldpc_code* c, int n_cw) {
+  if (!c || n_cw < 1) return 0;
+  size_t a = 0, b = 0;
+  dec_layout(*c, n_cw, nullptr, &a);
+  enc_layout(*c, n_cw, nullptr, &b);
+  return a > b ? a : b;
+}
+
+extern "C" int nrx_ldpc_decode(const nrx_ldpc_code* c, int n_cw, const float* llr, int iterations,
+                               uint8_t* info_out, uint8_t* success, void* ws, size_t ws_bytes, void* stream) {
+  if (!c || n_cw < 0 || iterations < 0 || !llr || !info_out || !success) return NRX_ERR_INVALID;
+  if (n_cw == 0) return NRX_OK;
+  if (n_cw > 65535) return NRX_ERR_UNSUPPORTED;
+  size_t need = 0;
+  dec_layout(*c, n_cw, nullptr, &need);
+  if (!ws || ws_bytes < need) return NRX_ERR_WORKSPACE;
+  const DecWs w = dec_layout(*c, n_cw, static_cast<uint8_t*>(ws), nullptr);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int vb = (c->n + kThreads - 1) / kThreads, cb = (c->m + kThreads - 1) / kThreads;
+  k_ldpc_init<<<dim3(256, n_cw), kThreads, 0, st>>>(*c, llr, w);
+  for (int it = 0; it < iterations; ++it) {
+    k_ldpc_var<<<dim3(vb, n_cw), kThreads, 0, st>>>(*c, w, 0);
+    k_ldpc_check<<<dim3(cb, n_cw), kThreads, 0, st>>>(*c, w);
+    k_ldpc_flag<<<(n_cw + 255) / 256, 256, 0, st>>>(w, n_cw);
+  }
+  // codewords that never satisfied every check: hard bits of the final messages
+  k_ldpc_var<<<dim3(vb, n_cw), kThreads, 0, st>>>(*c, w, 1);
+  k_ldpc_extract<<<dim3(64, n_cw), kThreads, 0, st>>>(*c, w, info_out, success, n_cw);
+  return launch_status();
+}
+
+extern "C" int nrx_ldpc_encode(const nrx_ldpc_code* c, int n_cw, const uint8_t* info, uint8_t* tx, void* ws,
+                               size_t ws_bytes, void* stream) {
+  if (!c || n_cw < 0 || !info || !tx) return NRX_ERR_INVALID;
+  if (!c->has_chain) return NRX_ERR_UNSUPPORTED;
+  if (n_cw == 0) return NRX_OK;
+  if (n_cw > 65535) return NRX_ERR_UNSUPPORTED;
+  size_t need = 0;
+  enc_layout(*c, n_cw, nullptr, &need);
+  if (!ws || ws_bytes < need) return NRX_ERR_WORKSPACE;
+  const EncWs w = enc_layout(*c, n_cw, static_cast<uint8_t*>(ws), nullptr);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_enc_place<<<dim3((c->n + kThreads - 1) / kThreads, n_cw), kThreads, 0, st>>>(*c, info, w);
+  k_enc_syn<<<dim3((c->m + kThreads - 1) / kThreads, n_cw), kThreads, 0, st>>>(*c, w);
+  k_enc_chain<<<n_cw, kScanThreads, 0, st>>>(*c, w);
+  k_enc_tx<<<dim3((c->ntx + kThreads - 1) / kThreads, n_cw), kThreads, 0, st>>>(*c, w, tx);
+  return launch_status();
+}
+
+extern "C" int nrx_random_bits(uint64_t seed, uint64_t first_row, int rows, int cols, uint8_t* out, void* stream) {
+  if (rows < 0 || cols < 0 || (!out && rows && cols)) return NRX_ERR_INVALID;
+  if (!rows || !cols) return NRX_OK;
+  if (rows > 65535) return NRX_ERR_UNSUPPORTED;
+  const int blocks = (cols + 127) / 128;
+  k_random_bits<<<dim3((blocks + 127) / 128, rows), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      (uint32_t)seed, (uint32_t)(seed >> 32), first_row, cols, out);
+  return launch_status();
+}
+
+extern "C" int nrx_bits_to_labels(const nrx_slot_desc* slot, int n_slots, int ue, int mod_order, const uint8_t* bits,
+                                  uint8_t* labels, void* stream) {
+  SlotGeo g;
+  const int rc = slot_geo(slot, &g);
+  if (rc) return rc;
+  if (n_slots < 0 || ue < 0 || ue >= g.U || mod_order < 1 || mod_order > 8 || !bits || !labels) return NRX_ERR_INVALID;
+  if (!n_slots) return NRX_OK;
+  if (n_slots > 65535) return NRX_ERR_UNSUPPORTED;
+  const int nd = g.S * g.nsym;
+  k_bits_to_labels<<<dim3((nd + 255) / 256, n_slots), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      g, ue, mod_order, bits, labels);
+  return launch_status();
+}
+
+extern "C" int nrx_extract_llrs(const nrx_slot_desc* slot, int n_slots, int ue, int mod_order, const float* llr,
+                                int llr_width, float clip, float* out, void* stream) {
+  SlotGeo g;
+  const int rc = slot_geo(slot, &g);
+  if (rc) return rc;
+  if (n_slots < 0 || ue < 0 || ue >= g.U || mod_order < 1 || mod_order > llr_width || llr_width > 8 || !llr ||
+      !out || !(clip > 0.f))
+    return NRX_ERR_INVALID;
+  if (!n_slots) return NRX_OK;
+  if (n_slots > 65535) return NRX_ERR_UNSUPPORTED;
+  const int nd = g.S * g.nsym;
+  k_extract_llrs<<<dim3((nd + 255) / 256, n_slots), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      g, ue, mod_order, llr, llr_width, clip, out);
+  return launch_status();
+}
+
+extern "C" int nrx_count_mismatches(int rows, int cols, const uint8_t* a, const uint8_t* b, unsigned long long* errors,
+                                    void* stream) {
+  if (rows < 0 || cols < 0 || ((!a || !b || !errors) && rows && cols)) return NRX_ERR_INVALID;
+  if (!rows || !cols) return NRX_OK;
+  if (rows > 65535) return NRX_ERR_UNSUPPORTED;
+  const int blocks = min(64, (cols + 255) / 256);
+  k_mismatches<<<dim3(blocks, rows), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(cols, a, b, errors);
+  return launch_status();
+}

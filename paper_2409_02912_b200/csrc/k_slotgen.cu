@@ -654,7 +654,9 @@ extern "C" int nrx_synth_slots(const nrx_slot_desc* slot, const nrx_channel_desc
   q.h_eff = h_eff;
   q.h_c128 = h_eff_c128;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const bool exact = variates != nullptr || y_c128 || (h_eff && h_eff_c128);
+  // float64 when continuous variates come from the caller (reference stream) or a
+  // complex128 output is asked for; supplied labels / pilots alone keep float32
+  const bool exact = (variates && (variates->angles || variates->noise)) || y_c128 || (h_eff && h_eff_c128);
   const int rc = exact ? launch_synth<double>(q, n_slots, st) : launch_synth<float>(q, n_slots, st);
   if (rc != NRX_OK) return rc;
   const cudaError_t e = cudaPeekAtLastError();

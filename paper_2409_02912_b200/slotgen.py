@@ -268,6 +268,7 @@ class GpuSlotSource:
             lab = torch.empty((N, U, S, T), dtype=torch.uint8, device=dev)
             heff = torch.empty((N, U, S, T, B), dtype=h_dtype, device=dev) if with_h_eff else None
         keep = []
+        host_src = False
         var_s = None
         if variates is not None:
             var_s = _lib.SlotVariates()
@@ -276,6 +277,8 @@ class GpuSlotSource:
                 v = variates.get(name)
                 if v is None:
                     continue
+                if not (isinstance(v, torch.Tensor) and v.device == dev):
+                    host_src = True
                 t = v if isinstance(v, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v))
                 t = t.to(device=dev, dtype=dt).contiguous()
                 keep.append(t)
@@ -290,8 +293,8 @@ class GpuSlotSource:
             heff.data_ptr() if heff is not None else None, int(heff is not None and heff.dtype == torch.complex128),
             ws.data_ptr(), ws.numel(), st.cuda_stream)
         _lib.check(code, "nrx_synth_slots")
-        if keep:
-            st.synchronize()            # host-provided variates must outlive the kernels
+        if host_src:
+            st.synchronize()            # staged host variates must outlive the kernels
         return SlotBatch(y, pil, lab, heff, n0_t, mods, int(first_slot))
 
     def _dev(self, v, dtype, shape, broadcast_from=None):

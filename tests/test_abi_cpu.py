@@ -2,6 +2,7 @@
 header declares, names/validates/packs weights without a GPU."""
 
 import ctypes
+import glob
 import os
 import re
 
@@ -13,7 +14,7 @@ from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_tabl
 from paper_2409_02912_b200.engine import pack_weights, pilot_comb_values
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADERS = [os.path.join(ROOT, "include", h) for h in ("nrx_b200.h", "nrx_slotgen.h")]
+HEADERS = sorted(glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
 def declared_functions():
