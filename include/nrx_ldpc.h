@@ -54,8 +54,9 @@ typedef struct nrx_ldpc_desc {
   int32_t n_shortened;
   const int32_t* shortened;      /* info positions fixed to 0, not sent   */
   const int32_t* chain_cols;     /* (m) staircase parity column of chain
-                                    position i (check i holds chain i-1, i),
-                                    or NULL: decode only                  */
+                                    position i, or NULL: decode only      */
+  int32_t chain_step;            /* Z: check i holds chain positions i-Z
+                                    and i (Z interleaved accumulators)    */
 } nrx_ldpc_desc;
 
 typedef struct nrx_ldpc_code nrx_ldpc_code;   /* device-resident, opaque */

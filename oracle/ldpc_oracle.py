@@ -91,8 +91,8 @@ def decode(code, llrs, iterations=20):
 
 def staircase_codeword(code, info):
     """Mother codeword of an IRA code from (B, k_eff) info bits: shortened
-    info bits are zero, the parity chain p_i = s_i ^ p_{i-1} over the checks'
-    info syndromes s (check i holds chain positions i-1, i)."""
+    info bits are zero, the parity chains p_i = s_i ^ p_{i-Z} over the
+    checks' info syndromes s (check i holds chain positions i-Z, i)."""
     info = np.asarray(info, dtype=np.uint8)
     b = info.shape[0]
     u = np.zeros((b, code.k), dtype=np.uint8)
@@ -108,8 +108,9 @@ def staircase_codeword(code, info):
     for r in range(rc.shape[0]):
         cols = rc[r][(rc[r] >= 0) & is_info[rc[r]]]
         syn[:, r] = pad[:, cols].sum(axis=1) % 2
-    acc = np.zeros(b, dtype=np.uint8)
+    z = int(getattr(code, "chain_step", 1))
+    par = np.zeros((b, rc.shape[0]), dtype=np.uint8)
     for i, col in enumerate(np.asarray(code.chain_cols)):
-        acc ^= syn[:, i]
-        cw[:, col] = acc
+        par[:, i] = syn[:, i] ^ (par[:, i - z] if i >= z else 0)
+        cw[:, col] = par[:, i]
     return cw

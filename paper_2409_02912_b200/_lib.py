@@ -78,7 +78,8 @@ class LdpcDesc(ctypes.Structure):
                 ("cdeg", ctypes.c_int32), ("row_cols", ctypes.c_void_p), ("col_rows", ctypes.c_void_p),
                 ("col_slots", ctypes.c_void_p), ("info_positions", ctypes.c_void_p),
                 ("n_punctured", ctypes.c_int32), ("punctured", ctypes.c_void_p),
-                ("n_shortened", ctypes.c_int32), ("shortened", ctypes.c_void_p), ("chain_cols", ctypes.c_void_p)]
+                ("n_shortened", ctypes.c_int32), ("shortened", ctypes.c_void_p), ("chain_cols", ctypes.c_void_p),
+                ("chain_step", ctypes.c_int32)]
 
 
 class NrxLibraryError(RuntimeError):

@@ -10,30 +10,34 @@
 //   v2c     = total_col - c2v                          check update
 //   c2v     = (row_sign * sgn) * (s == argmin ? min2 : min1)
 //
-// Per iteration three launches over all codewords of the batch (grid.y =
-// codeword): k_ldpc_var (thread per variable: totals + hard bits),
-// k_ldpc_check (thread per check: syndrome, then min-sum messages from
-// two passes over the row so no per-row arrays live in registers) and
-// k_ldpc_flag (a codeword whose checks are all satisfied freezes: later
-// launches return at once for it, exactly the reference's per-codeword
-// early exit).  A final variable pass gives the hard bits of codewords that
-// never converged (the reference's for-else branch).
+// Codewords are decoded 32 at a time, interleaved: lane l of every warp
+// works on codeword l of its group, so the random gathers of the Tanner
+// graph move 128 contiguous bytes (one value per codeword) instead of a
+// 32-byte sector per 4-byte value.  Per iteration three launches (grid.y =
+// group): k_ldpc_var (warp per variable: totals + hard bits), k_ldpc_check
+// (warp per check: syndrome, then min-sum messages from two passes over the
+// row) and k_ldpc_flag (a codeword whose checks are all satisfied freezes:
+// its lane is skipped from then on, exactly the reference's per-codeword
+// early exit; a group with all lanes done returns at once).  A final
+// variable pass gives the hard bits of codewords that never converged (the
+// reference's for-else branch).
 //
 // Encoder (codes with a staircase parity part): information bits placed,
-// per-check information syndromes s_i, then the parity chain
-// p_i = s_i ^ p_{i-1} as one block-wide XOR prefix scan per codeword, and
-// the transmitted positions gathered.
+// per-check information syndromes s_i, then the Z interleaved accumulator
+// chains p_i = s_i ^ p_{i-Z} (one thread per chain), and the transmitted
+// positions gathered.
 
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/nrx_ldpc.h"
 
 struct nrx_ldpc_code {
-  int n, m, k, dmax, cdeg, k_eff, ntx, has_chain;
+  int n, m, k, dmax, cdeg, k_eff, ntx, has_chain, chain_step;
   int32_t* row_cols;   // (m, dmax)
   int32_t* col_rows;   // (n, cdeg)
   int32_t* col_slots;  // (n, cdeg)
@@ -48,43 +52,49 @@ namespace nrx_ldpc {
 
 constexpr float kShortenedLlr = 60.0f;   // ldpc.py:25
 constexpr int kThreads = 256;
-constexpr int kScanThreads = 1024;
 
-struct Flags {
-  int done;
-  int unsat;
-};
+constexpr int kLanes = 32;           // codewords interleaved per group, one per lane
+constexpr int kWarps = 8;            // warps per block = elements per block
 
+// Decoder state, codeword-interleaved: element e of group g for lane l lives
+// at [(g * count + e) * 32 + l], so a warp working on one variable / check
+// moves 128 contiguous bytes for 32 codewords at once.
 struct DecWs {
-  float* chan;
-  float* total;
-  float* c2v;
-  uint8_t* hard;
-  Flags* flags;
+  float* chan;      // [G][n][32]
+  float* total;     // [G][n][32]
+  float* c2v;       // [G][m][dmax][32]
+  uint8_t* hard;    // [G][n][32]
+  uint32_t* done;   // [G] lane mask of finished codewords
+  uint32_t* unsat;  // [G][check blocks] lane mask with an unsatisfied check
 };
 
 size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
+int check_blocks(const nrx_ldpc_code& c) { return (c.m + kWarps - 1) / kWarps; }
+
 DecWs dec_layout(const nrx_ldpc_code& c, int n_cw, uint8_t* base, size_t* total_bytes) {
   DecWs w{};
+  const size_t G = (size_t)(n_cw + kLanes - 1) / kLanes;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
     off = align256(off + bytes);
     return o;
   };
-  const size_t o_chan = take(sizeof(float) * c.n * (size_t)n_cw);
-  const size_t o_total = take(sizeof(float) * c.n * (size_t)n_cw);
-  const size_t o_c2v = take(sizeof(float) * (size_t)c.m * c.dmax * n_cw);
-  const size_t o_hard = take((size_t)c.n * n_cw);
-  const size_t o_flags = take(sizeof(Flags) * (size_t)n_cw);
+  const size_t o_chan = take(sizeof(float) * c.n * kLanes * G);
+  const size_t o_total = take(sizeof(float) * c.n * kLanes * G);
+  const size_t o_c2v = take(sizeof(float) * (size_t)c.m * c.dmax * kLanes * G);
+  const size_t o_hard = take((size_t)c.n * kLanes * G);
+  const size_t o_done = take(sizeof(uint32_t) * G);
+  const size_t o_unsat = take(sizeof(uint32_t) * check_blocks(c) * G);
   if (total_bytes) *total_bytes = off;
   if (base) {
     w.chan = reinterpret_cast<float*>(base + o_chan);
     w.total = reinterpret_cast<float*>(base + o_total);
     w.c2v = reinterpret_cast<float*>(base + o_c2v);
     w.hard = base + o_hard;
-    w.flags = reinterpret_cast<Flags*>(base + o_flags);
+    w.done = reinterpret_cast<uint32_t*>(base + o_done);
+    w.unsat = reinterpret_cast<uint32_t*>(base + o_unsat);
   }
   return w;
 }
@@ -108,54 +118,67 @@ EncWs enc_layout(const nrx_ldpc_code& c, int n_cw, uint8_t* base, size_t* total_
 }
 
 // ---------------------------------------------------------------------------
-// decoder kernels
+// decoder kernels (grid.y = group of 32 codewords)
 // ---------------------------------------------------------------------------
 
-__global__ void k_ldpc_init(nrx_ldpc_code c, const float* llr, DecWs w) {
-  const int cw = blockIdx.y;
-  const size_t ne = (size_t)c.m * c.dmax;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ne || i < (size_t)c.n;
+__global__ void k_ldpc_init(nrx_ldpc_code c, const float* llr, int n_cw, DecWs w) {
+  const int g = blockIdx.y;
+  const size_t ne = (size_t)c.m * c.dmax * kLanes, nv = (size_t)c.n * kLanes;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ne || i < nv;
        i += (size_t)gridDim.x * blockDim.x) {
-    if (i < (size_t)c.n) {
-      const int src = c.chan_src[i];
-      // ln(p0/p1) convention: the channel value is the negated logit LLR
-      w.chan[(size_t)cw * c.n + i] =
-          src >= 0 ? -llr[(size_t)cw * c.ntx + src] : (src == -2 ? kShortenedLlr : 0.f);
+    if (i < nv) {
+      const int j = (int)(i / kLanes), cw = g * kLanes + (int)(i % kLanes);
+      const int src = c.chan_src[j];
+      float v = 0.f;   // ln(p0/p1) convention: the channel value is the negated logit LLR
+      if (cw < n_cw) v = src >= 0 ? -llr[(size_t)cw * c.ntx + src] : (src == -2 ? kShortenedLlr : 0.f);
+      w.chan[(size_t)g * nv + i] = v;
     }
-    if (i < ne) w.c2v[(size_t)cw * ne + i] = 0.f;
+    if (i < ne) w.c2v[(size_t)g * ne + i] = 0.f;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) w.flags[cw] = Flags{0, 0};
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int valid = min(kLanes, n_cw - g * kLanes);
+    w.done[g] = valid >= kLanes ? 0u : ~((1u << valid) - 1u);   // absent codewords count as done
+  }
 }
 
-// Variable update: total = chan + ((c2v_0 + c2v_1) + c2v_2); hard bits.
-__global__ void __launch_bounds__(kThreads) k_ldpc_var(nrx_ldpc_code c, DecWs w, int only_open) {
-  const int cw = blockIdx.y;
-  if (w.flags[cw].done) return;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= c.n) return;
-  const float* c2v = w.c2v + (size_t)cw * c.m * c.dmax;
+// Variable update, warp per variable: total = chan + ((c2v_0 + c2v_1) + c2v_2).
+__global__ void __launch_bounds__(kWarps * 32) k_ldpc_var(nrx_ldpc_code c, DecWs w, int only_open) {
+  const int g = blockIdx.y;
+  const uint32_t done = w.done[g];
+  if (done == 0xffffffffu) return;
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (j >= c.n || ((done >> lane) & 1u)) return;
+  const float* c2v = w.c2v + (size_t)g * c.m * c.dmax * kLanes;
   float s = 0.f;
   for (int t = 0; t < c.cdeg; ++t) {
     const int r = c.col_rows[(size_t)j * c.cdeg + t];
     if (r < 0) break;
-    const float v = c2v[(size_t)r * c.dmax + c.col_slots[(size_t)j * c.cdeg + t]];
+    const float v = c2v[((size_t)r * c.dmax + c.col_slots[(size_t)j * c.cdeg + t]) * kLanes + lane];
     s = t == 0 ? v : __fadd_rn(s, v);
   }
-  const float tot = __fadd_rn(w.chan[(size_t)cw * c.n + j], s);
-  if (!only_open) w.total[(size_t)cw * c.n + j] = tot;
-  w.hard[(size_t)cw * c.n + j] = tot < 0.f ? 1 : 0;
+  const size_t e = ((size_t)g * c.n + j) * kLanes + lane;
+  const float tot = __fadd_rn(w.chan[e], s);
+  if (!only_open) w.total[e] = tot;
+  w.hard[e] = tot < 0.f ? 1 : 0;
 }
 
-// Check update (two passes over the row) + syndrome of this iteration's hard bits.
-__global__ void __launch_bounds__(kThreads) k_ldpc_check(nrx_ldpc_code c, DecWs w) {
-  const int cw = blockIdx.y;
-  if (w.flags[cw].done) return;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+// Check update, warp per check (two passes over the row), plus the lanes whose
+// hard bits violate this check.
+__global__ void __launch_bounds__(kWarps * 32) k_ldpc_check(nrx_ldpc_code c, DecWs w) {
+  __shared__ uint32_t block_unsat;
+  const int g = blockIdx.y;
+  const uint32_t done = w.done[g];
+  if (done == 0xffffffffu) return;   // uniform over the block
+  if (threadIdx.x == 0) block_unsat = 0u;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kWarps + (threadIdx.x >> 5);
   int syn = 0;
-  if (r < c.m) {
+  if (r < c.m && !((done >> lane) & 1u)) {
     const int32_t* cols = c.row_cols + (size_t)r * c.dmax;
-    float* msg = w.c2v + ((size_t)cw * c.m + r) * c.dmax;
-    const float* tot = w.total + (size_t)cw * c.n;
+    float* msg = w.c2v + (((size_t)g * c.m + r) * c.dmax) * kLanes + lane;
+    const float* tot = w.total + (size_t)g * c.n * kLanes + lane;
     float min1 = INFINITY, min2 = INFINITY;
     int amin = 0, neg = 0;
     bool first = true;
@@ -163,9 +186,9 @@ __global__ void __launch_bounds__(kThreads) k_ldpc_check(nrx_ldpc_code c, DecWs 
       const int col = cols[s];
       float mag = INFINITY;
       if (col >= 0) {
-        const float v = tot[col];
+        const float v = tot[(size_t)col * kLanes];
         syn ^= v < 0.f ? 1 : 0;
-        const float x = __fsub_rn(v, msg[s]);
+        const float x = __fsub_rn(v, msg[s * kLanes]);
         mag = fabsf(x);
         neg ^= x < 0.f ? 1 : 0;
       }
@@ -183,32 +206,43 @@ __global__ void __launch_bounds__(kThreads) k_ldpc_check(nrx_ldpc_code c, DecWs 
     for (int s = 0; s < c.dmax; ++s) {
       const int col = cols[s];
       if (col < 0) {
-        msg[s] = 0.f;
+        msg[s * kLanes] = 0.f;
         continue;
       }
-      const float x = __fsub_rn(tot[col], msg[s]);
+      const float x = __fsub_rn(tot[(size_t)col * kLanes], msg[s * kLanes]);
       const float sg = x < 0.f ? -1.f : 1.f;
-      msg[s] = __fmul_rn(rs * sg, s == amin ? min2 : min1);
+      msg[s * kLanes] = __fmul_rn(rs * sg, s == amin ? min2 : min1);
     }
   }
-  if (__syncthreads_or(syn) && threadIdx.x == 0) atomicOr(&w.flags[cw].unsat, 1);
+  const uint32_t bal = __ballot_sync(0xffffffffu, syn);
+  if (lane == 0 && bal) atomicOr(&block_unsat, bal);
+  __syncthreads();
+  if (threadIdx.x == 0) w.unsat[(size_t)g * gridDim.x + blockIdx.x] = block_unsat;
 }
 
 // A codeword whose checks were all satisfied by this iteration's hard bits is done.
-__global__ void k_ldpc_flag(DecWs w, int n_cw) {
-  const int cw = blockIdx.x * blockDim.x + threadIdx.x;
-  if (cw >= n_cw) return;
-  Flags f = w.flags[cw];
-  if (!f.done && !f.unsat) f.done = 1;
-  f.unsat = 0;
-  w.flags[cw] = f;
+__global__ void k_ldpc_flag(DecWs w, int nblk) {
+  __shared__ uint32_t acc;
+  const int g = blockIdx.x;
+  const uint32_t done = w.done[g];
+  if (done == 0xffffffffu) return;
+  if (threadIdx.x == 0) acc = 0u;
+  __syncthreads();
+  uint32_t v = 0u;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) v |= w.unsat[(size_t)g * nblk + i];
+  v = __reduce_or_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && v) atomicOr(&acc, v);
+  __syncthreads();
+  if (threadIdx.x == 0) w.done[g] = done | ~acc;
 }
 
 __global__ void k_ldpc_extract(nrx_ldpc_code c, DecWs w, uint8_t* info, uint8_t* success, int n_cw) {
-  const int cw = blockIdx.y;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c.k_eff; i += gridDim.x * blockDim.x)
-    info[(size_t)cw * c.k_eff + i] = w.hard[(size_t)cw * c.n + c.keep_pos[i]];
-  if (blockIdx.x == 0 && threadIdx.x == 0) success[cw] = static_cast<uint8_t>(w.flags[cw].done);
+  const int g = blockIdx.y;
+  const int lane = threadIdx.x & 31, cw = g * kLanes + lane;
+  if (cw >= n_cw) return;
+  for (int i = blockIdx.x * kWarps + (threadIdx.x >> 5); i < c.k_eff; i += gridDim.x * kWarps)
+    info[(size_t)cw * c.k_eff + i] = w.hard[((size_t)g * c.n + c.keep_pos[i]) * kLanes + lane];
+  if (blockIdx.x == 0 && threadIdx.x < 32) success[cw] = static_cast<uint8_t>((w.done[g] >> lane) & 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -236,40 +270,17 @@ __global__ void k_enc_syn(nrx_ldpc_code c, EncWs w) {
   w.syn[(size_t)cw * c.m + r] = static_cast<uint8_t>(s);
 }
 
-// p_i = s_0 ^ ... ^ s_i written to the chain's parity column, one block per codeword.
-__global__ void __launch_bounds__(kScanThreads) k_enc_chain(nrx_ldpc_code c, EncWs w) {
-  __shared__ int warp_x[kScanThreads / 32];
-  const int cw = blockIdx.x;
+// Accumulator chains: p_i = s_i ^ p_{i-Z}, one thread per chain z < Z.
+__global__ void k_enc_chain(nrx_ldpc_code c, EncWs w) {
+  const int cw = blockIdx.y;
+  const int z = blockIdx.x * blockDim.x + threadIdx.x;
+  if (z >= c.chain_step) return;
   const uint8_t* syn = w.syn + (size_t)cw * c.m;
   uint8_t* bits = w.cw + (size_t)cw * c.n;
-  const int per = (c.m + kScanThreads - 1) / kScanThreads;
-  const int beg = threadIdx.x * per, end = min(c.m, beg + per);
-  int x = 0;
-  for (int i = beg; i < end; ++i) x ^= syn[i];
-  // exclusive XOR scan of the per-thread segment parities
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int incl = x;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl ^= y;
-  }
-  if (lane == 31) warp_x[wid] = incl;
-  __syncthreads();
-  if (wid == 0) {
-    int v = lane < kScanThreads / 32 ? warp_x[lane] : 0;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, v, d);
-      if (lane >= d) v ^= y;
-    }
-    if (lane < kScanThreads / 32) warp_x[lane] = v;   // inclusive over warps
-  }
-  __syncthreads();
-  int acc = (incl ^ x) ^ (wid > 0 ? warp_x[wid - 1] : 0);   // exclusive prefix of this segment
-  for (int i = beg; i < end; ++i) {
+  uint8_t acc = 0;
+  for (int i = z; i < c.m; i += c.chain_step) {
     acc ^= syn[i];
-    bits[c.chain_cols[i]] = static_cast<uint8_t>(acc);
+    bits[c.chain_cols[i]] = acc;
   }
 }
 
@@ -435,6 +446,7 @@ extern "C" int nrx_ldpc_create(const nrx_ldpc_desc* d, nrx_ldpc_code** out) {
   }
   if (keep_pos.empty() || tx_pos.empty()) return NRX_ERR_INVALID;
   if (d->chain_cols) {
+    if (d->chain_step < 1 || d->chain_step > m) return NRX_ERR_INVALID;
     for (int i = 0; i < m; ++i)
       if (d->chain_cols[i] < 0 || d->chain_cols[i] >= n || info_slot[d->chain_cols[i]] != -2) return NRX_ERR_INVALID;
   }
@@ -447,6 +459,7 @@ extern "C" int nrx_ldpc_create(const nrx_ldpc_desc* d, nrx_ldpc_code** out) {
   c->k_eff = static_cast<int>(keep_pos.size());
   c->ntx = static_cast<int>(tx_pos.size());
   c->has_chain = d->chain_cols != nullptr;
+  c->chain_step = d->chain_step;
   int rc = NRX_OK;
   rc = rc ? rc : upload(&c->row_cols, std::vector<int32_t>(d->row_cols, d->row_cols + (size_t)m * d->dmax));
   rc = rc ? rc : upload(&c->col_rows, std::vector<int32_t>(d->col_rows, d->col_rows + (size_t)n * d->cdeg));
@@ -494,22 +507,23 @@ extern "C" int nrx_ldpc_decode(const nrx_ldpc_code* c, int n_cw, const float* ll
                                uint8_t* info_out, uint8_t* success, void* ws, size_t ws_bytes, void* stream) {
   if (!c || n_cw < 0 || iterations < 0 || !llr || !info_out || !success) return NRX_ERR_INVALID;
   if (n_cw == 0) return NRX_OK;
-  if (n_cw > 65535) return NRX_ERR_UNSUPPORTED;
+  const int G = (n_cw + kLanes - 1) / kLanes;
+  if (G > 65535) return NRX_ERR_UNSUPPORTED;
   size_t need = 0;
   dec_layout(*c, n_cw, nullptr, &need);
   if (!ws || ws_bytes < need) return NRX_ERR_WORKSPACE;
   const DecWs w = dec_layout(*c, n_cw, static_cast<uint8_t*>(ws), nullptr);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int vb = (c->n + kThreads - 1) / kThreads, cb = (c->m + kThreads - 1) / kThreads;
-  k_ldpc_init<<<dim3(256, n_cw), kThreads, 0, st>>>(*c, llr, w);
+  const int vb = (c->n + kWarps - 1) / kWarps, cb = check_blocks(*c);
+  k_ldpc_init<<<dim3(512, G), 256, 0, st>>>(*c, llr, n_cw, w);
   for (int it = 0; it < iterations; ++it) {
-    k_ldpc_var<<<dim3(vb, n_cw), kThreads, 0, st>>>(*c, w, 0);
-    k_ldpc_check<<<dim3(cb, n_cw), kThreads, 0, st>>>(*c, w);
-    k_ldpc_flag<<<(n_cw + 255) / 256, 256, 0, st>>>(w, n_cw);
+    k_ldpc_var<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w, 0);
+    k_ldpc_check<<<dim3(cb, G), kWarps * 32, 0, st>>>(*c, w);
+    k_ldpc_flag<<<G, 256, 0, st>>>(w, cb);
   }
   // codewords that never satisfied every check: hard bits of the final messages
-  k_ldpc_var<<<dim3(vb, n_cw), kThreads, 0, st>>>(*c, w, 1);
-  k_ldpc_extract<<<dim3(64, n_cw), kThreads, 0, st>>>(*c, w, info_out, success, n_cw);
+  k_ldpc_var<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w, 1);
+  k_ldpc_extract<<<dim3(256, G), kWarps * 32, 0, st>>>(*c, w, info_out, success, n_cw);
   return launch_status();
 }
 
@@ -526,7 +540,7 @@ extern "C" int nrx_ldpc_encode(const nrx_ldpc_code* c, int n_cw, const uint8_t* 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   k_enc_place<<<dim3((c->n + kThreads - 1) / kThreads, n_cw), kThreads, 0, st>>>(*c, info, w);
   k_enc_syn<<<dim3((c->m + kThreads - 1) / kThreads, n_cw), kThreads, 0, st>>>(*c, w);
-  k_enc_chain<<<n_cw, kScanThreads, 0, st>>>(*c, w);
+  k_enc_chain<<<dim3((c->chain_step + kThreads - 1) / kThreads, n_cw), kThreads, 0, st>>>(*c, w);
   k_enc_tx<<<dim3((c->ntx + kThreads - 1) / kThreads, n_cw), kThreads, 0, st>>>(*c, w, tx);
   return launch_status();
 }

@@ -15,7 +15,7 @@ k x m GF(2) matrix; a 273-PRB 16-QAM codeword (n0 = 169,838) is out of reach
 for both.  ``ira_code`` builds a rate-1/2 irregular-repeat-accumulate code
 instead: information columns of weight 3 spread over the checks by a seeded
 socket permutation (every check gets exactly three), plus a staircase
-(accumulator) parity part, so encoding is one XOR prefix scan.  The chain
+(accumulator) parity part, so encoding is a handful of XOR chain walks.  The chain
 order of the parity columns is a stride permutation, so the reference's
 rate-matching rule (puncture the trailing parity positions) removes parity
 bits spread evenly along the accumulator.  The same min-sum decoder runs the
@@ -50,6 +50,7 @@ class LdpcCode:
     punctured: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.int64))
     shortened: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.int64))
     chain_cols: np.ndarray | None = None   # (M,) parity column of chain position i
+    chain_step: int = 1                    # check i holds chain positions i - chain_step and i
 
     @property
     def num_checks(self) -> int:
@@ -94,9 +95,13 @@ def ira_code(k0: int, seed: int = 0) -> LdpcCode:
 
     Information column j sits in three distinct checks: 3 k0 sockets are
     dealt to the checks by a seeded permutation (three per check), and
-    repeated checks inside a column are swapped away.  Check i also holds the
-    accumulator chain positions i-1 and i; chain position i is parity column
-    k0 + (i * g mod k0), g a stride near the golden ratio coprime to k0."""
+    repeated checks inside a column are swapped away.  The parity part is a
+    block staircase: check i holds accumulator positions i - Z and i, i.e. Z
+    interleaved accumulator chains of length <= 16 (Z = ceil(k0 / 16)), the
+    dual-diagonal structure of quasi-cyclic LDPC parity parts, so belief
+    propagation crosses the accumulator in ~16 steps instead of k0.  Chain
+    position i is parity column k0 + (i * g mod k0), g a stride near the
+    golden ratio coprime to k0, which spreads the punctured tail columns."""
     if k0 < 3:
         raise ValueError(f"IRA code needs k0 >= 3, got {k0}")
     m, n = k0, 2 * k0
@@ -116,10 +121,11 @@ def ira_code(k0: int, seed: int = 0) -> LdpcCode:
         raise RuntimeError("could not place the information edges")
     rows.sort(axis=1)
     g = _coprime_stride(m)
+    z = max(1, -(-m // 16))
     chain_cols = k0 + (np.arange(m, dtype=np.int64) * g) % m
     # edge list (column, row)
-    e_col = [np.repeat(np.arange(k0), 3), chain_cols, chain_cols[:-1]]
-    e_row = [rows.reshape(-1), np.arange(m), np.arange(1, m)]
+    e_col = [np.repeat(np.arange(k0), 3), chain_cols, chain_cols[: m - z]]
+    e_row = [rows.reshape(-1), np.arange(m), np.arange(z, m)]
     col = np.concatenate(e_col)
     row = np.concatenate(e_row)
     order = np.lexsort((col, row))
@@ -141,7 +147,7 @@ def ira_code(k0: int, seed: int = 0) -> LdpcCode:
     col_rows[ccol, cpos] = crow
     col_slots[ccol, cpos] = cslot
     return LdpcCode(n, k0, row_cols, col_rows, col_slots, np.arange(k0, dtype=np.int64),
-                    chain_cols=chain_cols.astype(np.int64))
+                    chain_cols=chain_cols.astype(np.int64), chain_step=z)
 
 
 def rate_matched_ira_code(num_tx_bits: int, rate: float, seed: int = 0) -> LdpcCode:
@@ -159,7 +165,8 @@ def rate_matched_ira_code(num_tx_bits: int, rate: float, seed: int = 0) -> LdpcC
     parity_positions = np.setdiff1d(np.arange(base.n), base.info_positions)
     punctured = parity_positions[num_tx_bits - k_eff:]
     code = LdpcCode(base.n, base.k, base.row_cols, base.col_rows, base.col_slots, base.info_positions,
-                    np.asarray(punctured, dtype=np.int64), np.asarray(shortened, dtype=np.int64), base.chain_cols)
+                    np.asarray(punctured, dtype=np.int64), np.asarray(shortened, dtype=np.int64), base.chain_cols,
+                    base.chain_step)
     assert code.num_tx_bits == num_tx_bits and code.k_eff == k_eff
     return code
 
@@ -190,6 +197,7 @@ class GpuLdpc:
         d.n_punctured, d.punctured = arr["punct"].size, arr["punct"].ctypes.data if arr["punct"].size else None
         d.n_shortened, d.shortened = arr["short"].size, arr["short"].ctypes.data if arr["short"].size else None
         d.chain_cols = chain.ctypes.data if chain is not None else None
+        d.chain_step = int(code.chain_step)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             code_rc = self.lib.nrx_ldpc_create(ctypes.byref(d), ctypes.byref(h))

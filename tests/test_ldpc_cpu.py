@@ -47,16 +47,17 @@ def test_ira_structure():
     assert (n, m, k) == (1000, 500, 500)
     deg = (code.col_rows >= 0).sum(axis=1)
     assert (deg[:k] == 3).all()
-    chain = code.chain_cols
+    chain, z = code.chain_cols, code.chain_step
+    assert z == 32                                              # ceil(500 / 16)
     assert sorted(chain.tolist()) == list(range(k, n))
-    assert deg[chain[:-1]].tolist() == [2] * (m - 1) and deg[chain[-1]] == 1
-    # every check: exactly three information columns, chain positions i-1 and i
+    assert (deg[chain[: m - z]] == 2).all() and (deg[chain[m - z:]] == 1).all()
+    # every check: exactly three information columns, chain positions i-Z and i
     rc = code.row_cols
     info_deg = ((rc >= 0) & (rc < k)).sum(axis=1)
     assert (info_deg == 3).all()
-    for i in (0, 1, 250, m - 1):
+    for i in (0, 1, 31, 32, 250, m - 1):
         par = sorted(c for c in rc[i] if c >= k)
-        want = sorted([chain[i]] + ([chain[i - 1]] if i else []))
+        want = sorted([chain[i]] + ([chain[i - z]] if i >= z else []))
         assert par == want
     # column lists consistent with the row lists, no repeated check in a column
     for j in range(n):
