@@ -1,0 +1,92 @@
+"""Classical baseline receiver on the GPU: the
+reference's "ls_lmmse" ReceiverBank entry — comb LS estimate, per-RE LMMSE
+equalisation, exact APP demapping, clipping — as one kernel
+(``nrx_ls_lmmse``, include/nrx_classical.h).
+
+Reference interfaces mirrored (file:line under /root/reference/pkg/src/nrxsim):
+  ls_estimate / lmmse_equalize / app_demap     classical.py:40-174
+  ReceiverBank.run("ls_lmmse")                 evaluation.py:79-84, 130-135
+
+``GpuLsLmmse`` has the ``forward_device`` signature of ``NrxEngine``, so the
+GPU Monte-Carlo loops (slotgen.evaluate_uncoded, ldpc.evaluate_coded) run it
+as the comparison receiver on exactly the same slots.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .slotgen import qam_table
+
+LLR_CLIP = 20.0   # classical.py:24 / evaluation.py:27
+
+
+@dataclass(frozen=True)
+class _RxConfig:
+    """The fields the GPU Monte-Carlo loops read from a receiver's config."""
+    m_max: int
+    num_iterations: int = 1
+    variant: str = "single"
+
+
+class GpuLsLmmse:
+    """LS + LMMSE + exact APP demap on the device (float64 arithmetic)."""
+
+    needs_n0 = True
+
+    def __init__(self, bs_antennas: int = 4, m_max: int = 8, clip: float = LLR_CLIP, device=None):
+        from .engine import _require_cuda
+        torch = _require_cuda()
+        self.lib = _lib.load()
+        self.bs_antennas = int(bs_antennas)
+        self.clip = float(clip)
+        self.config = _RxConfig(m_max=int(m_max))
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._qam = np.ascontiguousarray(qam_table())
+
+    def forward_device(self, cfg, y, pilots, noise_feat, mod_order, num_iterations, llr, chest=None,
+                       workspace=None, stream=None, n0=None):
+        """y (N,S,T,B), pilots (P,U,F,K), mod_order (N*U,) int32, n0 (N,)
+        float64 device tensors -> llr (N,U,S,T,W) float32 (chest untouched)."""
+        import torch
+        if n0 is None:
+            raise ValueError("the LMMSE receiver needs the linear noise power n0 per slot")
+        n = y.shape[0]
+        n0 = n0.to(device=self.device, dtype=torch.float64).reshape(-1).contiguous()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        s = _lib.slot_desc(cfg)
+        rc = self.lib.nrx_ls_lmmse(ctypes.byref(s), self.bs_antennas, n, y.data_ptr(),
+                                   int(y.dtype == torch.complex128), pilots.data_ptr(),
+                                   int(pilots.dtype == torch.complex128), pilots.shape[0], n0.data_ptr(),
+                                   mod_order.data_ptr(), self._qam.ctypes.data, self.clip, llr.data_ptr(),
+                                   llr.shape[-1], st.cuda_stream)
+        _lib.check(rc, "nrx_ls_lmmse")
+
+
+def ls_lmmse_llrs(y, books, cfg, mcs_per_ue, n0, clip: float = LLR_CLIP, device=None):
+    """numpy in/out drop-in for ReceiverBank.run("ls_lmmse") (evaluation.py:130-135):
+    y (N,S,T,B), per-slot books (or one book), scalar or (N,) n0 -> list per UE
+    of (N,S,T,m_u) float32 LLR grids clipped to +-clip."""
+    import torch
+    from .nrx import stack_pilots
+    y = np.asarray(y)
+    n = y.shape[0]
+    orders = [m.modulation_order for m in mcs_per_ue]
+    rx = GpuLsLmmse(cfg.bs_antennas, max(orders), clip, device)
+    dev = rx.device
+    pil = torch.from_numpy(np.ascontiguousarray(stack_pilots(books, n, cfg))).to(dev)
+    yt = torch.from_numpy(np.ascontiguousarray(y.astype(np.complex128))).to(dev)
+    n0_t = torch.from_numpy(np.broadcast_to(np.asarray(n0, dtype=np.float64).reshape(-1), (n,)).copy()).to(dev)
+    mods = torch.tensor(orders * n, dtype=torch.int32, device=dev)
+    llr = torch.empty((n, cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, max(orders)), dtype=torch.float32,
+                      device=dev)
+    rx.forward_device(cfg, yt, pil.to(torch.complex128), None, mods, 1, llr, n0=n0_t)
+    out = llr.cpu().numpy()
+    return [out[:, u, ..., :m] for u, m in enumerate(orders)]
+
+
+__all__ = ["GpuLsLmmse", "ls_lmmse_llrs", "LLR_CLIP"]

@@ -330,7 +330,8 @@ def evaluate_coded(engine, source, mcs_per_ue, snr_db_grid, n_slots: int, batch:
                 payload.append(info)
             sb = source.generate(nb, mods[: nb * U], n0_t[:nb], seed=key + 15, first_slot=start,
                                  variates={"labels": labels[:nb]})
-            engine.forward_device(cfg, sb.y, sb.pilots, nf[:nb], sb.mod_order, n_it, llr[:nb], chest[:nb])
+            extra = {"n0": sb.n0} if getattr(engine, "needs_n0", False) else {}
+            engine.forward_device(cfg, sb.y, sb.pilots, nf[:nb], sb.mod_order, n_it, llr[:nb], chest[:nb], **extra)
             errs.zero_()
             for u, d in enumerate(dec):
                 cw_llr = torch.empty((nb, d.num_tx_bits), dtype=torch.float32, device=dev)

@@ -396,7 +396,8 @@ def evaluate_uncoded(engine, source: GpuSlotSource, mcs_per_ue, snr_db_grid, n_s
             sb = source.generate(nb, mods[: nb * U], n0_t[:nb], seed=(int(seed) << 16) + k, first_slot=start,
                                  out=out if out is not None and out.y.shape[0] == nb else None)
             out = sb
-            engine.forward_device(cfg, sb.y, sb.pilots, nf[:nb], sb.mod_order, n_it, llr[:nb], chest[:nb])
+            extra = {"n0": sb.n0} if getattr(engine, "needs_n0", False) else {}
+            engine.forward_device(cfg, sb.y, sb.pilots, nf[:nb], sb.mod_order, n_it, llr[:nb], chest[:nb], **extra)
             e = errs[: nb * U].zero_()
             count_bit_errors(cfg, llr[:nb], sb.labels, sb.mod_order, out=e)
             tot += torch.stack([(e > 0).sum(), e.sum()])
