@@ -409,8 +409,9 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
           tmem_ld8(tcol + 8 * cc, mv);
           ld_shared_f8(stb1_s + 32u * cc, bb);
           tmem_wait_ld();
+          // channels >= d come out as exact zeros: zero fc1 columns and zero bias padding
 #pragma unroll
-          for (int e = 0; e < 8; ++e) mv[e] = 8 * cc + 8 <= g.d || 8 * cc + e < g.d ? mv[e] + bb[e] : 0.f;
+          for (int e = 0; e < 8; ++e) mv[e] += bb[e];
           *reinterpret_cast<uint4*>(mrow + (size_t)cc * g.rows_slab * 8) =
               mask_chunk(pack_chunk(mv, static_cast<const ET*>(nullptr)), vmask);
         }
