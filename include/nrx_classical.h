@@ -49,6 +49,27 @@ int nrx_ls_lmmse(const nrx_slot_desc* slot, int bs_antennas, int n_slots, const 
                  const int32_t* mod_order, const double* qam_points, float clip, float* llr_out, int llr_width,
                  void* stream);
 
+/*
+ * K-Best detection with max-log LLRs on a given channel (the reference's
+ * "perfect_kbest" receiver with the true effective channel:
+ * classical.kbest_detect classical.py:195-261 via evaluation._kbest_grids
+ * :87-111).  Breadth-first over the streams U-1 .. 0 after a QR of the
+ * B x U channel, keeping the k best partial paths (k <= NRX_CL_MAX_K);
+ * LLR = (min metric with bit 0 - min metric with bit 1) / max(n0, 1e-12),
+ * +-clip when a hypothesis is missing from the list.  Data REs only (the
+ * other REs of llr_out are written as zeros, like the reference's grids).
+ *   h   (n_slots, U, S, T, B) complex channel (h_c128 selects double2)
+ *   reference_pairing  1: reproduce the reference exactly — its interference
+ *       term pairs R[level, level+1:] (ascending streams) with the decided
+ *       symbols in decision order (descending streams), classical.py:220-221,
+ *       which is the true interference only for U <= 2; 0: the correct
+ *       pairing R[level, j] * x_j (differs from the reference for U >= 3).
+ */
+#define NRX_CL_MAX_K 32
+int nrx_kbest(const nrx_slot_desc* slot, int bs_antennas, int n_slots, const void* y, int y_c128, const void* h,
+              int h_c128, const double* n0, const int32_t* mod_order, const double* qam_points, int k,
+              int reference_pairing, float clip, float* llr_out, int llr_width, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,11 +1,13 @@
-"""Classical baseline receiver on the GPU: the
+"""Classical baseline receivers on the GPU: the
 reference's "ls_lmmse" ReceiverBank entry — comb LS estimate, per-RE LMMSE
-equalisation, exact APP demapping, clipping — as one kernel
-(``nrx_ls_lmmse``, include/nrx_classical.h).
+equalisation, exact APP demapping, clipping — and its "perfect_kbest"
+entry — K-Best detection with max-log LLRs on the true channel — as one
+kernel each (``nrx_ls_lmmse``, ``nrx_kbest``, include/nrx_classical.h).
 
 Reference interfaces mirrored (file:line under /root/reference/pkg/src/nrxsim):
   ls_estimate / lmmse_equalize / app_demap     classical.py:40-174
-  ReceiverBank.run("ls_lmmse")                 evaluation.py:79-84, 130-135
+  kbest_detect                                 classical.py:195-261
+  ReceiverBank.run("ls_lmmse" / "perfect_kbest")  evaluation.py:79-111, 130-140
 
 ``GpuLsLmmse`` has the ``forward_device`` signature of ``NrxEngine``, so the
 GPU Monte-Carlo loops (slotgen.evaluate_uncoded, ldpc.evaluate_coded) run it
@@ -67,6 +69,69 @@ class GpuLsLmmse:
         _lib.check(rc, "nrx_ls_lmmse")
 
 
+class GpuKBest:
+    """K-Best detection with max-log LLRs on the true effective channel
+    (the reference's "perfect_kbest", evaluation.py:139-140); float64."""
+
+    needs_n0 = True
+    needs_h_eff = True
+
+    def __init__(self, bs_antennas: int = 4, m_max: int = 8, k: int = 16, clip: float = LLR_CLIP, device=None,
+                 reference_pairing: bool = True):
+        """reference_pairing=True reproduces the reference bit for bit, whose
+        interference term pairs R[level, level+1:] with the decided symbols in
+        decision (descending-stream) order (classical.py:220-221) — correct
+        for U <= 2 only; False uses the true R[level, j] x_j for any U."""
+        from .engine import _require_cuda
+        torch = _require_cuda()
+        self.lib = _lib.load()
+        self.bs_antennas, self.k, self.clip = int(bs_antennas), int(k), float(clip)
+        self.reference_pairing = bool(reference_pairing)
+        self.config = _RxConfig(m_max=int(m_max))
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._qam = np.ascontiguousarray(qam_table())
+
+    def forward_device(self, cfg, y, pilots, noise_feat, mod_order, num_iterations, llr, chest=None,
+                       workspace=None, stream=None, n0=None, h_eff=None):
+        """y (N,S,T,B), h_eff (N,U,S,T,B), n0 (N,) float64, mod_order (N*U,)
+        device tensors -> llr (N,U,S,T,W) float32 on the data REs (zeros elsewhere)."""
+        import torch
+        if n0 is None or h_eff is None:
+            raise ValueError("K-Best needs the noise power n0 and the channel h_eff per slot")
+        n0 = n0.to(device=self.device, dtype=torch.float64).reshape(-1).contiguous()
+        h_eff = h_eff.contiguous()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        s = _lib.slot_desc(cfg)
+        rc = self.lib.nrx_kbest(ctypes.byref(s), self.bs_antennas, y.shape[0], y.data_ptr(),
+                                int(y.dtype == torch.complex128), h_eff.data_ptr(),
+                                int(h_eff.dtype == torch.complex128), n0.data_ptr(), mod_order.data_ptr(),
+                                self._qam.ctypes.data, self.k, int(self.reference_pairing), self.clip,
+                                llr.data_ptr(), llr.shape[-1],
+                                st.cuda_stream)
+        _lib.check(rc, "nrx_kbest")
+
+
+def kbest_llrs(y, h_eff, cfg, mcs_per_ue, n0, k: int = 16, clip: float = LLR_CLIP, device=None,
+               reference_pairing: bool = True):
+    """numpy drop-in for ReceiverBank.run("perfect_kbest"): y (N,S,T,B),
+    true h_eff (N,U,S,T,B) -> list per UE of (N,S,T,m_u) float32 grids."""
+    import torch
+    y = np.asarray(y)
+    n = y.shape[0]
+    orders = [m.modulation_order for m in mcs_per_ue]
+    rx = GpuKBest(cfg.bs_antennas, max(orders), k, clip, device, reference_pairing)
+    dev = rx.device
+    yt = torch.from_numpy(np.ascontiguousarray(y.astype(np.complex128))).to(dev)
+    ht = torch.from_numpy(np.ascontiguousarray(np.asarray(h_eff).astype(np.complex128))).to(dev)
+    n0_t = torch.from_numpy(np.broadcast_to(np.asarray(n0, dtype=np.float64).reshape(-1), (n,)).copy()).to(dev)
+    mods = torch.tensor(orders * n, dtype=torch.int32, device=dev)
+    llr = torch.empty((n, cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, max(orders)), dtype=torch.float32,
+                      device=dev)
+    rx.forward_device(cfg, yt, None, None, mods, 1, llr, n0=n0_t, h_eff=ht)
+    out = llr.cpu().numpy()
+    return [out[:, u, ..., :m] for u, m in enumerate(orders)]
+
+
 def ls_lmmse_llrs(y, books, cfg, mcs_per_ue, n0, clip: float = LLR_CLIP, device=None):
     """numpy in/out drop-in for ReceiverBank.run("ls_lmmse") (evaluation.py:130-135):
     y (N,S,T,B), per-slot books (or one book), scalar or (N,) n0 -> list per UE
@@ -89,4 +154,4 @@ def ls_lmmse_llrs(y, books, cfg, mcs_per_ue, n0, clip: float = LLR_CLIP, device=
     return [out[:, u, ..., :m] for u, m in enumerate(orders)]
 
 
-__all__ = ["GpuLsLmmse", "ls_lmmse_llrs", "LLR_CLIP"]
+__all__ = ["GpuLsLmmse", "GpuKBest", "ls_lmmse_llrs", "kbest_llrs", "LLR_CLIP"]

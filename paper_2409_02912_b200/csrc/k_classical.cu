@@ -205,6 +205,143 @@ __global__ void __launch_bounds__(128) k_ls_lmmse(ClParams p) {
   }
 }
 
+struct KbParams {
+  int S, T, U, B, W, K, ref_pairing;
+  int is_pilot[32];
+  float clip;
+  double2 qam[NRX_SG_QAM_POINTS];
+  const void* y;
+  int y_c128;
+  const void* h;
+  int h_c128;
+  const double* n0;
+  const int32_t* mod;
+  float* llr;
+};
+
+// One thread per RE: MGS QR of the B x U channel, breadth-first K-Best over
+// the streams U-1 .. 0 (the reference's level order), max-log LLRs from the
+// final list.  Partial-path metrics are invariant to the per-column phase
+// of the QR, so MGS (positive real diagonal) and LAPACK's Householder QR
+// give the same metrics up to float64 rounding.
+__global__ void __launch_bounds__(128) k_kbest(KbParams p) {
+  const int n = blockIdx.y;
+  const int re = blockIdx.x * blockDim.x + threadIdx.x;
+  if (re >= p.S * p.T) return;
+  const int s = re / p.T, t = re - s * p.T;
+  const int B = p.B, U = p.U;
+  if (p.is_pilot[t]) {
+    for (int u = 0; u < U; ++u) {
+      float* out = p.llr + ((((size_t)n * U + u) * p.S + s) * p.T + t) * p.W;
+      for (int j = 0; j < p.W; ++j) out[j] = 0.f;
+    }
+    return;
+  }
+  double2 q[NRX_CL_MAX_RX_ANT][NRX_CL_MAX_UES], r[NRX_CL_MAX_UES][NRX_CL_MAX_UES], yt[NRX_CL_MAX_UES];
+  for (int u = 0; u < U; ++u) {
+    double2 v[NRX_CL_MAX_RX_ANT];
+    for (int b = 0; b < B; ++b) v[b] = ldc(p.h, ((((size_t)n * U + u) * p.S + s) * p.T + t) * B + b, p.h_c128);
+    for (int j = 0; j < u; ++j) {
+      double2 d = make_double2(0.0, 0.0);
+      for (int b = 0; b < B; ++b) {
+        const double2 pr = cconjmul(q[b][j], v[b]);
+        d.x += pr.x;
+        d.y += pr.y;
+      }
+      r[j][u] = d;
+      for (int b = 0; b < B; ++b) {
+        const double2 pr = cmul(d, q[b][j]);
+        v[b].x -= pr.x;
+        v[b].y -= pr.y;
+      }
+    }
+    double nrm = 0.0;
+    for (int b = 0; b < B; ++b) nrm += v[b].x * v[b].x + v[b].y * v[b].y;
+    nrm = sqrt(nrm);
+    r[u][u] = make_double2(nrm, 0.0);
+    for (int j = u + 1; j < U; ++j) r[j][u] = make_double2(0.0, 0.0);
+    const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+    for (int b = 0; b < B; ++b) q[b][u] = make_double2(v[b].x * inv, v[b].y * inv);
+  }
+  for (int u = 0; u < U; ++u) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int b = 0; b < B; ++b) {
+      const double2 pr = cconjmul(q[b][u], ldc(p.y, (((size_t)n * p.S + s) * p.T + t) * B + b, p.y_c128));
+      acc.x += pr.x;
+      acc.y += pr.y;
+    }
+    yt[u] = acc;
+  }
+
+  // breadth-first K-Best: paths hold the symbol index of every decided stream
+  uint8_t sym[NRX_CL_MAX_K][NRX_CL_MAX_UES], nsym[NRX_CL_MAX_K][NRX_CL_MAX_UES];
+  double met[NRX_CL_MAX_K], nmet[NRX_CL_MAX_K];
+  int npath = 1;
+  met[0] = 0.0;
+  for (int level = U - 1; level >= 0; --level) {
+    const int m = p.mod[n * U + level];
+    const int cnt = 1 << m;
+    const double2* pts = p.qam + qam_offset(m);
+    int nn = 0, worst = 0;
+    for (int a = 0; a < npath; ++a) {
+      double2 intf = make_double2(0.0, 0.0);   // already-decided (higher) streams on this row
+      for (int j = level + 1; j < U; ++j) {
+        // reference pairing: R[level, level+1+i] times the i-th decided symbol,
+        // i.e. stream U-1-i (classical.py:220-221); else R[level, j] * x_j
+        const int js = p.ref_pairing ? U - 1 - (j - level - 1) : j;
+        const int mj = p.mod[n * U + js];
+        const double2 pr = cmul(r[level][j], p.qam[qam_offset(mj) + sym[a][js]]);
+        intf.x += pr.x;
+        intf.y += pr.y;
+      }
+      for (int c = 0; c < cnt; ++c) {
+        const double2 rx = cmul(r[level][level], pts[c]);
+        const double dx = yt[level].x - intf.x - rx.x, dy = yt[level].y - intf.y - rx.y;
+        const double hh = hypot(dx, dy);
+        const double mm = met[a] + hh * hh;
+        int slot = -1;
+        if (nn < p.K) {
+          slot = nn++;
+        } else if (mm < nmet[worst]) {
+          slot = worst;
+        }
+        if (slot < 0) continue;
+        nmet[slot] = mm;
+        for (int j = level + 1; j < U; ++j) nsym[slot][j] = sym[a][j];
+        nsym[slot][level] = static_cast<uint8_t>(c);
+        if (nn == p.K) {   // keep track of the largest kept metric
+          worst = 0;
+          for (int i = 1; i < nn; ++i)
+            if (nmet[i] > nmet[worst]) worst = i;
+        }
+      }
+    }
+    npath = nn;
+    for (int a = 0; a < npath; ++a) {
+      met[a] = nmet[a];
+      for (int j = level; j < U; ++j) sym[a][j] = nsym[a][j];
+    }
+  }
+
+  const double n0e = fmax(p.n0[n], kVarFloor);
+  for (int u = 0; u < U; ++u) {
+    const int m = p.mod[n * U + u];
+    float* out = p.llr + ((((size_t)n * U + u) * p.S + s) * p.T + t) * p.W;
+    for (int j = 0; j < m; ++j) {
+      double m1 = INFINITY, m0 = INFINITY;
+      for (int a = 0; a < npath; ++a) {
+        if ((sym[a][u] >> (m - 1 - j)) & 1) m1 = fmin(m1, met[a]);
+        else m0 = fmin(m0, met[a]);
+      }
+      double v = (m0 - m1) / n0e;
+      if (isinf(m0)) v = p.clip;
+      if (isinf(m1)) v = -p.clip;
+      out[j] = static_cast<float>(fmin(fmax(v, -(double)p.clip), (double)p.clip));
+    }
+    for (int j = m; j < p.W; ++j) out[j] = 0.f;
+  }
+}
+
 void builtin_qam(double2* out) {
   for (int m = 2; m <= 8; m += 2) {
     const int cnt = 1 << m;
@@ -284,6 +421,54 @@ extern "C" int nrx_ls_lmmse(const nrx_slot_desc* slot, int bs_antennas, int n_sl
   p.llr = llr_out;
   const dim3 grid((p.S * p.T + 127) / 128, n_slots);
   k_ls_lmmse<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e == cudaErrorNoKernelImageForDevice || e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+    return NRX_ERR_NO_DEVICE;
+  return e == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
+}
+
+extern "C" int nrx_kbest(const nrx_slot_desc* slot, int bs_antennas, int n_slots, const void* y, int y_c128,
+                         const void* h, int h_c128, const double* n0, const int32_t* mod_order,
+                         const double* qam_points, int k, int reference_pairing, float clip, float* llr_out,
+                         int llr_width, void* stream) {
+  if (!slot || n_slots < 0 || !y || !h || !n0 || !mod_order || !llr_out || !(clip > 0.f) || k < 1 ||
+      bs_antennas < 1)
+    return NRX_ERR_INVALID;
+  if (slot->num_subcarriers < 1 || slot->num_symbols < 1 || slot->num_ues < 1 || slot->num_pilot_symbols < 0 ||
+      slot->num_pilot_symbols > NRX_MAX_PILOT_SYMBOLS)
+    return NRX_ERR_INVALID;
+  if (slot->num_symbols > 32 || slot->num_ues > NRX_CL_MAX_UES || bs_antennas > NRX_CL_MAX_RX_ANT ||
+      k > NRX_CL_MAX_K || llr_width < 1 || llr_width > 8)
+    return NRX_ERR_UNSUPPORTED;
+  if (n_slots == 0) return NRX_OK;
+  if (n_slots > 65535) return NRX_ERR_UNSUPPORTED;
+  KbParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.S = slot->num_subcarriers;
+  p.T = slot->num_symbols;
+  p.U = slot->num_ues;
+  p.B = bs_antennas;
+  p.W = llr_width;
+  p.K = k;
+  p.ref_pairing = reference_pairing ? 1 : 0;
+  for (int i = 0; i < slot->num_pilot_symbols; ++i) {
+    if (slot->pilot_symbols[i] < 0 || slot->pilot_symbols[i] >= p.T) return NRX_ERR_INVALID;
+    p.is_pilot[slot->pilot_symbols[i]] = 1;
+  }
+  p.clip = clip;
+  if (qam_points)
+    std::memcpy(p.qam, qam_points, sizeof(p.qam));
+  else
+    builtin_qam(p.qam);
+  p.y = y;
+  p.y_c128 = y_c128;
+  p.h = h;
+  p.h_c128 = h_c128;
+  p.n0 = n0;
+  p.mod = mod_order;
+  p.llr = llr_out;
+  const dim3 grid((p.S * p.T + 127) / 128, n_slots);
+  k_kbest<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);
   const cudaError_t e = cudaPeekAtLastError();
   if (e == cudaErrorNoKernelImageForDevice || e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
     return NRX_ERR_NO_DEVICE;

@@ -329,8 +329,10 @@ def evaluate_coded(engine, source, mcs_per_ue, snr_db_grid, n_slots: int, batch:
                                                   labels.data_ptr(), st.cuda_stream), "nrx_bits_to_labels")
                 payload.append(info)
             sb = source.generate(nb, mods[: nb * U], n0_t[:nb], seed=key + 15, first_slot=start,
-                                 variates={"labels": labels[:nb]})
+                                 variates={"labels": labels[:nb]}, with_h_eff=getattr(engine, "needs_h_eff", False))
             extra = {"n0": sb.n0} if getattr(engine, "needs_n0", False) else {}
+            if getattr(engine, "needs_h_eff", False):
+                extra["h_eff"] = sb.h_eff
             engine.forward_device(cfg, sb.y, sb.pilots, nf[:nb], sb.mod_order, n_it, llr[:nb], chest[:nb], **extra)
             errs.zero_()
             for u, d in enumerate(dec):

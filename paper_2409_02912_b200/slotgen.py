@@ -262,6 +262,8 @@ class GpuSlotSource:
         n0_t = self._dev(n0, torch.float64, (N,))
         if out is not None and out.y.shape[0] == N:
             y, pil, lab, heff = out.y, out.pilots, out.labels, out.h_eff
+            if with_h_eff and heff is None:
+                heff = torch.empty((N, U, S, T, B), dtype=h_dtype, device=dev)
         else:
             y = torch.empty((N, S, T, B), dtype=y_dtype, device=dev)
             pil = torch.empty((N, U, self.F, len(cfg.pilot_symbols)), dtype=pilots_dtype, device=dev)
@@ -394,9 +396,12 @@ def evaluate_uncoded(engine, source: GpuSlotSource, mcs_per_ue, snr_db_grid, n_s
         for start in range(mine.start, mine.stop, cap):
             nb = min(cap, mine.stop - start)
             sb = source.generate(nb, mods[: nb * U], n0_t[:nb], seed=(int(seed) << 16) + k, first_slot=start,
-                                 out=out if out is not None and out.y.shape[0] == nb else None)
+                                 out=out if out is not None and out.y.shape[0] == nb else None,
+                                 with_h_eff=getattr(engine, "needs_h_eff", False))
             out = sb
             extra = {"n0": sb.n0} if getattr(engine, "needs_n0", False) else {}
+            if getattr(engine, "needs_h_eff", False):
+                extra["h_eff"] = sb.h_eff
             engine.forward_device(cfg, sb.y, sb.pilots, nf[:nb], sb.mod_order, n_it, llr[:nb], chest[:nb], **extra)
             e = errs[: nb * U].zero_()
             count_bit_errors(cfg, llr[:nb], sb.labels, sb.mod_order, out=e)

@@ -9,7 +9,7 @@ import pytest
 from oracle import classical_oracle as co
 from oracle import slotgen_oracle as so
 from slotgen_cases import case_names, load_case
-from test_classical_cpu import load_cl
+from test_classical_cpu import GOLDEN, load_cl
 
 pytestmark = pytest.mark.gpu
 
@@ -59,6 +59,46 @@ def test_ls_lmmse_c2_vs_oracle_and_ber():
         assert ber < 0.2, ber
 
 
+@pytest.mark.parametrize("k", [16, 4])
+@pytest.mark.parametrize("name", case_names())
+def test_kbest_matches_reference(name, k):
+    """perfect_kbest on the true channel vs the reference (float64 both
+    sides; list membership can differ only on metric ties at the K-th place,
+    so all but a negligible fraction of LLRs must agree)."""
+    from paper_2409_02912_b200.classical import kbest_llrs
+    from paper_2409_02912_b200.config import McsEntry
+    c = load_case(name)
+    mcs = [McsEntry(0, m, 0.5) for m in c.orders]
+    got = kbest_llrs(c.a["y"], c.a["h_eff"], c.cfg, mcs, c.n0, k=k)
+    with np.load(f"{GOLDEN}/kb_{name}.npz") as z:
+        ref = [z[f"k{k}_llr_{u}"] for u in range(len(c.orders))]
+    for g, r in zip(got, ref):
+        assert g.shape == r.shape
+        close = np.isclose(g, r, rtol=1e-5, atol=1e-4)
+        assert close.mean() > 0.999, (name, k, close.mean())
+
+
+def test_kbest_pairing_modes():
+    """The two interference pairings agree for U <= 2 and differ for U = 3,
+    where the corrected one decides at least as well (reference defect at
+    classical.py:220-221)."""
+    from paper_2409_02912_b200.classical import kbest_llrs
+    from paper_2409_02912_b200.config import McsEntry
+    from paper_2409_02912_b200.slotgen import labels_to_bits
+    for name in ("sg_desk", "sg_u3_comb4"):
+        c = load_case(name)
+        mcs = [McsEntry(0, m, 0.5) for m in c.orders]
+        a = kbest_llrs(c.a["y"], c.a["h_eff"], c.cfg, mcs, c.n0, k=16)
+        b = kbest_llrs(c.a["y"], c.a["h_eff"], c.cfg, mcs, c.n0, k=16, reference_pairing=False)
+        same = all(np.array_equal(x, z) for x, z in zip(a, b))
+        assert same == (len(c.orders) <= 2)
+        if not same:
+            s_idx, t_idx = np.nonzero(c.cfg.data_mask)
+            bits = labels_to_bits(c.a["labels"], c.cfg, c.orders)
+            err = lambda g: sum(int(((x[:, s_idx, t_idx] > 0) != bb).sum()) for x, bb in zip(g, bits))
+            assert err(b) <= err(a)
+
+
 def test_monte_carlo_loops_run_the_baseline():
     from paper_2409_02912_b200.classical import GpuLsLmmse
     from paper_2409_02912_b200.config import McsEntry, SlotConfig, default_mcs_table
@@ -74,3 +114,7 @@ def test_monte_carlo_loops_run_the_baseline():
     cod = evaluate_coded(rx, src, mcs, [0.0, 30.0], n_slots=16, batch=8, receiver="ls_lmmse")
     assert cod[0].receiver == "ls_lmmse" and cod[0].tbler > cod[1].tbler
     assert cod[1].tbler < 0.2
+    from paper_2409_02912_b200.classical import GpuKBest
+    kb = evaluate_uncoded(GpuKBest(4, 4, 16), src, (t[14], t[14]), [0.0, 30.0], n_slots=16, batch=8,
+                          receiver="perfect_kbest")
+    assert kb[1].ber < unc[1].ber + 1e-3 and kb[0].ber < unc[0].ber   # true channel beats LS
