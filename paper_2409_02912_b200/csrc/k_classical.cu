@@ -183,22 +183,30 @@ __global__ void __launch_bounds__(128) k_ls_lmmse(ClParams p) {
     const double2* pts = p.qam + qam_offset(m);
     const int cnt = 1 << m;
     float* out = p.llr + ((((size_t)n * U + u) * p.S + s) * p.T + t) * p.W;
-    for (int kb = 0; kb < m; ++kb) {
-      double top1 = -INFINITY, top0 = -INFINITY;
-      for (int i = 0; i < cnt; ++i) {
-        const double d = hypot(z.x - pts[i].x, z.y - pts[i].y);
-        const double met = -(d * d) / nvar;
-        if ((i >> (m - 1 - kb)) & 1) top1 = fmax(top1, met);
-        else top0 = fmax(top0, met);
+    // log-sum-exp per bit subset with one shared shift (the largest metric):
+    // log(sum_1 e^met) - log(sum_0 e^met) is the reference's per-subset
+    // max-shifted form up to float64 rounding; a subset that underflows gives
+    // +-inf, clipped like the reference's huge finite value.
+    double top = -INFINITY;
+    for (int i = 0; i < cnt; ++i) {
+      const double d = hypot(z.x - pts[i].x, z.y - pts[i].y);
+      top = fmax(top, -(d * d) / nvar);
+    }
+    double s1[8] = {0, 0, 0, 0, 0, 0, 0, 0}, s0[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < cnt; ++i) {
+      const double d = hypot(z.x - pts[i].x, z.y - pts[i].y);
+      const double e = exp(-(d * d) / nvar - top);
+#pragma unroll
+      for (int kb = 0; kb < 8; ++kb) {
+        if (kb >= m) break;
+        if ((i >> (m - 1 - kb)) & 1) s1[kb] += e;
+        else s0[kb] += e;
       }
-      double s1 = 0.0, s0 = 0.0;
-      for (int i = 0; i < cnt; ++i) {
-        const double d = hypot(z.x - pts[i].x, z.y - pts[i].y);
-        const double met = -(d * d) / nvar;
-        if ((i >> (m - 1 - kb)) & 1) s1 += exp(met - top1);
-        else s0 += exp(met - top0);
-      }
-      const double llr = (top1 + log(s1)) - (top0 + log(s0));
+    }
+#pragma unroll
+    for (int kb = 0; kb < 8; ++kb) {
+      if (kb >= m) break;
+      const double llr = log(s1[kb]) - log(s0[kb]);
       out[kb] = fminf(fmaxf(static_cast<float>(llr), -p.clip), p.clip);
     }
     for (int kb = m; kb < p.W; ++kb) out[kb] = 0.f;
