@@ -53,7 +53,9 @@ __device__ __forceinline__ double2 cmul_nofma(double2 a, double2 b) {
                       __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
 }
 
-template <typename OutT, typename YT, typename PT>
+// BT > 0: the rx antenna count fixed at compile time, so the feature row
+// stays in registers (BT = 0: runtime B, the row lives in local memory).
+template <typename OutT, typename YT, typename PT, int BT>
 __global__ void __launch_bounds__(128) k_ls_feat(Geom g, const YT* __restrict__ y, const PT* __restrict__ pilots,
                                                  int n_pilot_sets, const float* __restrict__ noise_feat,
                                                  OutT* __restrict__ feats) {
@@ -70,9 +72,11 @@ __global__ void __launch_bounds__(128) k_ls_feat(Geom g, const YT* __restrict__ 
   for (int c = 0; c < 48; ++c) f[c] = 0.f;
 
   if (valid) {
-    const int B = g.B;
+    const int B = BT > 0 ? BT : g.B;
     const YT* yrow = y + (((size_t)n * g.S + s) * g.T + t) * B;
-    for (int b = 0; b < B; ++b) {
+#pragma unroll
+    for (int b = 0; b < (BT > 0 ? BT : 8); ++b) {
+      if (b >= B) break;
       float2 v = ld_c_f(yrow + b);
       f[2 * b] = v.x;
       f[2 * b + 1] = v.y;
@@ -97,7 +101,9 @@ __global__ void __launch_bounds__(128) k_ls_feat(Geom g, const YT* __restrict__ 
     const double2 q1 = F > 1 ? pilot_scale(ld_c(pil + (size_t)(j + 1) * g.K + k)) : q0;
     const YT* y0 = y + (((size_t)n * g.S + (o + j * g.comb)) * g.T + pt) * B;
     const YT* y1 = y + (((size_t)n * g.S + (o + (j + 1) * g.comb)) * g.T + pt) * B;
-    for (int b = 0; b < B; ++b) {
+#pragma unroll
+    for (int b = 0; b < (BT > 0 ? BT : 8); ++b) {
+      if (b >= B) break;
       const double2 r0 = cmul_nofma(ld_c(y0 + b), q0);
       double2 h = r0;
       if (F > 1) {
@@ -122,14 +128,23 @@ template <typename OutT>
 int launch_ls_feat_t(const Geom& g, const void* y, int y_c128, const void* pil, int pil_c128, int n_sets,
                      const float* noise, OutT* feats, cudaStream_t st) {
   dim3 grid(cdiv(g.rows_slab, 128), g.NU);
+  const bool b4 = g.B == 4;
+#define NRX_LSF(YT, PT)                                                                                         \
+  do {                                                                                                          \
+    if (b4)                                                                                                     \
+      k_ls_feat<OutT, YT, PT, 4><<<grid, 128, 0, st>>>(g, (const YT*)y, (const PT*)pil, n_sets, noise, feats);  \
+    else                                                                                                        \
+      k_ls_feat<OutT, YT, PT, 0><<<grid, 128, 0, st>>>(g, (const YT*)y, (const PT*)pil, n_sets, noise, feats);  \
+  } while (0)
   if (y_c128 && pil_c128)
-    k_ls_feat<OutT, double2, double2><<<grid, 128, 0, st>>>(g, (const double2*)y, (const double2*)pil, n_sets, noise, feats);
+    NRX_LSF(double2, double2);
   else if (y_c128)
-    k_ls_feat<OutT, double2, float2><<<grid, 128, 0, st>>>(g, (const double2*)y, (const float2*)pil, n_sets, noise, feats);
+    NRX_LSF(double2, float2);
   else if (pil_c128)
-    k_ls_feat<OutT, float2, double2><<<grid, 128, 0, st>>>(g, (const float2*)y, (const double2*)pil, n_sets, noise, feats);
+    NRX_LSF(float2, double2);
   else
-    k_ls_feat<OutT, float2, float2><<<grid, 128, 0, st>>>(g, (const float2*)y, (const float2*)pil, n_sets, noise, feats);
+    NRX_LSF(float2, float2);
+#undef NRX_LSF
   return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
 }
 
