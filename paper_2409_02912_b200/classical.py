@@ -155,3 +155,137 @@ def ls_lmmse_llrs(y, books, cfg, mcs_per_ue, n0, clip: float = LLR_CLIP, device=
 
 
 __all__ = ["GpuLsLmmse", "GpuKBest", "ls_lmmse_llrs", "kbest_llrs", "LLR_CLIP"]
+
+
+# ---------------------------------------------------------------------------
+# covariance-based LMMSE channel estimation + K-Best ("lmmse_kbest")
+# ---------------------------------------------------------------------------
+
+VAR_FLOOR = 1e-12   # classical.py:25
+
+
+@dataclass(frozen=True)
+class CovarianceModel:
+    """Sample frequency / time covariance of the effective per-stream channel
+    (channel.CovarianceModel, channel.py:223-236), as device tensors."""
+    freq: object     # (S, S) complex128
+    time: object     # (T, T) complex128
+    num_samples: int
+
+
+def covariance_variates(cfg, profiles, num_samples: int, seed: int = 0, num_sinusoids: int = 32) -> dict:
+    """The reference's draws for estimate_covariance (channel.py:239-268):
+    sample i of UE u uses default_rng((seed, 0xC0F, i, u)) for the
+    angles-then-phases of TdlChannelSource.sample.  Fed to the GPU slot
+    generator they reproduce the reference's channel draws."""
+    U, B, Nu = cfg.num_ues, cfg.bs_antennas, cfg.ue_antennas
+    L = max(p.delays_s.size for p in profiles[:U])
+    ang = np.zeros((num_samples, U, B, Nu, L, num_sinusoids))
+    ph = np.zeros_like(ang)
+    for i in range(num_samples):
+        for u in range(U):
+            r = np.random.default_rng((seed, 0xC0F, i, u))
+            nt = profiles[u].delays_s.size
+            ang[i, u, :, :, :nt] = r.uniform(0.0, 2.0 * np.pi, size=(B, Nu, nt, num_sinusoids))
+            ph[i, u, :, :, :nt] = r.uniform(0.0, 2.0 * np.pi, size=(B, Nu, nt, num_sinusoids))
+    return dict(angles=ang, phases=ph)
+
+
+def estimate_covariance(source, num_samples: int, seed: int = 0, reference_stream: bool = False,
+                        batch: int = 64) -> CovarianceModel:
+    """GPU estimate_covariance: channels from the GPU slot generator (device
+    Philox draws, or the reference's own draws with reference_stream=True),
+    then R_f = sum h h^H over (draw, UE, symbol, antenna) and R_t likewise,
+    Hermitian-symmetrised (channel.py:239-268)."""
+    import torch
+    if num_samples < 100:
+        raise ValueError(f"need at least 100 samples for covariance estimation, got {num_samples}")
+    cfg, dev = source.cfg, source.device
+    U, S, T, B = cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, cfg.bs_antennas
+    r_f = torch.zeros((S, S), dtype=torch.complex128, device=dev)
+    r_t = torch.zeros((T, T), dtype=torch.complex128, device=dev)
+    variates = covariance_variates(cfg, source.profiles, num_samples, seed, source.num_sinusoids) \
+        if reference_stream else None
+    for start in range(0, num_samples, batch):
+        nb = min(batch, num_samples - start)
+        v = None if variates is None else {k: a[start:start + nb] for k, a in variates.items()}
+        sb = source.generate(nb, [2] * U, 0.0, seed=(int(seed) << 8) ^ 0xC0F, first_slot=start, variates=v,
+                             with_h_eff=True, h_dtype=torch.complex128, y_dtype=torch.complex128)
+        h = sb.h_eff                                                  # (n, U, S, T, B)
+        hf = h.permute(2, 0, 1, 3, 4).reshape(S, -1)
+        ht = h.permute(3, 0, 1, 2, 4).reshape(T, -1)
+        r_f += hf @ hf.conj().T
+        r_t += ht @ ht.conj().T
+    r_f /= num_samples * U * T * B
+    r_t /= num_samples * U * S * B
+    return CovarianceModel(0.5 * (r_f + r_f.conj().T), 0.5 * (r_t + r_t.conj().T), num_samples)
+
+
+def lmmse_weights(cfg, cov: CovarianceModel, n0: float):
+    """Wiener filters of lmmse_estimate (classical.py:81-103): per UE the
+    frequency filter W_f (S, F_u) from its comb and the time filter W_t (T, K)."""
+    import torch
+    n0e = max(float(n0), VAR_FLOOR)
+    ps = torch.tensor(list(cfg.pilot_symbols), device=cov.time.device)
+    eye = lambda k: torch.eye(k, dtype=torch.complex128, device=cov.time.device)
+    r_t = cov.time
+    w_t = torch.linalg.solve(r_t[ps][:, ps] + n0e * eye(ps.numel()), r_t[:, ps].conj().T).conj().T
+    w_f = []
+    for u in range(cfg.num_ues):
+        sc = torch.arange(u % cfg.comb_size, cfg.num_subcarriers, cfg.comb_size, device=cov.freq.device)
+        r_f = cov.freq
+        w_f.append(torch.linalg.solve(r_f[sc][:, sc] + n0e * eye(sc.numel()), r_f[:, sc].conj().T).conj().T)
+    return w_f, w_t
+
+
+def lmmse_estimate(cfg, y, pilots, weights):
+    """Device lmmse_estimate: comb LS values, then W_f along frequency and
+    W_t along time.  y (N,S,T,B), pilots (P,U,F,K) comb values -> h (N,U,S,T,B)."""
+    import torch
+    w_f, w_t = weights
+    y = y.to(torch.complex128)
+    pil = pilots.to(torch.complex128)
+    n = y.shape[0]
+    ps = list(cfg.pilot_symbols)
+    out = torch.empty((n, cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, cfg.bs_antennas),
+                      dtype=torch.complex128, device=y.device)
+    for u in range(cfg.num_ues):
+        sc = torch.arange(u % cfg.comb_size, cfg.num_subcarriers, cfg.comb_size, device=y.device)
+        p = pil[:, u, :sc.numel()].expand(n, -1, -1)                         # (N, F, K)
+        raw = y[:, sc][:, :, ps] * (p.conj() / p.abs() ** 2)[..., None]      # (N, F, K, B)
+        est_f = torch.einsum("sf,nfkb->nskb", w_f[u], raw)
+        out[:, u] = torch.einsum("tk,nskb->nstb", w_t, est_f)
+    return out
+
+
+class GpuLmmseKBest:
+    """The reference's "lmmse_kbest" receiver (evaluation.py:136-138): LMMSE
+    channel estimate from sample covariances, then K-Best on the estimate."""
+
+    needs_n0 = True
+
+    def __init__(self, cov: CovarianceModel, bs_antennas: int = 4, m_max: int = 8, k: int = 16,
+                 clip: float = LLR_CLIP, device=None, reference_pairing: bool = True):
+        self.cov = cov
+        self.kb = GpuKBest(bs_antennas, m_max, k, clip, device, reference_pairing)
+        self.config = self.kb.config
+        self.device = self.kb.device
+        self._w = {}
+
+    def forward_device(self, cfg, y, pilots, noise_feat, mod_order, num_iterations, llr, chest=None,
+                       workspace=None, stream=None, n0=None):
+        if n0 is None:
+            raise ValueError("the LMMSE estimator needs the noise power n0")
+        n0s = n0.reshape(-1).cpu().numpy()
+        if not np.all(n0s == n0s[0]):
+            raise ValueError("one n0 per call (the Wiener filters depend on it)")
+        key = float(n0s[0])
+        if key not in self._w:
+            self._w = {key: lmmse_weights(cfg, self.cov, key)}
+        h = lmmse_estimate(cfg, y, pilots, self._w[key])
+        self.kb.forward_device(cfg, y, pilots, noise_feat, mod_order, num_iterations, llr, chest, workspace, stream,
+                               n0=n0, h_eff=h)
+
+
+__all__ += ["CovarianceModel", "covariance_variates", "estimate_covariance", "lmmse_weights", "lmmse_estimate",
+            "GpuLmmseKBest"]

@@ -118,3 +118,43 @@ def test_monte_carlo_loops_run_the_baseline():
     kb = evaluate_uncoded(GpuKBest(4, 4, 16), src, (t[14], t[14]), [0.0, 30.0], n_slots=16, batch=8,
                           receiver="perfect_kbest")
     assert kb[1].ber < unc[1].ber + 1e-3 and kb[0].ber < unc[0].ber   # true channel beats LS
+
+
+def _lm(name):
+    with np.load(f"{GOLDEN}/lm_{name}.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.mark.parametrize("name", ["sg_desk", "sg_mixed", "sg_b8_t7"])
+def test_covariance_reference_stream(name):
+    from paper_2409_02912_b200.classical import estimate_covariance
+    from paper_2409_02912_b200.slotgen import GpuSlotSource
+    c = load_case(name)
+    g = _lm(name)
+    cov = estimate_covariance(GpuSlotSource(c.cfg, c.profiles), 120, seed=4, reference_stream=True)
+    np.testing.assert_allclose(cov.freq.cpu().numpy(), g["r_f"], rtol=0, atol=1e-12 * np.abs(g["r_f"]).max())
+    np.testing.assert_allclose(cov.time.cpu().numpy(), g["r_t"], rtol=0, atol=1e-12 * np.abs(g["r_t"]).max())
+
+
+@pytest.mark.parametrize("name", ["sg_desk", "sg_mixed", "sg_b8_t7"])
+def test_lmmse_kbest_matches_reference(name):
+    torch = __import__("torch")
+    from paper_2409_02912_b200.classical import CovarianceModel, GpuLmmseKBest, lmmse_estimate, lmmse_weights
+    c = load_case(name)
+    g = _lm(name)
+    cov = CovarianceModel(torch.from_numpy(g["r_f"]).cuda(), torch.from_numpy(g["r_t"]).cuda(), 120)
+    y = torch.from_numpy(c.a["y"]).cuda()
+    pil = torch.from_numpy(c.a["pilots"]).cuda()
+    h = lmmse_estimate(c.cfg, y, pil, lmmse_weights(c.cfg, cov, c.n0)).cpu().numpy()
+    np.testing.assert_allclose(h, g["h_est"], rtol=0, atol=1e-10 * np.abs(g["h_est"]).max())
+    U = c.cfg.num_ues
+    rx = GpuLmmseKBest(cov, c.cfg.bs_antennas, max(c.orders), 16)
+    mods = torch.tensor(list(c.orders) * c.n, dtype=torch.int32, device="cuda")
+    llr = torch.empty((c.n, U, c.cfg.num_subcarriers, c.cfg.num_symbols, max(c.orders)), dtype=torch.float32,
+                      device="cuda")
+    rx.forward_device(c.cfg, y, pil, None, mods, 1, llr, n0=torch.full((c.n,), c.n0, dtype=torch.float64,
+                                                                      device="cuda"))
+    got = llr.cpu().numpy()
+    for u, m in enumerate(c.orders):
+        close = np.isclose(got[:, u, ..., :m], g[f"llr_{u}"], rtol=1e-5, atol=1e-4)
+        assert close.mean() > 0.999, (name, close.mean())
