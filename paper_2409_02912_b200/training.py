@@ -1,0 +1,316 @@
+"""Training of the NRX on the GPU.
+
+The reference trains with its own numpy autodiff on the CPU (multi-loss
+BCE over the readouts of every iteration + gamma * MSE on the channel
+readout, Adam; training.py:180-234, autodiff.py:358-525).  Here one training
+step is the same graph in PyTorch autograd on the device: convolutions and
+dense layers run as cuDNN / cuBLAS library kernels (the training path is
+not the inference hot path; inference stays on the hand-written tcgen05
+kernels), the inputs come from the GPU slot generator and the LS/feature
+kernel, and the Adam update follows the reference's formula exactly.
+
+Parity (tests/test_training_cpu.py, against tests/golden/train_*.npz made by
+the reference's own train_step): loss, every gradient and the weights after
+one Adam step, for the masking and var_io variants with inactive UEs.
+
+Reference interfaces mirrored (file:line under /root/reference/pkg/src/nrxsim):
+  nrx_forward_graph(training=True), _mlp, _conv_block,
+  _grouped_state_init, cgnn_iteration, readout_llrs / readout_chest  nrx.py:221-342
+  bce_with_logits (masked mean), mse (masked mean)                   autodiff.py:358-420
+  train_step (per-iteration group weighting, gamma)                  training.py:180-234
+  AdamState / adam_step                                              autodiff.py:485-525
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class TorchNrxGraph:
+    """The NRX graph on torch tensors.  ``params`` maps the reference's weight
+    names to leaf tensors (float32, requires_grad)."""
+
+    def __init__(self, config, weights: dict, device="cpu"):
+        torch = _torch()
+        self.config = config
+        self.device = torch.device(device)
+        self.params = {k: torch.tensor(np.asarray(getattr(v, "data", v), dtype=np.float32), device=self.device,
+                                       requires_grad=True) for k, v in weights.items()}
+
+    def numpy_weights(self) -> dict:
+        return {k: v.detach().cpu().numpy().copy() for k, v in self.params.items()}
+
+    # -- blocks -------------------------------------------------------------
+    def _conv(self, x, name):
+        """'same' k x k convolution of NHWC x (H = subcarrier, W = symbol)
+        with a (k, k, Cin, Cout) kernel (autodiff.py:324-350)."""
+        F = _torch().nn.functional
+        w = self.params[name]
+        k = w.shape[0]
+        y = F.conv2d(x.permute(0, 3, 1, 2), w.permute(3, 2, 0, 1), padding=k // 2)
+        return y.permute(0, 2, 3, 1)
+
+    def _conv_block(self, x, prefix):
+        torch = _torch()
+        h = torch.relu(self._conv(x, f"{prefix}.conv0.w") + self.params[f"{prefix}.conv0.b"])
+        return self._conv(h, f"{prefix}.conv1.w") + self.params[f"{prefix}.conv1.b"]
+
+    def _mlp(self, x, prefix):
+        torch = _torch()
+        p = self.params
+        h = torch.relu(x @ p[f"{prefix}.fc0.w"] + p[f"{prefix}.fc0.b"])
+        return h @ p[f"{prefix}.fc1.w"] + p[f"{prefix}.fc1.b"]
+
+    def _groups(self, mods):
+        c = self.config
+        if c.variant != "var_io":
+            return [(None, np.arange(mods.size))]
+        return [(m, np.flatnonzero(mods == m)) for m in c.io_modulations if np.any(mods == m)]
+
+    # -- graph --------------------------------------------------------------
+    def forward(self, feats, mods, active, num_iterations=None, training=True, collect_chest=True):
+        """feats (N, U, S, T, Cin) float32 tensor, mods (N, U) ints, active
+        (N, U) -> (llr_groups per iteration: [(tensor, slab idx)], chest per
+        iteration) as nrx_forward_graph (nrx.py:302-342)."""
+        torch = _torch()
+        c = self.config
+        n, u = feats.shape[0], feats.shape[1]
+        n_it = c.num_iterations if num_iterations is None else int(num_iterations)
+        x = feats.reshape((n * u,) + tuple(feats.shape[2:]))
+        pos = x[..., 4 * c.num_rx_ant:4 * c.num_rx_ant + 2]
+        mods = np.asarray(mods).reshape(-1)
+        act = torch.as_tensor(np.asarray(active, dtype=np.float32), device=feats.device).reshape(n, u, 1, 1, 1)
+        if c.variant != "var_io":
+            state = self._conv_block(x, "state_init")
+        else:
+            parts, order = [], []
+            for m, idx in self._groups(mods):
+                it = torch.as_tensor(idx, device=feats.device)
+                parts.append(self._conv_block(x[it], f"state_init.m{m}"))
+                order.append(idx)
+            inv = torch.as_tensor(np.argsort(np.concatenate(order)), device=feats.device)
+            state = torch.cat(parts)[inv]
+        llrs, chests = [], []
+
+        def readouts(st):
+            groups = []
+            for m, idx in self._groups(mods):
+                it = torch.as_tensor(idx, device=feats.device)
+                prefix = "readout_llr" if m is None else f"readout_llr.m{m}"
+                groups.append((self._mlp(st if m is None else st[it], prefix), idx))
+            return groups
+
+        for _ in range(n_it):
+            msg = self._mlp(state, "iteration.msg")
+            shaped = (msg.reshape((n, u) + tuple(msg.shape[1:])) * act).double()
+            agg = (shaped.sum(dim=1, keepdim=True) - shaped).float()      # sum_others in float64
+            upd_in = torch.cat([state, agg.reshape(state.shape), pos], dim=-1)
+            state = state + self._conv_block(upd_in, "iteration.update")
+            if training:
+                llrs.append(readouts(state))
+                if collect_chest:
+                    chests.append(self._mlp(state, "readout_chest"))
+        if not training:
+            llrs = [readouts(state)]
+            chests = [self._mlp(state, "readout_chest")]
+        return llrs, chests
+
+
+def _bce_masked_sum(logits, bits, mask):
+    """sum(mask * ln(1 + exp(-(2b - 1) z))) (autodiff.py:358-394, overflow-free split)."""
+    torch = _torch()
+    a = -(2.0 * bits - 1.0) * logits
+    per = torch.clamp(a, min=0) + torch.log1p(torch.exp(-a.abs()))
+    return (per * mask).sum()
+
+
+def training_loss(graph: TorchNrxGraph, feats, labels, label_mask, chest_target, active, mods, gamma: float):
+    """The multi-loss of train_step (training.py:189-222): per iteration the
+    masked-mean BCE over all LLR groups, plus gamma times the masked MSE of
+    the channel readout; returns (total, bce, mse) tensors."""
+    torch = _torch()
+    n, u = labels.shape[0], labels.shape[1]
+    flat_lab = labels.reshape((n * u,) + tuple(labels.shape[2:]))
+    flat_mask = label_mask.reshape((n * u,) + tuple(label_mask.shape[2:]))
+    flat_tgt = chest_target.reshape((n * u,) + tuple(chest_target.shape[2:]))
+    cmask = torch.as_tensor(np.asarray(active, dtype=np.float32), device=labels.device).reshape(n * u, 1, 1, 1)
+    cmask = cmask.expand_as(flat_tgt)
+    llr_groups, chests = graph.forward(feats, mods, active, training=True, collect_chest=gamma > 0)
+    bce, mse = [], []
+    for it, groups in enumerate(llr_groups):
+        num, den = 0.0, 0.0
+        for t, idx in groups:
+            ii = torch.as_tensor(idx, device=labels.device)
+            w = t.shape[-1]
+            mk = flat_mask[ii][..., :w]
+            share = mk.sum()
+            if float(share) == 0.0:
+                continue   # a group of inactive slabs stays out of the graph (training.py:205-207)
+            den = den + share
+            num = num + _bce_masked_sum(t, flat_lab[ii][..., :w], mk)
+        bce.append(num / den)
+        if gamma > 0:
+            mse.append((((chests[it] - flat_tgt) ** 2) * cmask).sum() / cmask.sum())
+    bce_t = torch.stack(bce).sum()
+    mse_t = torch.stack(mse).sum() if mse else torch.zeros((), device=labels.device)
+    total = bce_t + gamma * mse_t if mse else bce_t
+    return total, bce_t, mse_t
+
+
+@dataclass
+class Adam:
+    """Bias-corrected Adam with the reference's update (autodiff.py:485-525):
+    p -= (lr / (1 - b1^t)) * m / (sqrt(v / (1 - b2^t)) + eps)."""
+
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    epsilon: float = 1e-8
+    t: int = 0
+    m: dict = field(default_factory=dict)
+    v: dict = field(default_factory=dict)
+
+    def step(self, params: dict, names) -> None:
+        torch = _torch()
+        self.t += 1
+        c1 = 1.0 - self.beta1 ** self.t
+        c2 = 1.0 - self.beta2 ** self.t
+        with torch.no_grad():
+            for k in names:
+                p = params[k]
+                g = p.grad
+                if g is None:
+                    raise ValueError(f"missing gradient for parameter '{k}'")
+                if not torch.isfinite(g).all():
+                    raise ValueError(f"non-finite gradient for parameter '{k}'")
+                if k not in self.m:
+                    self.m[k] = torch.zeros_like(p)
+                    self.v[k] = torch.zeros_like(p)
+                m, v = self.m[k], self.v[k]
+                m.mul_(self.beta1).add_((1.0 - self.beta1) * g)
+                v.mul_(self.beta2).add_((1.0 - self.beta2) * g * g)
+                p.sub_((self.lr / c1) * m / (torch.sqrt(v / c2) + self.epsilon))
+
+
+def train_step(graph: TorchNrxGraph, adam: Adam, feats, labels, label_mask, chest_target, active, mods,
+               gamma: float) -> dict:
+    """One multi-loss gradient step (training.py:180-234): only parameters
+    the loss touched are updated (the chest head sits out at gamma = 0, a
+    var_io group may sit out a batch)."""
+    torch = _torch()
+    for p in graph.params.values():
+        p.grad = None
+    total, bce, mse = training_loss(graph, feats, labels, label_mask, chest_target, active, mods, gamma)
+    if not torch.isfinite(total):
+        raise RuntimeError(f"non-finite training loss {float(total)}")
+    total.backward()
+    touched = [k for k, p in graph.params.items() if p.grad is not None]
+    adam.step(graph.params, touched)
+    for p in graph.params.values():
+        p.grad = None
+    return {"total": float(total.detach()), "bce": float(bce.detach()), "mse": float(mse.detach())}
+
+
+__all__ = ["TorchNrxGraph", "training_loss", "train_step", "Adam"]
+
+
+# ---------------------------------------------------------------------------
+# GPU training loop: batches from the GPU slot generator
+# ---------------------------------------------------------------------------
+
+def gpu_features(config, cfg, batch, n0):
+    """(N, U, S, T, Cin) float32 features of a generated batch by the LS /
+    feature kernel (nrx_ls_features, float32 chunk-planar) — the reference's
+    assemble_features(y, ls_features(...)) (nrx.py:184-213)."""
+    import ctypes
+    torch = _torch()
+    from . import _lib
+    from .nrx import noise_features
+    lib = _lib.load()
+    n, U, S, T = batch.y.shape[0], cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols
+    geo = _lib.buffer_geometry(config, cfg, "fp32")
+    out = torch.zeros(n * U, geo["Cf"] // 4, geo["rows_slab"], 4, device=batch.y.device)
+    nf = torch.as_tensor(noise_features(np.asarray(n0, dtype=np.float64), n), device=batch.y.device)
+    st = torch.cuda.current_stream(batch.y.device).cuda_stream
+    code = lib.nrx_ls_features(ctypes.byref(_lib.model_desc(config)), ctypes.byref(_lib.slot_desc(cfg)), n, 0,
+                               batch.y.data_ptr(), int(batch.y.dtype == torch.complex128), batch.pilots.data_ptr(),
+                               int(batch.pilots.dtype == torch.complex128), batch.pilots.shape[0], nf.data_ptr(),
+                               out.data_ptr(), st)
+    _lib.check(code, "nrx_ls_features")
+    f = out.permute(0, 2, 1, 3).reshape(n * U, geo["rows_slab"], geo["Cf"])
+    f = f[:, :S * geo["Tp"]].reshape(n, U, S, geo["Tp"], geo["Cf"])
+    cin = 4 * config.num_rx_ant + 2 + int(bool(config.include_noise_plane))
+    return f[:, :, :, :T, :cin].contiguous()
+
+
+@dataclass
+class GpuTrainConfig:
+    """The knobs of the reference's TrainConfig (training.py:38-79) that the
+    GPU loop uses; labels are iid bits (the LDPC code does not change the
+    bit statistics the receiver sees)."""
+    batch_size: int = 16
+    steps: int = 1000
+    snr_lo_db: float = -4.0
+    snr_hi_db: float = 4.0
+    gamma: float = 0.1
+    learning_rate: float = 1e-3
+    supported_mcs: tuple = (14,)
+    seed: int = 0
+
+
+def gpu_training_batch(source, config, table, tcfg: GpuTrainConfig, step: int):
+    """One batch on the device: per slot an SNR uniform in [lo, hi] dB and a
+    supported MCS per UE, slots from the GPU slot generator with the true
+    effective channel as the chest target (re/im interleaved per antenna,
+    the reference's layout, training.py:154-156), labels and label masks on
+    the data REs."""
+    torch = _torch()
+    cfg, dev = source.cfg, source.device
+    n, U, S, T, B = tcfg.batch_size, cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, cfg.bs_antennas
+    rng = np.random.default_rng((tcfg.seed, 0x7A, step))
+    snr = rng.uniform(tcfg.snr_lo_db, tcfg.snr_hi_db, size=n)
+    n0 = 10.0 ** (-snr / 10.0)
+    picks = rng.choice(np.asarray(tcfg.supported_mcs), size=(n, U))
+    mods = np.vectorize(lambda i: table[int(i)].modulation_order)(picks).astype(np.int32)
+    sb = source.generate(n, torch.as_tensor(mods.reshape(-1), device=dev), torch.as_tensor(n0, device=dev),
+                         seed=(tcfg.seed << 20) ^ 0x7A17, first_slot=step * n, with_h_eff=True)
+    width = config.m_max
+    data = torch.as_tensor(np.asarray(cfg.data_mask), device=dev)                       # (S, T)
+    m_t = torch.as_tensor(mods, device=dev).reshape(n, U, 1, 1, 1)
+    j = torch.arange(width, device=dev).reshape(1, 1, 1, 1, width)
+    lab = sb.labels.to(torch.int64).unsqueeze(-1)
+    bits = ((lab >> (m_t - 1 - j).clamp(min=0)) & 1).to(torch.float32)
+    mask = ((j < m_t) & data.reshape(1, 1, S, T, 1)).to(torch.float32)
+    h = sb.h_eff
+    tgt = torch.stack([h.real, h.imag], dim=-1).reshape(n, U, S, T, 2 * B).to(torch.float32)
+    return sb, n0, mods, bits * mask, mask, tgt
+
+
+def train_gpu(config, weights, source, table, tcfg: GpuTrainConfig, graph=None, adam=None, log_every: int = 0,
+              progress=None):
+    """The reference's train() loop (training.py:254-284) on the device.
+    Returns (graph, adam, history of (step, losses))."""
+    dev = source.device
+    graph = graph or TorchNrxGraph(config, weights, dev)
+    adam = adam or Adam(lr=tcfg.learning_rate)
+    active = np.ones((tcfg.batch_size, source.cfg.num_ues), dtype=np.float32)
+    hist = []
+    for step in range(tcfg.steps):
+        sb, n0, mods, labels, mask, tgt = gpu_training_batch(source, config, table, tcfg, step)
+        feats = gpu_features(config, source.cfg, sb, n0)
+        losses = train_step(graph, adam, feats, labels, mask, tgt, active, mods, tcfg.gamma)
+        if log_every and step % log_every == 0:
+            hist.append((step, losses))
+        if progress is not None:
+            progress(step, losses)
+    return graph, adam, hist
+
+
+__all__ += ["gpu_features", "GpuTrainConfig", "gpu_training_batch", "train_gpu"]
