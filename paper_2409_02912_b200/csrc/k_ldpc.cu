@@ -46,6 +46,7 @@ struct nrx_ldpc_code {
   int32_t* tx_pos;     // (ntx)
   int32_t* info_slot;  // (n): payload index of an info position, -1 shortened, -2 parity
   int32_t* chain_cols; // (m) or null
+  int4* edges;         // (n): the column's checks as (row << 8 | slot), -1 padded
 };
 
 namespace nrx_ldpc {
@@ -54,7 +55,8 @@ constexpr float kShortenedLlr = 60.0f;   // ldpc.py:25
 constexpr int kThreads = 256;
 
 constexpr int kLanes = 32;           // codewords interleaved per group, one per lane
-constexpr int kWarps = 8;            // warps per block = elements per block
+constexpr int kWarps = 8;            // warps per block
+constexpr int kVarsPerWarp = 4;      // variables per warp in the variable update
 
 // Decoder state, codeword-interleaved: element e of group g for lane l lives
 // at [(g * count + e) * 32 + l], so a warp working on one variable / check
@@ -63,7 +65,6 @@ struct DecWs {
   float* chan;      // [G][n][32]
   float* total;     // [G][n][32]
   float* c2v;       // [G][m][dmax][32]
-  uint8_t* hard;    // [G][n][32]
   uint32_t* done;   // [G] lane mask of finished codewords
   uint32_t* unsat;  // [G][check blocks] lane mask with an unsatisfied check
 };
@@ -84,7 +85,6 @@ DecWs dec_layout(const nrx_ldpc_code& c, int n_cw, uint8_t* base, size_t* total_
   const size_t o_chan = take(sizeof(float) * c.n * kLanes * G);
   const size_t o_total = take(sizeof(float) * c.n * kLanes * G);
   const size_t o_c2v = take(sizeof(float) * (size_t)c.m * c.dmax * kLanes * G);
-  const size_t o_hard = take((size_t)c.n * kLanes * G);
   const size_t o_done = take(sizeof(uint32_t) * G);
   const size_t o_unsat = take(sizeof(uint32_t) * check_blocks(c) * G);
   if (total_bytes) *total_bytes = off;
@@ -92,7 +92,6 @@ DecWs dec_layout(const nrx_ldpc_code& c, int n_cw, uint8_t* base, size_t* total_
     w.chan = reinterpret_cast<float*>(base + o_chan);
     w.total = reinterpret_cast<float*>(base + o_total);
     w.c2v = reinterpret_cast<float*>(base + o_c2v);
-    w.hard = base + o_hard;
     w.done = reinterpret_cast<uint32_t*>(base + o_done);
     w.unsat = reinterpret_cast<uint32_t*>(base + o_unsat);
   }
@@ -141,30 +140,46 @@ __global__ void k_ldpc_init(nrx_ldpc_code c, const float* llr, int n_cw, DecWs w
   }
 }
 
-// Variable update, warp per variable: total = chan + ((c2v_0 + c2v_1) + c2v_2).
-__global__ void __launch_bounds__(kWarps * 32) k_ldpc_var(nrx_ldpc_code c, DecWs w, int only_open) {
+// Variable update, warp per kVarsPerWarp variables (their edge records and
+// message gathers all issued before use): total = chan + ((c2v_0 + c2v_1) + c2v_2).
+// The hard bits are the signs of the totals; a converged lane's totals stay
+// frozen, so they are its decision.
+__global__ void __launch_bounds__(kWarps * 32) k_ldpc_var(nrx_ldpc_code c, DecWs w) {
   const int g = blockIdx.y;
   const uint32_t done = w.done[g];
   if (done == 0xffffffffu) return;
   const int lane = threadIdx.x & 31;
-  const int j = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  if (j >= c.n || ((done >> lane) & 1u)) return;
-  const float* c2v = w.c2v + (size_t)g * c.m * c.dmax * kLanes;
-  float s = 0.f;
-  for (int t = 0; t < c.cdeg; ++t) {
-    const int r = c.col_rows[(size_t)j * c.cdeg + t];
-    if (r < 0) break;
-    const float v = c2v[((size_t)r * c.dmax + c.col_slots[(size_t)j * c.cdeg + t]) * kLanes + lane];
-    s = t == 0 ? v : __fadd_rn(s, v);
+  if ((done >> lane) & 1u) return;
+  const int j0 = (blockIdx.x * kWarps + (threadIdx.x >> 5)) * kVarsPerWarp;
+  const float* c2v = w.c2v + (size_t)g * c.m * c.dmax * kLanes + lane;
+  int4 ed[kVarsPerWarp];
+#pragma unroll
+  for (int q = 0; q < kVarsPerWarp; ++q)
+    ed[q] = j0 + q < c.n ? __ldg(c.edges + j0 + q) : make_int4(-1, -1, -1, -1);
+  float v[kVarsPerWarp][3], ch[kVarsPerWarp];
+#pragma unroll
+  for (int q = 0; q < kVarsPerWarp; ++q) {
+    const int e3[3] = {ed[q].x, ed[q].y, ed[q].z};
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+      v[q][t] = e3[t] >= 0 ? c2v[((size_t)(e3[t] >> 8) * c.dmax + (e3[t] & 255)) * kLanes] : 0.f;
+    ch[q] = j0 + q < c.n ? w.chan[((size_t)g * c.n + j0 + q) * kLanes + lane] : 0.f;
   }
-  const size_t e = ((size_t)g * c.n + j) * kLanes + lane;
-  const float tot = __fadd_rn(w.chan[e], s);
-  if (!only_open) w.total[e] = tot;
-  w.hard[e] = tot < 0.f ? 1 : 0;
+#pragma unroll
+  for (int q = 0; q < kVarsPerWarp; ++q) {
+    if (j0 + q >= c.n) break;
+    float s = v[q][0];
+    if (ed[q].y >= 0) s = __fadd_rn(s, v[q][1]);
+    if (ed[q].z >= 0) s = __fadd_rn(s, v[q][2]);
+    if (ed[q].x < 0) s = 0.f;
+    w.total[((size_t)g * c.n + j0 + q) * kLanes + lane] = __fadd_rn(ch[q], s);
+  }
 }
 
-// Check update, warp per check (two passes over the row), plus the lanes whose
-// hard bits violate this check.
+// Check update, warp per check: v2c of every slot kept in registers between
+// the min-sum pass and the message write; plus the lanes whose hard bits
+// violate this check.  DMAX > 0: row width fixed at compile time.
+template <int DMAX>
 __global__ void __launch_bounds__(kWarps * 32) k_ldpc_check(nrx_ldpc_code c, DecWs w) {
   __shared__ uint32_t block_unsat;
   const int g = blockIdx.y;
@@ -174,23 +189,33 @@ __global__ void __launch_bounds__(kWarps * 32) k_ldpc_check(nrx_ldpc_code c, Dec
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int dmax = DMAX > 0 ? DMAX : c.dmax;
   int syn = 0;
   if (r < c.m && !((done >> lane) & 1u)) {
-    const int32_t* cols = c.row_cols + (size_t)r * c.dmax;
-    float* msg = w.c2v + (((size_t)g * c.m + r) * c.dmax) * kLanes + lane;
+    const int32_t* cols = c.row_cols + (size_t)r * dmax;
+    float* msg = w.c2v + (((size_t)g * c.m + r) * dmax) * kLanes + lane;
     const float* tot = w.total + (size_t)g * c.n * kLanes + lane;
+    constexpr int RD = DMAX > 0 ? DMAX : 1;
+    float xs[RD];
+    int cl[RD];
     float min1 = INFINITY, min2 = INFINITY;
     int amin = 0, neg = 0;
     bool first = true;
-    for (int s = 0; s < c.dmax; ++s) {
-      const int col = cols[s];
-      float mag = INFINITY;
+#pragma unroll
+    for (int s = 0; s < (DMAX > 0 ? DMAX : NRX_LDPC_MAX_ROW_DEG); ++s) {
+      if (s >= dmax) break;
+      const int col = __ldg(cols + s);
+      float mag = INFINITY, x = 0.f;
       if (col >= 0) {
         const float v = tot[(size_t)col * kLanes];
         syn ^= v < 0.f ? 1 : 0;
-        const float x = __fsub_rn(v, msg[s * kLanes]);
+        x = __fsub_rn(v, msg[s * kLanes]);
         mag = fabsf(x);
         neg ^= x < 0.f ? 1 : 0;
+      }
+      if (DMAX > 0) {
+        xs[s] = x;
+        cl[s] = col;
       }
       // np.argmin: first index of the smallest magnitude (invalid slots are +inf)
       if (first || mag < min1) {
@@ -203,13 +228,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_ldpc_check(nrx_ldpc_code c, Dec
       }
     }
     const float rs = neg ? -1.f : 1.f;
-    for (int s = 0; s < c.dmax; ++s) {
-      const int col = cols[s];
+#pragma unroll
+    for (int s = 0; s < (DMAX > 0 ? DMAX : NRX_LDPC_MAX_ROW_DEG); ++s) {
+      if (s >= dmax) break;
+      const int col = DMAX > 0 ? cl[s] : __ldg(cols + s);
       if (col < 0) {
         msg[s * kLanes] = 0.f;
         continue;
       }
-      const float x = __fsub_rn(tot[(size_t)col * kLanes], msg[s * kLanes]);
+      const float x = DMAX > 0 ? xs[s] : __fsub_rn(tot[(size_t)col * kLanes], msg[s * kLanes]);
       const float sg = x < 0.f ? -1.f : 1.f;
       msg[s * kLanes] = __fmul_rn(rs * sg, s == amin ? min2 : min1);
     }
@@ -241,7 +268,7 @@ __global__ void k_ldpc_extract(nrx_ldpc_code c, DecWs w, uint8_t* info, uint8_t*
   const int lane = threadIdx.x & 31, cw = g * kLanes + lane;
   if (cw >= n_cw) return;
   for (int i = blockIdx.x * kWarps + (threadIdx.x >> 5); i < c.k_eff; i += gridDim.x * kWarps)
-    info[(size_t)cw * c.k_eff + i] = w.hard[((size_t)g * c.n + c.keep_pos[i]) * kLanes + lane];
+    info[(size_t)cw * c.k_eff + i] = w.total[((size_t)g * c.n + c.keep_pos[i]) * kLanes + lane] < 0.f ? 1 : 0;
   if (blockIdx.x == 0 && threadIdx.x < 32) success[cw] = static_cast<uint8_t>((w.done[g] >> lane) & 1u);
 }
 
@@ -399,7 +426,8 @@ extern "C" int nrx_ldpc_create(const nrx_ldpc_desc* d, nrx_ldpc_code** out) {
   if (!d || !out) return NRX_ERR_INVALID;
   *out = nullptr;
   if (d->n < 2 || d->m < 1 || d->k < 1 || d->k >= d->n || d->dmax < 1 || d->cdeg < 1) return NRX_ERR_INVALID;
-  if (d->cdeg > NRX_LDPC_MAX_COL_DEG || d->dmax > NRX_LDPC_MAX_ROW_DEG) return NRX_ERR_UNSUPPORTED;
+  if (d->cdeg > NRX_LDPC_MAX_COL_DEG || d->dmax > NRX_LDPC_MAX_ROW_DEG || d->m >= (1 << 23))
+    return NRX_ERR_UNSUPPORTED;   // edge records pack (row << 8 | slot) into an int32
   if (!d->row_cols || !d->col_rows || !d->col_slots || !d->info_positions) return NRX_ERR_INVALID;
   if (d->n_punctured < 0 || d->n_shortened < 0 || (d->n_punctured && !d->punctured) ||
       (d->n_shortened && !d->shortened))
@@ -469,6 +497,19 @@ extern "C" int nrx_ldpc_create(const nrx_ldpc_desc* d, nrx_ldpc_code** out) {
   rc = rc ? rc : upload(&c->tx_pos, tx_pos);
   rc = rc ? rc : upload(&c->info_slot, info_slot);
   if (!rc && d->chain_cols) rc = upload(&c->chain_cols, std::vector<int32_t>(d->chain_cols, d->chain_cols + m));
+  if (!rc) {
+    std::vector<int4> edges(n, make_int4(-1, -1, -1, -1));
+    for (int j = 0; j < n; ++j) {
+      int e[3] = {-1, -1, -1};
+      for (int t = 0; t < d->cdeg && t < 3; ++t) {
+        const int r = d->col_rows[(size_t)j * d->cdeg + t];
+        if (r < 0) break;
+        e[t] = (r << 8) | d->col_slots[(size_t)j * d->cdeg + t];
+      }
+      edges[j] = make_int4(e[0], e[1], e[2], -1);
+    }
+    rc = upload(&c->edges, edges);
+  }
   if (rc) {
     nrx_ldpc_destroy(c);
     return rc == NRX_ERR_CUDA && cudaGetLastError() == cudaErrorNoDevice ? NRX_ERR_NO_DEVICE : rc;
@@ -483,6 +524,7 @@ extern "C" void nrx_ldpc_destroy(nrx_ldpc_code* c) {
                      c->info_slot, c->chain_cols};
   for (int32_t* p : ptrs)
     if (p) cudaFree(p);
+  if (c->edges) cudaFree(c->edges);
   delete c;
 }
 
@@ -514,15 +556,17 @@ extern "C" int nrx_ldpc_decode(const nrx_ldpc_code* c, int n_cw, const float* ll
   if (!ws || ws_bytes < need) return NRX_ERR_WORKSPACE;
   const DecWs w = dec_layout(*c, n_cw, static_cast<uint8_t*>(ws), nullptr);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int vb = (c->n + kWarps - 1) / kWarps, cb = check_blocks(*c);
+  const int vb = (c->n + kWarps * kVarsPerWarp - 1) / (kWarps * kVarsPerWarp), cb = check_blocks(*c);
+  auto check_fn = c->dmax == 5 ? k_ldpc_check<5> : c->dmax == 6 ? k_ldpc_check<6> : c->dmax == 7 ? k_ldpc_check<7>
+                : c->dmax == 8 ? k_ldpc_check<8> : k_ldpc_check<0>;
   k_ldpc_init<<<dim3(512, G), 256, 0, st>>>(*c, llr, n_cw, w);
   for (int it = 0; it < iterations; ++it) {
-    k_ldpc_var<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w, 0);
-    k_ldpc_check<<<dim3(cb, G), kWarps * 32, 0, st>>>(*c, w);
+    k_ldpc_var<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w);
+    check_fn<<<dim3(cb, G), kWarps * 32, 0, st>>>(*c, w);
     k_ldpc_flag<<<G, 256, 0, st>>>(w, cb);
   }
-  // codewords that never satisfied every check: hard bits of the final messages
-  k_ldpc_var<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w, 1);
+  // codewords that never satisfied every check: totals of the final messages
+  k_ldpc_var<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w);
   k_ldpc_extract<<<dim3(256, G), kWarps * 32, 0, st>>>(*c, w, info_out, success, n_cw);
   return launch_status();
 }
