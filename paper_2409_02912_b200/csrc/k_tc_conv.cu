@@ -34,10 +34,6 @@ namespace nrx {
 namespace tc {
 
 enum ConvTail { TAIL_NONE = 0, TAIL_MSG = 1, TAIL_READOUT = 2 };
-#ifndef NRX_TAIL_BATCH
-#define NRX_TAIL_BATCH 1
-#endif
-constexpr int kTailBatch = NRX_TAIL_BATCH;  // TMEM chunk loads in flight per tail-stage wait
 
 struct ConvTcParams {
   Geom g;
@@ -494,17 +490,9 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       tc_fence_after();
       float v[NC];
       const uint32_t taddr = tmem_base + lane_off + acc * NP + cbase;
-#ifdef NRX_CONV_LD_EACH
-#pragma unroll
-      for (int c = 0; c < NC / 8; ++c) {
-        tmem_ld8(taddr + 8 * c, v + 8 * c);
-        tmem_wait_ld();
-      }
-#else
 #pragma unroll
       for (int c = 0; c < NC / 8; ++c) tmem_ld8(taddr + 8 * c, v + 8 * c);
       tmem_wait_ld();
-#endif
       tc_fence_before();
       mbar_arrive(B_tempty + 8u * (acc));
 

@@ -51,9 +51,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-#ifndef NRX_MBAR_SUSPEND_NS
-#define NRX_MBAR_SUSPEND_NS 0
-#endif
 // uint32 shared-address overloads (no generic->shared conversion per call)
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -72,28 +69,10 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// try_wait with a suspend-time hint: a waiting warp sleeps in the barrier
-// unit instead of spinning (issue slots stay with the working warps).
-__device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(addr), "r"(parity), "r"(NRX_MBAR_SUSPEND_NS)
-      : "memory");
-  return ok != 0;
-}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
-#if NRX_MBAR_SUSPEND_NS > 0
-  while (!mbar_try_wait_sleep(a, parity)) {
-  }
-#else
   while (!mbar_try_wait(a, parity)) {
   }
-#endif
 }
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
   while (!mbar_try_wait(a, parity)) {
