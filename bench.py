@@ -294,6 +294,27 @@ def run_ours(args):
     value = slots_total / elapsed
     ms_per_step = elapsed / args.steps * 1e3
 
+    # N > 1: the same step followed by the gather of its LLRs to rank 0 over
+    # NCCL (SURVEY.md §8e "with gather"); compute-only stays the headline value
+    with_gather = None
+    if world > 1:
+        from paper_2409_02912_b200.shard import StepGather
+        gat = StepGather(llr)
+        n_g = max(5, args.steps // 4)
+        dist.barrier()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for i in range(n_g):
+            step(i)
+            gat(llr)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        tg = max_over_ranks(g0.elapsed_time(g1) / 1e3, dev)
+        with_gather = {"value": round(B * n_g * world / tg, 2), "unit": "slots/s", "steps": n_g,
+                       "gather_bytes_per_step_into_rank0": gat.bytes_per_step(llr),
+                       "note": "each step's (B,U,S,T,4) float32 LLRs of every rank gathered to rank 0 (NCCL)"}
+
     # roofline of the dominant kernel (conv_update0), device time of each launch
     peaks, peak_src = load_peaks()
     flops_launch = conv_update0_flops_per_slab_re() * B * U * S * T
@@ -364,6 +385,7 @@ def run_ours(args):
         "latency_us": lat,
         "latency_other_configs_us": lat_other,
         "e2e": e2e,
+        "with_gather": with_gather,
         "monte_carlo": mc,
         "next_rows": nxt,
         "roofline": {"kernel": "conv_update0 (iteration.update.conv0, 3x3 114->56, implicit GEMM)",

@@ -48,3 +48,38 @@ def gather_slot_results(local: np.ndarray, n_slots: int, device=None, dst: int =
     if rank != dst:
         return None
     return np.concatenate([g[:sizes[r]].cpu().numpy() for r, g in enumerate(gathered)])
+
+
+def sum_over_ranks(t):
+    """All-reduce SUM of a counter tensor (the Monte-Carlo loops' ``reduce``
+    argument: slotgen.evaluate_uncoded, ldpc.evaluate_coded)."""
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return t
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t
+
+
+class StepGather:
+    """Gather of one step's per-rank result tensor (same shape on every rank,
+    e.g. the (B, U, S, T, W) LLRs of a bench step) into rank dst's
+    preallocated buffers — the "with gather" variant of SURVEY.md §8e, on
+    NCCL over NVLink for CUDA tensors (gloo for CPU tensors)."""
+
+    def __init__(self, like, dst: int = 0):
+        import torch
+        import torch.distributed as dist
+        self.world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+        self.rank = dist.get_rank() if self.world > 1 else 0
+        self.dst = dst
+        self.bufs = [torch.empty_like(like) for _ in range(self.world)] if self.rank == dst else None
+
+    def __call__(self, t):
+        import torch.distributed as dist
+        if self.world == 1:
+            return [t]
+        dist.gather(t, self.bufs if self.rank == self.dst else None, dst=self.dst)
+        return self.bufs
+
+    def bytes_per_step(self, t) -> int:
+        return t.numel() * t.element_size() * max(0, self.world - 1)

@@ -11,7 +11,7 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2409_02912_b200.shard import gather_slot_results, max_over_ranks, shard_slots
+from paper_2409_02912_b200.shard import StepGather, gather_slot_results, max_over_ranks, shard_slots, sum_over_ranks
 
 
 def _free_port():
@@ -73,3 +73,29 @@ def test_two_rank_gloo_gather_matches_single_process(tmp_path):
     ref = _errors(orc, cfg, config, w, mcs, y, books, bits, range(len(y)))
     np.testing.assert_array_equal(res[:-1].reshape(-1, 2), ref)
     assert res[-1] == 2  # max over ranks of (rank + 1)
+
+
+def _worker_gather(rank, world, port, result_path):
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    step = torch.full((3, 2, 4), float(rank + 1))
+    g = StepGather(step)
+    out = g(step)
+    counts = sum_over_ranks(torch.tensor([rank + 1, 10 * (rank + 1)], dtype=torch.int64))
+    if rank == 0:
+        np.save(result_path, np.concatenate([torch.stack(out).reshape(-1).numpy(), counts.numpy(),
+                                             [g.bytes_per_step(step)]]))
+    dist.destroy_process_group()
+
+
+def test_step_gather_and_counter_reduce_world2(tmp_path):
+    """The bench's with-gather step (one result tensor per rank into rank 0)
+    and the Monte-Carlo counter all-reduce, on gloo with world size 2."""
+    path = str(tmp_path / "g.npy")
+    mp.spawn(_worker_gather, args=(2, _free_port(), path), nprocs=2, join=True)
+    r = np.load(path)
+    got = r[:48].reshape(2, 3, 2, 4)
+    assert (got[0] == 1).all() and (got[1] == 2).all()
+    assert list(r[48:50]) == [3, 30]
+    assert r[50] == 3 * 2 * 4 * 4
