@@ -48,6 +48,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/tbler.json")
     ap.add_argument("--rt", default="", help="NRXW checkpoint of an RT model to add to the C2 sweep")
+    ap.add_argument("--c2-slots", type=int, default=256, help="slots per SNR point at C2")
     args = ap.parse_args()
     here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     config, w = checkpoint_load(os.path.join(here, "tests", "golden", "desk_d16_it2_long.nrxw"))
@@ -63,11 +64,14 @@ def main():
     # 273 PRB C2 slots, MCS 14 (16-QAM, r = 553/1024): the baselines through the scalable IRA code
     cfg = SlotConfig(num_subcarriers=3276, num_ues=2)
     t = default_mcs_table()
-    rxs = [("ls_lmmse", lambda s: GpuLsLmmse(4, 4)), ("perfect_kbest", lambda s: GpuKBest(4, 4, 16))]
+    rxs = [("ls_lmmse", lambda s: GpuLsLmmse(4, 4)),
+           ("lmmse_kbest", lambda s: GpuLmmseKBest(estimate_covariance(s, 200, seed=3), 4, 4, 16)),
+           ("perfect_kbest", lambda s: GpuKBest(4, 4, 16))]
     if args.rt:
         rt_config, rt_w = checkpoint_load(args.rt)
         rxs.insert(0, ("nrx_rt_gpu_trained", lambda s: NrxEngine(rt_config, rt_w, precision="fp16")))
-    res.append(sweep("C2 273 PRB", cfg, (t[14], t[14]), rxs, [6.0, 8.0, 10.0, 12.0, 14.0, 16.0, 18.0, 20.0], 32, 16))
+    res.append(sweep("C2 273 PRB", cfg, (t[14], t[14]), rxs, [4.0, 6.0, 8.0, 10.0, 12.0, 14.0, 16.0, 18.0, 20.0],
+                     args.c2_slots, 16))
     os.makedirs(os.path.dirname(os.path.abspath(args.out)), exist_ok=True)
     with open(args.out, "w") as f:
         json.dump(res, f, indent=1)
