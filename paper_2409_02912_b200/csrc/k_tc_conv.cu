@@ -74,7 +74,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 
 // Shared-memory carve-up (identical on host and device).
 struct ConvSmem {
-  uint32_t w, a, tw0, tw1, ta, th, bars, tmem_ptr, sbias, tb0, tb1, total;
+  uint32_t w, a, tw0, tw1, ta, th, bars, tmem_ptr, sbias, tb0, tb1, dt, total;
 };
 __host__ __device__ inline ConvSmem conv_smem_layout(const ConvTcParams& p, int tail) {
   ConvSmem s;
@@ -104,6 +104,8 @@ __host__ __device__ inline ConvSmem conv_smem_layout(const ConvTcParams& p, int 
   off += 256 * 4;
   s.tb1 = off;
   off += 64 * 4;
+  s.dt = off;  // symbol-axis positional encoding (per-lane indexed: shared, not the constant bank)
+  off += 32 * 4;
   s.total = off;
   return s;
 }
@@ -142,6 +144,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   float* sbias = reinterpret_cast<float*>(smem + L.sbias);
   float* stb0 = reinterpret_cast<float*>(smem + L.tb0);
   float* stb1 = reinterpret_cast<float*>(smem + L.tb1);
+  float* sdt = reinterpret_cast<float*>(smem + L.dt);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) tmem_alloc(tmem_ptr, p.tmem_cols);
@@ -165,6 +168,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   }
   if (threadIdx.x >= 64 && threadIdx.x < 64 + NP)
     sbias[threadIdx.x - 64] = reinterpret_cast<const float*>(p.wbase + p.b_off[io])[threadIdx.x - 64];
+  if (threadIdx.x < 32) sdt[threadIdx.x] = g.dt[threadIdx.x];
   if (TAIL) {
     const float* b0 = reinterpret_cast<const float*>(p.wbase + p.tb0[io]);
     const float* b1 = reinterpret_cast<const float*>(p.wbase + p.tb1[io]);
@@ -500,7 +504,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       const int clo = cbase / 8, chi = cbase / 8 + NC / 8;
       const bool need_pos = MODE != EPI_RELU && valid && (MODE != EPI_RESIDUAL || g.d % 8 != 0) &&
                             ((g.d / 8 >= clo && g.d / 8 < chi) || ((g.d + 1) / 8 >= clo && (g.d + 1) / 8 < chi));
-      const float pdt = need_pos ? g.dt[t] : 0.f;
+      const float pdt = need_pos ? sdt[t] : 0.f;
       const float pdf = need_pos ? pos_df(s, slab % g.U, g) : 0.f;
       ET* const drow = chunk_ptr(dst, slab, nd, 0, row, g);
       const uint32_t vmask = valid ? 0xffffffffu : 0u;

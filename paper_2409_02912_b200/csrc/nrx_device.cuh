@@ -11,9 +11,10 @@ namespace nrx {
 // Distance from subcarrier s to the nearest comb subcarrier of UE u
 // (positional_encoding, nrx.py:165-167).
 __device__ __forceinline__ int comb_dist(int s, int u, const Geom& g) {
-  const int o = u % g.comb;
+  const int o = u < g.comb ? u : u % g.comb;
   if (s <= o) return o - s;
-  const int lo = o + ((s - o) / g.comb) * g.comb;
+  const int q = g.comb == 1 ? s - o : (int)__umulhi((unsigned)(s - o), g.comb_magic);  // exact (make_geom)
+  const int lo = o + q * g.comb;
   int d = s - lo;
   const int hi = lo + g.comb;
   if (hi < g.S && hi - s < d) d = hi - s;
@@ -27,7 +28,8 @@ __device__ __forceinline__ int comb_dist(int s, int u, const Geom& g) {
 // while the float64 error is < 2^-28 / 2^k.
 __device__ __forceinline__ float pos_df(int s, int u, const Geom& g) {
   if (!g.freq_enc) return 0.f;
-  return __fdiv_rn((float)comb_dist(s, u, g), (float)g.S);
+  const int k = comb_dist(s, u, g);  // < comb
+  return g.comb <= 16 ? g.df_tab[k] : __fdiv_rn((float)k, (float)g.S);
 }
 
 // Value a producer writes into state channel c >= d (pos encoding / zero).

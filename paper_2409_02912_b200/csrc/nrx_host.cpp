@@ -99,6 +99,12 @@ int make_geom(const nrx_model_desc* m, const nrx_slot_desc* s, int n_slots, int 
   g->T = s->num_symbols;
   g->B = m->num_rx_ant;
   g->comb = s->comb_size;
+  // (s - o) / comb as __umulhi(s - o, ceil(2^32 / comb)) is exact while (s - o) * comb^2 < 2^32
+  if ((uint64_t)s->num_subcarriers * (uint64_t)s->comb_size * (uint64_t)s->comb_size >= (1ull << 32))
+    return NRX_ERR_UNSUPPORTED;
+  g->comb_magic = s->comb_size > 1 ? (uint32_t)(((1ull << 32) + s->comb_size - 1) / s->comb_size) : 0u;
+  for (int k = 0; k < 16; ++k)  // IEEE float division, as __fdiv_rn((float)k, (float)S) on the device
+    g->df_tab[k] = (float)k / (float)s->num_subcarriers;
   g->K = s->num_pilot_symbols;
   for (int i = 0; i < g->K; ++i) g->ps[i] = s->pilot_symbols[i];
   g->ks = m->kernel_size;

@@ -33,6 +33,8 @@ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // Geometry + channel bookkeeping, passed by value to kernels.
 struct Geom {
   int N, U, NU, S, T, B, comb, K;
+  uint32_t comb_magic;        // ceil(2^32 / comb): (s - o) / comb by one __umulhi (comb > 1)
+  float df_tab[16];           // float32(k / S) for k < comb <= 16 (the frequency encoding)
   int ps[NRX_MAX_PILOT_SYMBOLS];
   int ks, r, Tp, H;           // kernel size, radius, padded symbols, halo rows
   float inv_Tp;               // 1 / Tp: row -> (s, t) by one multiply (rows < 2^21)
