@@ -84,7 +84,7 @@ __host__ __device__ inline ConvSmem conv_smem_layout(const ConvTcParams& p, int 
   s.a = off;
   off += p.stages * p.abytes;
   s.tw0 = s.tw1 = s.ta = s.th = off;
-  if (tail) {  // tail weights, double-buffered state tile (A), single hidden tile (H)
+  if (tail) {  // tail weights, double-buffered state tile (A), hidden tile(s) (H: two for TAIL_MSG)
     s.tw0 = off;
     off += p.tw0bytes;
     s.tw1 = off;
@@ -92,7 +92,7 @@ __host__ __device__ inline ConvSmem conv_smem_layout(const ConvTcParams& p, int 
     s.ta = off;
     off += 2u * p.g.Cs * NRX_TILE_M * 2;
     s.th = off;
-    off += (uint32_t)p.thp * NRX_TILE_M * 2;
+    off += (tail == TAIL_MSG ? 2u : 1u) * p.thp * NRX_TILE_M * 2;
   }
   s.bars = off;
   off += 32 * 8;
@@ -183,6 +183,12 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   const uint32_t col_h = 2 * NP, col_o = 2 * NP + 2 * p.thp;
   const uint32_t ta_bytes = (uint32_t)g.Cs * NRX_TILE_M * 2, th_bytes = (uint32_t)p.thp * NRX_TILE_M * 2;
   const int R = p.rbox;
+  // fc1 of tile j is issued LAG tiles after conv(j).  TAIL_MSG: LAG = 3 with two
+  // hidden tiles, so the MMA warp's wait for a hidden layer never holds back the
+  // next conv by less than two epilogue iterations; TAIL_READOUT (wider hidden
+  // layer, one tile fits): LAG = 2.
+  constexpr int LAG = TAIL == TAIL_MSG ? 3 : 2;
+  constexpr uint32_t NTH = TAIL == TAIL_MSG ? 2 : 1;
 #ifdef NRX_TIMING
   long long t_a = 0, t_b = 0, t_c = 0, t_d = 0, t_all = clock64();
 #endif
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     }
     // tail MLP, software-pipelined against the epilogue: in loop step i the MMA
     // warp issues conv(i), fc0(i-1) (hidden = state_tile x W0, N = thp) and
-    // fc1(i-2) (out = relu-hidden x W1, N = top); buffers alternate by tile parity
+    // fc1(i-LAG) (out = relu-hidden x W1, N = top); buffers alternate by tile parity
     auto issue_fc0 = [&](int j) {
       const int b = j & 1;
       const uint32_t id0 = idesc_f16kind<ET>(NRX_TILE_M, p.thp);
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       mbar_wait(B_h_ready + 8u * (b), (j >> 1) & 1);
       NRX_TADD(t_d, tw);
       tc_fence_after();
-      uint64_t ad = smem_desc(smem_u32(smem + L.th), NRX_TILE_M * 16, 128);
+      uint64_t ad = smem_desc(smem_u32(smem + L.th + (NTH == 2 ? b : 0) * th_bytes), NRX_TILE_M * 16, 128);
       uint64_t bd = smem_desc(smem_u32(smem + L.tw1), p.top * 16, 128);
       for (int kc = 0; kc < p.thp / 8; kc += 2) {
         mma_bf16_warp(tmem_base + col_o + b * p.top, ad, bd, id1, kc != 0);
@@ -334,13 +340,12 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       mma_commit_warp(B_tfull + 8u * (acc));
       // earlier tiles' MLP tails run while this tile's conv MMAs execute
       if (TAIL && it >= 1) issue_fc0(it - 1);
-      if (TAIL && it >= 2) issue_fc1(it - 2);
+      if (TAIL && it >= LAG) issue_fc1(it - LAG);
       ++it;
     }
-    if (TAIL) {  // drain: fc0(n-1), fc1(n-2), fc1(n-1)
+    if (TAIL) {  // drain: fc0(n-1), fc1(n-LAG) .. fc1(n-1)
       if (it >= 1) issue_fc0(it - 1);
-      if (it >= 2) issue_fc1(it - 2);
-      if (it >= 1) issue_fc1(it - 1);
+      for (int j = it - LAG > 0 ? it - LAG : 0; j < it; ++j) issue_fc1(j);
     }
   } else {  // ---------------- epilogue: warps 2 .. 2 + 4*PARTS - 1
     // bf16 keeps an fp32 master of the state (dst32, STATE_INIT / RESIDUAL); fp16 has none
@@ -352,7 +357,8 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     const int cbase = part * NC;
     const int nd = p.cdst / 8, n32 = p.d4 / 4;
     const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
-    int hist_slab[2] = {0, 0}, hist_tile[2] = {0, 0};  // tiles whose tail outputs are pending
+    // tiles whose tail outputs are pending: hs[k] / ht[k] = tile it-1-k (a register shift chain)
+    int hs[3] = {0, 0, 0}, ht[3] = {0, 0, 0};
     const uint32_t ta_s = smem_u32(smem + L.ta), th_s = smem_u32(smem + L.th);
     const uint32_t sbias_s = smem_u32(sbias), stb0_s = smem_u32(stb0), stb1_s = smem_u32(stb1);
     // chunks holding no state channel (8 cc >= d) are the positional / zero
@@ -373,7 +379,8 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       NRX_TADD(t_d, tw);
       tc_fence_after();
       const int hch = p.thp / 8, hbeg = part * hch / PARTS, hend = (part + 1) * hch / PARTS;
-      // TH is free: fc1 of the previous tile completed (tail_out ran first)
+      // TH[j] is free: fc1 of its previous tile (j - NTH) completed (tail_out(j + 1 - LAG) ran first)
+      const uint32_t thb = th_s + (NTH == 2 ? b : 0) * th_bytes;
       for (int c8 = hbeg; c8 < hend; ++c8) {
         float hv[8], bb[8];
         tmem_ld8(tmem_base + lane_off + col_h + b * p.thp + 8 * c8, hv);
@@ -381,7 +388,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) hv[e] += bb[e];
-        st_shared_u4(th_s + (uint32_t)(c8 * NRX_TILE_M + r) * 16u,
+        st_shared_u4(thb + (uint32_t)(c8 * NRX_TILE_M + r) * 16u,
                      relu_chunk(pack_chunk(hv, static_cast<const ET*>(nullptr)), static_cast<const ET*>(nullptr)));
       }
       fence_proxy_async();
@@ -439,14 +446,15 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
             reinterpret_cast<float4*>(cp)[0] = make_float4(o[8], o[12], o[9], o[13]);
             reinterpret_cast<float4*>(cp)[1] = make_float4(o[10], o[14], o[11], o[15]);
           } else {
+            // constant register indices only (a runtime index would put o[] in local memory)
+            float* cf = reinterpret_cast<float*>(cp);
 #pragma unroll
-            for (int bb = 0; bb < 8; ++bb) {
-              if (bb >= g.B) break;
-              float im = 0.f;
+            for (int bb = 0; bb < 8; ++bb)
+              if (bb < g.B) cf[2 * bb] = o[8 + bb];
 #pragma unroll
-              for (int k = 0; k < 8; ++k)
-                if (k == bb) im = o[8 + g.B + k];
-              cp[bb] = make_float2(o[8 + bb], im);
+            for (int c = 9; c < 24; ++c) {
+              const int bb = c - 8 - g.B;  // imaginary part of antenna bb
+              if (bb >= 0 && bb < g.B) cf[2 * bb + 1] = o[c];
             }
           }
         }
@@ -571,20 +579,26 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         fence_proxy_async();  // state tile (generic-proxy stores) -> tensor-core reads
         tc_fence_before();
         mbar_arrive(B_ta_ready + 8u * (it & 1));
-        // pipelined tail stages: outputs of tile it-2 (frees the hidden tile),
-        // then the hidden layer of tile it-1
-        if (it >= 2) tail_out(it - 2, hist_slab[it & 1], hist_tile[it & 1]);
+        // pipelined tail stages: outputs of tile it-LAG (frees its hidden
+        // tile), then the hidden layer of tile it-1
+        if (it >= LAG) tail_out(it - LAG, hs[LAG - 1], ht[LAG - 1]);
         if (it >= 1) tail_hidden(it - 1);
-        hist_slab[it & 1] = slab;
-        hist_tile[it & 1] = tile;
+        hs[2] = hs[1];
+        ht[2] = ht[1];
+        hs[1] = hs[0];
+        ht[1] = ht[0];
+        hs[0] = slab;
+        ht[0] = tile;
       }
       NRX_TADD(t_b, t1);
       ++it;
     }
     if (TAIL) {  // drain, mirroring the MMA warp
-      if (it >= 2) tail_out(it - 2, hist_slab[it & 1], hist_tile[it & 1]);
+      if (it >= LAG) tail_out(it - LAG, hs[LAG - 1], ht[LAG - 1]);
       if (it >= 1) tail_hidden(it - 1);
-      if (it >= 1) tail_out(it - 1, hist_slab[(it - 1) & 1], hist_tile[(it - 1) & 1]);
+#pragma unroll
+      for (int k = LAG - 2; k >= 0; --k)  // tiles it-1-k, oldest first
+        if (it - 1 - k >= 0) tail_out(it - 1 - k, hs[k], ht[k]);
     }
   }
 #ifdef NRX_TIMING

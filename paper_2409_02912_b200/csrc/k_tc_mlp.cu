@@ -359,14 +359,15 @@ __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
       reinterpret_cast<float4*>(cp)[0] = make_float4(o[8], o[12], o[9], o[13]);
       reinterpret_cast<float4*>(cp)[1] = make_float4(o[10], o[14], o[11], o[15]);
     } else {
+      // constant register indices only (a runtime index would put o[] in local memory)
+      float* cf = reinterpret_cast<float*>(cp);
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        if (b >= g.B) break;
-        float im = 0.f;
+      for (int b = 0; b < 8; ++b)
+        if (b < g.B) cf[2 * b] = o[8 + b];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (k == b) im = o[8 + g.B + k];  // static register indexing
-        cp[b] = make_float2(o[8 + b], im);
+      for (int c = 9; c < 24; ++c) {
+        const int b = c - 8 - g.B;  // imaginary part of antenna b
+        if (b >= 0 && b < g.B) cf[2 * b + 1] = o[c];
       }
     }
   });

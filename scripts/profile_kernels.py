@@ -49,6 +49,10 @@ for name, ms in rec.items():
     total += per_launch * n_per_fwd
     tf = flops[name] * res / (per_launch / 1e3) / 1e12
     out[name] = {"ms": round(per_launch, 4), "launches_per_fwd": n_per_fwd, "tflops": round(tf, 1)}
+for name, ms in rec.items():  # kernels launched several times per forward: per position
+    k = int(round(len(ms) / args.reps))
+    if k > 1:
+        print(f"{name:18s} per launch position: " + ", ".join(f"{float(np.mean(ms[i::k])):.4f}" for i in range(k)))
 for name, v in out.items():
     v["share"] = round(v["ms"] * v["launches_per_fwd"] / total, 3)
     print(f"{name:18s} {v['ms']:8.4f} ms x{v['launches_per_fwd']:.0f}  {v['tflops']:7.1f} TFLOP/s  share {v['share']:.3f}")
