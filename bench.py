@@ -612,8 +612,27 @@ def e2e_throughput(eng, cfg, B, steps, world, dev):
         el = float(t.item())
     h2d = sum(t.numel() * t.element_size() for t in hosts[0])
     d2h = sum(t.numel() * t.element_size() for t in outs[0])
+    # the e2e roofline: a bare device -> pinned-host copy of one step's outputs
+    # (the larger direction; H2D runs concurrently on the other copy engine)
+    dev_outs = [torch.empty(o.shape, dtype=o.dtype, device=dev) for o in outs[0]]
+    for o, g in zip(outs[0], dev_outs):
+        o.copy_(g, non_blocking=True)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    ev0.record()
+    for _ in range(reps):
+        for o, g in zip(outs[0], dev_outs):
+            o.copy_(g, non_blocking=True)
+    ev1.record()
+    torch.cuda.synchronize()
+    d2h_gbs = d2h * reps / (ev0.elapsed_time(ev1) / 1e3) / 1e9
+    del dev_outs
     return {"value": round(B * steps * world / el, 2), "unit": "slots/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "pcie": {"d2h_copy_gbs": round(d2h_gbs, 1),
+                     "d2h_bound_slots_per_s": round(d2h_gbs * 1e9 / (d2h / B) * world, 1),
+                     "note": "bare pinned D2H copy of one step's LLR + chest; the e2e value cannot exceed this bound"},
             "api": "NrxEngine.run_stream (pinned host inputs -> GPU -> pinned host LLR/chest every step; "
                    "H2D/compute/D2H overlapped across steps; wall clock incl. final sync)"}
 
