@@ -612,27 +612,47 @@ def e2e_throughput(eng, cfg, B, steps, world, dev):
         el = float(t.item())
     h2d = sum(t.numel() * t.element_size() for t in hosts[0])
     d2h = sum(t.numel() * t.element_size() for t in outs[0])
-    # the e2e roofline: a bare device -> pinned-host copy of one step's outputs
-    # (the larger direction; H2D runs concurrently on the other copy engine)
+    # the e2e roofline: bare pinned copies of one step's outputs (D2H alone),
+    # and of its inputs and outputs at once (H2D and D2H on two streams, as
+    # run_stream overlaps them)
     dev_outs = [torch.empty(o.shape, dtype=o.dtype, device=dev) for o in outs[0]]
-    for o, g in zip(outs[0], dev_outs):
-        o.copy_(g, non_blocking=True)
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 10
-    ev0.record()
-    for _ in range(reps):
-        for o, g in zip(outs[0], dev_outs):
-            o.copy_(g, non_blocking=True)
-    ev1.record()
-    torch.cuda.synchronize()
-    d2h_gbs = d2h * reps / (ev0.elapsed_time(ev1) / 1e3) / 1e9
-    del dev_outs
+    dev_ins = [torch.empty(h.shape, dtype=h.dtype, device=dev) for h in hosts[0]]
+    s_a, s_b = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+    def timed(h2d_too, reps=10):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        done_a, done_b = torch.cuda.Event(), torch.cuda.Event()
+        torch.cuda.synchronize()
+        ev0.record()
+        s_a.wait_event(ev0)
+        s_b.wait_event(ev0)
+        for _ in range(reps):
+            with torch.cuda.stream(s_a):
+                for o, g in zip(outs[0], dev_outs):
+                    o.copy_(g, non_blocking=True)
+            if h2d_too:
+                with torch.cuda.stream(s_b):
+                    for g, h in zip(dev_ins, hosts[0]):
+                        g.copy_(h, non_blocking=True)
+        done_a.record(s_a)
+        done_b.record(s_b)
+        torch.cuda.current_stream().wait_event(done_a)
+        torch.cuda.current_stream().wait_event(done_b)
+        ev1.record()
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) / 1e3 / reps   # seconds per step
+
+    timed(True, 2)
+    t_d2h, t_duplex = timed(False), timed(True)
+    del dev_outs, dev_ins
+    pcie = {"d2h_copy_gbs": round(d2h / t_d2h / 1e9, 1),
+            "d2h_bound_slots_per_s": round(B * world / t_d2h, 1),
+            "duplex_bound_slots_per_s": round(B * world / t_duplex, 1),
+            "note": "bare pinned copies of one step's outputs (D2H) and of its inputs + outputs on two "
+                    "streams (duplex); the e2e value cannot exceed the duplex bound"}
     return {"value": round(B * steps * world / el, 2), "unit": "slots/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "pcie": {"d2h_copy_gbs": round(d2h_gbs, 1),
-                     "d2h_bound_slots_per_s": round(d2h_gbs * 1e9 / (d2h / B) * world, 1),
-                     "note": "bare pinned D2H copy of one step's LLR + chest; the e2e value cannot exceed this bound"},
+            "pcie": pcie,
             "api": "NrxEngine.run_stream (pinned host inputs -> GPU -> pinned host LLR/chest every step; "
                    "H2D/compute/D2H overlapped across steps; wall clock incl. final sync)"}
 

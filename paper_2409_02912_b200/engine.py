@@ -152,31 +152,34 @@ class NrxEngine:
         inputs[i] = (y, pilots, noise_feat, mod_order) pinned CPU tensors of
         batch i, outputs[i] = (llr, chest) pinned CPU tensors it is written
         to.  H2D of batch i+1 and D2H of batch i-1 run on their own streams
-        and overlap the forward of batch i (double-buffered device inputs and
-        outputs); returns after every output has landed in host memory.
+        and overlap the forward of batch i (triple-buffered device inputs and
+        outputs, so the copy engines never wait on a forward that is itself
+        waiting for a buffer); returns after every output has landed in host
+        memory.
         """
         torch = _require_cuda()
         if not inputs:
             return
         dev = self.device
+        nbuf = 3
         s_in, s_cmp, s_out = (torch.cuda.Stream(device=dev) for _ in range(3))
-        d_in = [tuple(torch.empty_like(t, device=dev) for t in inputs[0]) for _ in range(2)]
-        d_out = [tuple(torch.empty_like(t, device=dev) for t in outputs[0]) for _ in range(2)]
+        d_in = [tuple(torch.empty_like(t, device=dev) for t in inputs[0]) for _ in range(nbuf)]
+        d_out = [tuple(torch.empty_like(t, device=dev) for t in outputs[0]) for _ in range(nbuf)]
         ws = self.workspace(cfg, inputs[0][0].shape[0])
-        ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "cmp", "out")}
-        started = [False, False]
+        ev = {k: [torch.cuda.Event() for _ in range(nbuf)] for k in ("in", "cmp", "out")}
+        started = [False] * nbuf
         for i, (src, dst) in enumerate(zip(inputs, outputs)):
-            b = i & 1
+            b = i % nbuf
             with torch.cuda.stream(s_in):
                 if started[b]:
-                    s_in.wait_event(ev["cmp"][b])          # forward i-2 done reading d_in[b]
+                    s_in.wait_event(ev["cmp"][b])          # forward i-nbuf done reading d_in[b]
                 for d, h in zip(d_in[b], src):
                     d.copy_(h, non_blocking=True)
                 ev["in"][b].record(s_in)
             with torch.cuda.stream(s_cmp):
                 s_cmp.wait_event(ev["in"][b])
                 if started[b]:
-                    s_cmp.wait_event(ev["out"][b])         # D2H i-2 done reading d_out[b]
+                    s_cmp.wait_event(ev["out"][b])         # D2H i-nbuf done reading d_out[b]
                 y, pil, nf, mods = d_in[b]
                 self.forward_device(cfg, y, pil, nf, mods, num_iterations, d_out[b][0], d_out[b][1],
                                     workspace=ws, stream=s_cmp)
