@@ -402,6 +402,8 @@ def run_ours(args):
         "launches_per_step": n_launch,
         "clocks": sampler.summary(),
     }
+    if rank == 0 and world == 1 and not args.no_precision_sweep:
+        out["dropin_single_slot"] = dropin_latency(cfg, config, w, mcs)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_subprocess()
     if rank == 0:
@@ -535,6 +537,29 @@ def monte_carlo_pipeline(eng, cfg, B, steps, world, rank, dev):
             "launches_per_step": 2 + eng.launch_count(cfg, N_IT) + 1,
             "note": "device Philox variates, doubletdl channels, 16-QAM, n0 = 0.1; random-init receiver, so the "
                     "BER is ~0.5 by construction"}
+
+
+def dropin_latency(cfg, config, w, mcs, runs: int = 20):
+    """The drop-in ``nrx_forward`` exactly as the reference arm is timed: one C2
+    slot per call, numpy complex128 in, numpy LLRs / chest out (host copies,
+    pilot stacking, MCS checks and the weight fingerprint inside the call)."""
+    from paper_2409_02912_b200.nrx import nrx_forward
+    from paper_2409_02912_b200.synth import synth_slots
+    y, books, _ = synth_slots(cfg, [4, 4], 2, 0.1, seed=5)
+    out = {}
+    for prec in ("fp16", "fp32"):
+        for i in range(3):
+            nrx_forward(y[i % 2], books[i % 2], cfg, mcs, w, config, 0.1, precision=prec)
+        ts = []
+        for i in range(runs):
+            t0 = time.perf_counter()
+            nrx_forward(y[i % 2], books[i % 2], cfg, mcs, w, config, 0.1, precision=prec)
+            ts.append(time.perf_counter() - t0)
+        ts = np.asarray(ts)
+        out[prec] = {"p50_ms": round(float(np.median(ts) * 1e3), 3), "slots_per_s": round(float(1.0 / ts.mean()), 1)}
+    out["note"] = ("paper_2409_02912_b200.nrx.nrx_forward with the reference signature, one C2 slot per call "
+                   "(numpy in / numpy out), the call pattern the reference arm is timed with")
+    return out
 
 
 def next_rows(cfg, B, dev, reps: int = 3):
