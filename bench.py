@@ -219,16 +219,30 @@ def run_reference(args, slots: int, warmup: int):
             "sample": f"{slots} single-slot nrx_forward calls at C2 (273 PRB, 2 UE, d_s=56, N_it=2) after {warmup} warm-up"}
 
 
-def cpu_baseline_subprocess(slots=3, warmup=1):
-    """Run the reference arm in a child process so OpenBLAS gets all cores."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_subprocess(slots=5, warmup=1, threads=None):
+    """Run the reference arm in a child process so OpenBLAS gets all cores
+    (or `threads`); >= 1 warm-up, >= 5 runs at 273 PRB."""
     env = dict(os.environ)
-    env["OPENBLAS_NUM_THREADS"] = str(os.cpu_count() or 1)
+    env["OPENBLAS_NUM_THREADS"] = str(threads or os.cpu_count() or 1)
     env.pop("WORLD_SIZE", None); env.pop("RANK", None); env.pop("LOCAL_RANK", None)
     cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--cpu-json",
            "--steps", str(slots), "--warmup", str(warmup)]
     try:
         out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900).stdout
-        return json.loads(out.strip().splitlines()[-1])
+        res = json.loads(out.strip().splitlines()[-1])
+        res["cpu_model"] = cpu_model()
+        return res
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": "slots/s", "kind": "unavailable", "cores": os.cpu_count(),
                 "sample": f"failed: {e!r}"}
@@ -406,6 +420,8 @@ def run_ours(args):
         out["dropin_single_slot"] = dropin_latency(cfg, config, w, mcs)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_subprocess()
+        one = cpu_baseline_subprocess(slots=2, warmup=1, threads=1)
+        out["cpu_baseline"]["single_thread"] = {k: one.get(k) for k in ("value", "p50_ms", "cores", "sample")}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -467,11 +483,20 @@ def other_config_latencies(precision, dev, runs: int):
     c1 = NrxConfig.from_table(t, (14,), d_s=56, num_iterations=2)
     out["C1_24prb_1ue"] = latency_single_slot(NrxEngine(c1, init_weights(c1, 0), precision, dev), cfg1, dev, runs,
                                               note="C1 slot (24 PRB, 1 UE, RT d_s=56 N_it=2)")
+    for d, n in ((16, 2), (16, 4)):  # the desk models of configs[0] (configio.py:43-50)
+        cd = NrxConfig.from_table(t, (14,), d_s=d, num_iterations=n)
+        out[f"C1_24prb_1ue_d{d}_it{n}"] = latency_single_slot(
+            NrxEngine(cd, init_weights(cd, 0), precision, dev), cfg1, dev, runs, n_it=n,
+            note=f"C1 slot (24 PRB, 1 UE, desk d_s={d} N_it={n})")
     cfg = SlotConfig(num_subcarriers=S_C2, num_ues=2, comb_size=2)
     c3 = NrxConfig.from_table(t, (9, 14, 19, 27), variant="masking", d_s=56, num_iterations=2)
     out["C3_mixed_qpsk_256qam"] = latency_single_slot(
         NrxEngine(c3, init_weights(c3, 0), precision, dev), cfg, dev, runs, orders=[2, 8], width=8,
         note="C3 slot (273 PRB, UE0 QPSK + UE1 256-QAM ext., masking m_max=8)")
+    cv = NrxConfig.from_table(t, (9, 14, 19), variant="var_io", d_s=56, num_iterations=2)
+    out["C3_var_io_qpsk_64qam"] = latency_single_slot(
+        NrxEngine(cv, init_weights(cv, 0), precision, dev), cfg, dev, runs, orders=[2, 6], width=6,
+        note="C3 slot (273 PRB, UE0 QPSK + UE1 64-QAM, var_io: per-order input / output weight sets)")
     c4 = NrxConfig.from_table(t, (14,), d_s=56, num_iterations=8)
     e4 = NrxEngine(c4, init_weights(c4, 0), precision, dev)
     depth = {}
@@ -690,7 +715,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--precision", choices=("bf16", "fp16", "fp32"), default=os.environ.get("NRX_BENCH_PRECISION", "fp16"))
     ap.add_argument("--slots-per-step", type=int, default=32)
-    ap.add_argument("--latency-runs", type=int, default=2000)
+    ap.add_argument("--latency-runs", type=int, default=10000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-precision-sweep", action="store_true",
                     help="skip timing the other precisions (by_precision)")
