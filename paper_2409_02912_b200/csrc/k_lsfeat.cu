@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(128) k_ls_feat(Geom g, const YT* __restrict__ 
                                                  int n_pilot_sets, const float* __restrict__ noise_feat,
                                                  OutT* __restrict__ feats) {
   constexpr int CW = 16 / sizeof(OutT);
+  pdl_launch_dependents();  // the first conv's prologue may overlap this kernel's last wave
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   const int slab = blockIdx.y;
   if (row >= g.rows_slab) return;

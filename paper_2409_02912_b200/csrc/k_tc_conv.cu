@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   float* sdt = reinterpret_cast<float*>(smem + L.dt);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_launch_dependents();  // the next layer's prologue may run on SMs this grid frees
   if (warp == 0) tmem_alloc(tmem_ptr, p.tmem_cols);
   if (threadIdx.x == 32) {
     for (int s = 0; s < p.stages; ++s) {
@@ -205,6 +206,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         bulk_load(smem + L.tw0, p.wbase + p.tw0[io], p.tw0bytes, wbar);
         bulk_load(smem + L.tw1, p.wbase + p.tw1[io], p.tw1bytes, wbar);
       }
+      pdl_wait();  // activations: written by the previous layer
       // one pipeline stage per (tile, input source): finer-grained stages keep
       // more loads in flight next to the resident weights
       WorkIter w(g, g.NU, g.tiles, p.n_io, p.mod_order);
@@ -348,6 +350,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       for (int j = it - LAG > 0 ? it - LAG : 0; j < it; ++j) issue_fc1(j);
     }
   } else {  // ---------------- epilogue: warps 2 .. 2 + 4*PARTS - 1
+    pdl_wait();  // reads (residual) and writes activation buffers of the previous layers
     // bf16 keeps an fp32 master of the state (dst32, STATE_INIT / RESIDUAL); fp16 has none
     constexpr bool MASTER = std::is_same<ET, __nv_bfloat16>::value;
     constexpr int PARTS = conv_parts(NP);
@@ -728,7 +731,7 @@ static int launch_conv(const Geom& g, const ConvLaunch& c, const uint8_t* wb, co
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.NU * g.tiles;
   dim3 grid(total < num_sms() ? total : num_sms(), p.n_io);
-  fn<<<grid, conv_threads(p.np), smem, st>>>(p, m0, m1);
+  if (launch_pdl(fn, grid, dim3(conv_threads(p.np)), smem, st, p, m0, m1) != cudaSuccess) return NRX_ERR_CUDA;
   return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
 }
 

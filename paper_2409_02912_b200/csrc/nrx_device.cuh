@@ -8,6 +8,15 @@
 
 namespace nrx {
 
+// Programmatic dependent launch (PDL).  A kernel launched with programmatic
+// stream serialization may start while its predecessor still runs: it does its
+// prologue (barriers, TMEM, resident weights), then pdl_wait() blocks until the
+// predecessor grid has completed and its writes are visible.  Every read or
+// write of activation memory must come after pdl_wait().
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Lets the next PDL-launched kernel be scheduled (on SMs this grid frees).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // Distance from subcarrier s to the nearest comb subcarrier of UE u
 // (positional_encoding, nrx.py:165-167).
 __device__ __forceinline__ int comb_dist(int s, int u, const Geom& g) {

@@ -4,6 +4,7 @@
 #include <cuda.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 
@@ -294,6 +295,31 @@ inline int make_map(CUtensorMap* m, const void* base, const Geom& g, int C, int 
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? NRX_OK : NRX_ERR_CUDA;
+}
+
+// Launch with programmatic stream serialization (see pdl_wait); NRX_PDL=0 in
+// the environment turns it off (plain stream order).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("NRX_PDL");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+template <typename... Args, typename... Act>
+inline cudaError_t launch_pdl(void (*fn)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Act&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, fn, std::forward<Act>(args)...);
 }
 
 inline int num_sms() {
