@@ -204,3 +204,41 @@ def test_concurrent_threads_deterministic():
     for r in results:
         for u in range(len(base)):
             np.testing.assert_array_equal(r[u], base[u])
+
+
+def test_pdl_launch_bit_identical_to_stream_order(tmp_path):
+    """The tensor-core layers are launched with programmatic dependent launch
+    (each layer's prologue overlaps its predecessor; every activation access
+    waits for the predecessor grid).  The results must be bit-identical to
+    plain stream order (NRX_PDL=0, read once per process: run in a child)."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "fwd.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights\n"
+        "from paper_2409_02912_b200.nrx import nrx_forward\n"
+        "from paper_2409_02912_b200.synth import synth_slots\n"
+        "t = default_mcs_table()\n"
+        "cfg = SlotConfig(num_subcarriers=3276, num_ues=2, comb_size=2)\n"
+        "config = NrxConfig.from_table(t, (14,), d_s=56, num_iterations=2)\n"
+        "w = init_weights(config, 0)\n"
+        "rng = np.random.default_rng(5)\n"
+        "w = {k: v + (0.05 * rng.standard_normal(v.shape).astype(np.float32) if v.ndim == 1 else 0) for k, v in w.items()}\n"
+        "y, books, _ = synth_slots(cfg, [4, 4], 3, 0.1, seed=4)\n"
+        "out = {}\n"
+        "for p in ('fp16', 'bf16'):\n"
+        "    llrs, chest = nrx_forward(y, books, cfg, (t[14], t[14]), w, config, 0.1, precision=p)\n"
+        "    out[p + '_l0'], out[p + '_l1'], out[p + '_c'] = llrs[0], llrs[1], chest\n"
+        "np.savez(sys.argv[1], **out)\n")
+    res = {}
+    for pdl in ("1", "0"):
+        env = dict(os.environ, NRX_PDL=pdl)
+        f = tmp_path / f"out{pdl}.npz"
+        subprocess.run([sys.executable, str(script), str(f)], check=True, env=env, timeout=600)
+        with np.load(f) as z:
+            res[pdl] = {k: z[k] for k in z.files}
+    for k in res["1"]:
+        np.testing.assert_array_equal(res["1"][k], res["0"][k], err_msg=k)
