@@ -13,7 +13,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch  # noqa: E402
 
-from paper_2409_02912_b200.config import NrxConfig, SlotConfig, checkpoint_save, default_mcs_table, init_weights  # noqa: E402
+from paper_2409_02912_b200.config import (NrxConfig, SlotConfig, checkpoint_load, checkpoint_save,  # noqa: E402
+                                          default_mcs_table, init_weights)
 from paper_2409_02912_b200.engine import NrxEngine  # noqa: E402
 from paper_2409_02912_b200.slotgen import GpuSlotSource, evaluate_uncoded  # noqa: E402
 from paper_2409_02912_b200.training import GpuTrainConfig, train_gpu  # noqa: E402
@@ -28,13 +29,19 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--lr", type=float, default=2e-3)
     ap.add_argument("--out", default="gpurun_out/nrx_gpu.nrxw")
+    ap.add_argument("--init", default=None, help="continue from this NRXW checkpoint")
+    ap.add_argument("--seed", type=int, default=0, help="slot-stream seed of the training batches")
     args = ap.parse_args()
     table = default_mcs_table()
     cfg = SlotConfig(num_subcarriers=args.S, num_ues=2)
-    config = NrxConfig.from_table(table, (14,), d_s=args.d, num_iterations=args.it)
-    w = init_weights(config, 0)
+    if args.init:
+        config, w = checkpoint_load(args.init)
+    else:
+        config = NrxConfig.from_table(table, (14,), d_s=args.d, num_iterations=args.it)
+        w = init_weights(config, 0)
     src = GpuSlotSource(cfg)
-    tcfg = GpuTrainConfig(batch_size=args.batch, steps=args.steps, snr_lo_db=4.0, snr_hi_db=24.0, learning_rate=args.lr)
+    tcfg = GpuTrainConfig(batch_size=args.batch, steps=args.steps, snr_lo_db=4.0, snr_hi_db=24.0, learning_rate=args.lr,
+                          seed=args.seed)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     graph, _, hist = train_gpu(config, w, src, table, tcfg, log_every=max(1, args.steps // 10))
