@@ -96,3 +96,20 @@ def test_pilot_comb_values_layout():
     assert p.shape == (2, 13, 2)
     assert p[1, 3, 1] == vals[1, 1 + 3 * 2, 11]
     assert p[0, 12, 0] == vals[0, 24, 2]
+
+
+@pytest.mark.parametrize("precision,num_ues,n_it,expect", [
+    ("fp16", 2, 2, 7),   # ls_feat, init.conv0, init.conv1+msg, 2 x (update.conv0, update.conv1+tail)
+    ("bf16", 2, 8, 19),
+    ("fp16", 1, 2, 9),   # U != 2: standalone message kernel per iteration
+    ("fp32", 2, 2, 10),  # SIMT parity path: ls_feat, 2 init convs, 3 per iteration, readout
+])
+def test_forward_launch_count(precision, num_ues, n_it, expect):
+    """nrx_forward_launch_count is the per-forward kernel count bench.py
+    reports as gpu_launches; it must match the launch sequence of the path."""
+    config = NrxConfig(d_s=56, num_iterations=8)
+    cfg = SlotConfig(num_subcarriers=3276, num_ues=num_ues, comb_size=2)
+    lib = _lib.load()
+    m, s = _lib.model_desc(config), _lib.slot_desc(cfg)
+    prec = {"fp32": 0, "bf16": 1, "fp16": 2}[precision]
+    assert lib.nrx_forward_launch_count(ctypes.byref(m), ctypes.byref(s), prec, n_it) == expect
