@@ -53,6 +53,27 @@ def test_decoder_bit_exact_vs_oracle_on_ira():
     assert 0 < ref_ok.sum() < 12          # both converging and failing codewords exercised
 
 
+def test_decoder_multi_group_ragged_vs_oracle():
+    """70 codewords = three 32-lane groups, the last one ragged: each group is
+    decoded in its own pass (nrx_ldpc_decode); results match the oracle."""
+    torch = _t()
+    from paper_2409_02912_b200.ldpc import GpuLdpc, rate_matched_ira_code
+    code = rate_matched_ira_code(2 * 1152, 553 / 1024, seed=3)
+    rng = np.random.default_rng(11)
+    info = (rng.random((70, code.k_eff)) < 0.5).astype(np.uint8)
+    tx = lo.staircase_codeword(code, info)[:, code.tx_positions].astype(np.float64)
+    sig = np.linspace(0.5, 1.05, 70)[:, None]
+    llr = np.clip(2 * ((2 * tx - 1) + sig * rng.normal(size=tx.shape)) / sig ** 2, -20, 20).astype(np.float32)
+    g = GpuLdpc(code)
+    for it in (20, 4):
+        dec, ok = g.decode(torch.from_numpy(llr).cuda(), it)
+        ref_dec, ref_ok = lo.decode(code, llr, it)
+        np.testing.assert_array_equal(ok.cpu().numpy(), ref_ok)
+        np.testing.assert_array_equal(dec.cpu().numpy(), ref_dec)
+    assert 0 < ref_ok.sum() < 70
+    g.close()
+
+
 @pytest.mark.parametrize("e,rate", [(1152, 553 / 1024), (900, 0.33), (3276 * 12 * 4, 553 / 1024)])
 def test_encoder_matches_oracle_and_round_trips(e, rate):
     torch = _t()
