@@ -13,12 +13,13 @@
 // Codewords are decoded 32 at a time, interleaved: lane l of every warp
 // works on codeword l of its group, so the random gathers of the Tanner
 // graph move 128 contiguous bytes (one value per codeword) instead of a
-// 32-byte sector per 4-byte value.  Per iteration three launches (grid.y =
-// group): k_ldpc_var (warp per variable: totals + hard bits), k_ldpc_check
+// 32-byte sector per 4-byte value.  Per iteration two launches (grid.y =
+// group): k_ldpc_var (warp per variable: totals + hard bits) and k_ldpc_check
 // (warp per check: syndrome, then min-sum messages from two passes over the
-// row) and k_ldpc_flag (a codeword whose checks are all satisfied freezes:
-// its lane is skipped from then on, exactly the reference's per-codeword
-// early exit; a group with all lanes done returns at once).  A final
+// row; the lanes with an unsatisfied check OR-ed into a per-group mask).  The
+// next variable pass marks the codewords whose checks were all satisfied as
+// done: a done lane is skipped from then on, exactly the reference's
+// per-codeword early exit, and a group with all lanes done returns at once.  A final
 // variable pass gives the hard bits of codewords that never converged (the
 // reference's for-else branch).
 //
@@ -66,8 +67,11 @@ struct DecWs {
   float* total;     // [G][n][32]
   float* c2v;       // [G][m][dmax][32]
   uint32_t* done;   // [G] lane mask of finished codewords
-  uint32_t* unsat;  // [G][check blocks] lane mask with an unsatisfied check
+  uint32_t* unsat;  // [2][G][32] lanes with an unsatisfied check, by iteration parity,
+                    // OR-ed by the check blocks into 32 slots (blockIdx.x % 32)
 };
+
+constexpr int kUnsatSlots = 32;     // spread of the check blocks' unsatisfied-lane atomics
 
 size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
@@ -86,7 +90,7 @@ DecWs dec_layout(const nrx_ldpc_code& c, int n_cw, uint8_t* base, size_t* total_
   const size_t o_total = take(sizeof(float) * c.n * kLanes * G);
   const size_t o_c2v = take(sizeof(float) * (size_t)c.m * c.dmax * kLanes * G);
   const size_t o_done = take(sizeof(uint32_t) * G);
-  const size_t o_unsat = take(sizeof(uint32_t) * check_blocks(c) * G);
+  const size_t o_unsat = take(sizeof(uint32_t) * 2 * G * kUnsatSlots);
   if (total_bytes) *total_bytes = off;
   if (base) {
     w.chan = reinterpret_cast<float*>(base + o_chan);
@@ -120,20 +124,20 @@ EncWs enc_layout(const nrx_ldpc_code& c, int n_cw, uint8_t* base, size_t* total_
 // decoder kernels (grid.y = group of 32 codewords)
 // ---------------------------------------------------------------------------
 
+// Channel values only: the zero initial messages are never stored, the
+// first iteration's kernels take them as zero (`first_pass`).
 __global__ void k_ldpc_init(nrx_ldpc_code c, const float* llr, int n_cw, DecWs w) {
   const int g = blockIdx.y;
-  const size_t ne = (size_t)c.m * c.dmax * kLanes, nv = (size_t)c.n * kLanes;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ne || i < nv;
-       i += (size_t)gridDim.x * blockDim.x) {
-    if (i < nv) {
-      const int j = (int)(i / kLanes), cw = g * kLanes + (int)(i % kLanes);
-      const int src = c.chan_src[j];
-      float v = 0.f;   // ln(p0/p1) convention: the channel value is the negated logit LLR
-      if (cw < n_cw) v = src >= 0 ? -llr[(size_t)cw * c.ntx + src] : (src == -2 ? kShortenedLlr : 0.f);
-      w.chan[(size_t)g * nv + i] = v;
-    }
-    if (i < ne) w.c2v[(size_t)g * ne + i] = 0.f;
+  const size_t nv = (size_t)c.n * kLanes;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nv; i += (size_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i / kLanes), cw = g * kLanes + (int)(i % kLanes);
+    const int src = __ldg(c.chan_src + j);
+    float v = 0.f;   // ln(p0/p1) convention: the channel value is the negated logit LLR
+    if (cw < n_cw) v = src >= 0 ? -llr[(size_t)cw * c.ntx + src] : (src == -2 ? kShortenedLlr : 0.f);
+    w.chan[(size_t)g * nv + i] = v;
   }
+  if (blockIdx.x == 0 && threadIdx.x < kUnsatSlots)   // "iteration -1": no lane newly satisfied
+    w.unsat[((size_t)gridDim.y + g) * kUnsatSlots + threadIdx.x] = 0xffffffffu;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const int valid = min(kLanes, n_cw - g * kLanes);
     w.done[g] = valid >= kLanes ? 0u : ~((1u << valid) - 1u);   // absent codewords count as done
@@ -144,11 +148,23 @@ __global__ void k_ldpc_init(nrx_ldpc_code c, const float* llr, int n_cw, DecWs w
 // message gathers all issued before use): total = chan + ((c2v_0 + c2v_1) + c2v_2).
 // The hard bits are the signs of the totals; a converged lane's totals stay
 // frozen, so they are its decision.
-__global__ void __launch_bounds__(kWarps * 32) k_ldpc_var(nrx_ldpc_code c, DecWs w) {
+//
+// Early exit: a codeword whose checks were all satisfied by the previous
+// check pass's hard bits (parity `1 - par` of w.unsat) is done from now on;
+// block 0 records the new mask and clears parity `par` for this iteration's
+// check pass.  FIRST: the messages are still all zero (not read).
+template <bool FIRST>
+__global__ void __launch_bounds__(kWarps * 32) k_ldpc_var(nrx_ldpc_code c, DecWs w, int par) {
   const int g = blockIdx.y;
-  const uint32_t done = w.done[g];
-  if (done == 0xffffffffu) return;
   const int lane = threadIdx.x & 31;
+  const uint32_t unsat =
+      __reduce_or_sync(0xffffffffu, w.unsat[((size_t)(par ^ 1) * gridDim.y + g) * kUnsatSlots + lane]);
+  const uint32_t done = w.done[g] | ~unsat;
+  if (blockIdx.x == 0 && threadIdx.x < kUnsatSlots) {
+    w.unsat[((size_t)par * gridDim.y + g) * kUnsatSlots + lane] = 0u;
+    if (lane == 0) w.done[g] = done;
+  }
+  if (done == 0xffffffffu) return;
   if ((done >> lane) & 1u) return;
   const int j0 = (blockIdx.x * kWarps + (threadIdx.x >> 5)) * kVarsPerWarp;
   const float* c2v = w.c2v + (size_t)g * c.m * c.dmax * kLanes + lane;
@@ -162,7 +178,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_ldpc_var(nrx_ldpc_code c, DecWs
     const int e3[3] = {ed[q].x, ed[q].y, ed[q].z};
 #pragma unroll
     for (int t = 0; t < 3; ++t)
-      v[q][t] = e3[t] >= 0 ? c2v[((size_t)(e3[t] >> 8) * c.dmax + (e3[t] & 255)) * kLanes] : 0.f;
+      v[q][t] = !FIRST && e3[t] >= 0 ? c2v[((size_t)(e3[t] >> 8) * c.dmax + (e3[t] & 255)) * kLanes] : 0.f;
     ch[q] = j0 + q < c.n ? w.chan[((size_t)g * c.n + j0 + q) * kLanes + lane] : 0.f;
   }
 #pragma unroll
@@ -179,8 +195,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_ldpc_var(nrx_ldpc_code c, DecWs
 // Check update, warp per check: v2c of every slot kept in registers between
 // the min-sum pass and the message write; plus the lanes whose hard bits
 // violate this check.  DMAX > 0: row width fixed at compile time.
-template <int DMAX>
-__global__ void __launch_bounds__(kWarps * 32) k_ldpc_check(nrx_ldpc_code c, DecWs w) {
+template <int DMAX, bool FIRST>
+__global__ void __launch_bounds__(kWarps * 32) k_ldpc_check(nrx_ldpc_code c, DecWs w, int par) {
   __shared__ uint32_t block_unsat;
   const int g = blockIdx.y;
   const uint32_t done = w.done[g];
@@ -209,7 +225,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_ldpc_check(nrx_ldpc_code c, Dec
       if (col >= 0) {
         const float v = tot[(size_t)col * kLanes];
         syn ^= v < 0.f ? 1 : 0;
-        x = __fsub_rn(v, msg[s * kLanes]);
+        x = FIRST ? v : __fsub_rn(v, msg[s * kLanes]);
         mag = fabsf(x);
         neg ^= x < 0.f ? 1 : 0;
       }
@@ -236,7 +252,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_ldpc_check(nrx_ldpc_code c, Dec
         msg[s * kLanes] = 0.f;
         continue;
       }
-      const float x = DMAX > 0 ? xs[s] : __fsub_rn(tot[(size_t)col * kLanes], msg[s * kLanes]);
+      const float x = DMAX > 0 ? xs[s] : FIRST ? tot[(size_t)col * kLanes]
+                                                : __fsub_rn(tot[(size_t)col * kLanes], msg[s * kLanes]);
       const float sg = x < 0.f ? -1.f : 1.f;
       msg[s * kLanes] = __fmul_rn(rs * sg, s == amin ? min2 : min1);
     }
@@ -244,32 +261,31 @@ __global__ void __launch_bounds__(kWarps * 32) k_ldpc_check(nrx_ldpc_code c, Dec
   const uint32_t bal = __ballot_sync(0xffffffffu, syn);
   if (lane == 0 && bal) atomicOr(&block_unsat, bal);
   __syncthreads();
-  if (threadIdx.x == 0) w.unsat[(size_t)g * gridDim.x + blockIdx.x] = block_unsat;
+  if (threadIdx.x == 0 && block_unsat)
+    atomicOr(w.unsat + ((size_t)par * gridDim.y + g) * kUnsatSlots + blockIdx.x % kUnsatSlots, block_unsat);
 }
 
-// A codeword whose checks were all satisfied by this iteration's hard bits is done.
-__global__ void k_ldpc_flag(DecWs w, int nblk) {
-  __shared__ uint32_t acc;
-  const int g = blockIdx.x;
-  const uint32_t done = w.done[g];
-  if (done == 0xffffffffu) return;
-  if (threadIdx.x == 0) acc = 0u;
-  __syncthreads();
-  uint32_t v = 0u;
-  for (int i = threadIdx.x; i < nblk; i += blockDim.x) v |= w.unsat[(size_t)g * nblk + i];
-  v = __reduce_or_sync(0xffffffffu, v);
-  if ((threadIdx.x & 31) == 0 && v) atomicOr(&acc, v);
-  __syncthreads();
-  if (threadIdx.x == 0) w.done[g] = done | ~acc;
-}
+// Hard decisions of the kept information bits, transposed through shared
+// memory: gathered lane-per-codeword (128 B per position), written
+// codeword-major with consecutive threads on consecutive bytes.
+constexpr int kExtractTile = 256;
 
-__global__ void k_ldpc_extract(nrx_ldpc_code c, DecWs w, uint8_t* info, uint8_t* success, int n_cw) {
+__global__ void __launch_bounds__(kWarps * 32) k_ldpc_extract(nrx_ldpc_code c, DecWs w, uint8_t* info,
+                                                            uint8_t* success, int n_cw) {
+  __shared__ uint8_t bits[kLanes][kExtractTile + 4];
   const int g = blockIdx.y;
-  const int lane = threadIdx.x & 31, cw = g * kLanes + lane;
-  if (cw >= n_cw) return;
-  for (int i = blockIdx.x * kWarps + (threadIdx.x >> 5); i < c.k_eff; i += gridDim.x * kWarps)
-    info[(size_t)cw * c.k_eff + i] = w.total[((size_t)g * c.n + c.keep_pos[i]) * kLanes + lane] < 0.f ? 1 : 0;
-  if (blockIdx.x == 0 && threadIdx.x < 32) success[cw] = static_cast<uint8_t>((w.done[g] >> lane) & 1u);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int base = blockIdx.x * kExtractTile;
+  const float* tot = w.total + (size_t)g * c.n * kLanes + lane;
+  for (int i = warp; i < kExtractTile; i += kWarps)
+    if (base + i < c.k_eff) bits[lane][i] = tot[(size_t)__ldg(c.keep_pos + base + i) * kLanes] < 0.f ? 1 : 0;
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < kLanes * kExtractTile; idx += kWarps * 32) {
+    const int l = idx / kExtractTile, i = idx % kExtractTile, cw = g * kLanes + l;
+    if (cw < n_cw && base + i < c.k_eff) info[(size_t)cw * c.k_eff + base + i] = bits[l][i];
+  }
+  const int cw = g * kLanes + lane;
+  if (blockIdx.x == 0 && threadIdx.x < 32 && cw < n_cw) success[cw] = static_cast<uint8_t>((w.done[g] >> lane) & 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -557,17 +573,22 @@ extern "C" int nrx_ldpc_decode(const nrx_ldpc_code* c, int n_cw, const float* ll
   const DecWs w = dec_layout(*c, n_cw, static_cast<uint8_t*>(ws), nullptr);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int vb = (c->n + kWarps * kVarsPerWarp - 1) / (kWarps * kVarsPerWarp), cb = check_blocks(*c);
-  auto check_fn = c->dmax == 5 ? k_ldpc_check<5> : c->dmax == 6 ? k_ldpc_check<6> : c->dmax == 7 ? k_ldpc_check<7>
-                : c->dmax == 8 ? k_ldpc_check<8> : k_ldpc_check<0>;
+  auto check_fn = [&](bool first) {
+    return first ? (c->dmax == 5 ? k_ldpc_check<5, true> : c->dmax == 6 ? k_ldpc_check<6, true>
+                  : c->dmax == 7 ? k_ldpc_check<7, true> : c->dmax == 8 ? k_ldpc_check<8, true> : k_ldpc_check<0, true>)
+                 : (c->dmax == 5 ? k_ldpc_check<5, false> : c->dmax == 6 ? k_ldpc_check<6, false>
+                  : c->dmax == 7 ? k_ldpc_check<7, false> : c->dmax == 8 ? k_ldpc_check<8, false> : k_ldpc_check<0, false>);
+  };
   k_ldpc_init<<<dim3(512, G), 256, 0, st>>>(*c, llr, n_cw, w);
   for (int it = 0; it < iterations; ++it) {
-    k_ldpc_var<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w);
-    check_fn<<<dim3(cb, G), kWarps * 32, 0, st>>>(*c, w);
-    k_ldpc_flag<<<G, 256, 0, st>>>(w, cb);
+    (it == 0 ? k_ldpc_var<true> : k_ldpc_var<false>)<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w, it & 1);
+    check_fn(it == 0)<<<dim3(cb, G), kWarps * 32, 0, st>>>(*c, w, it & 1);
   }
   // codewords that never satisfied every check: totals of the final messages
-  k_ldpc_var<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w);
-  k_ldpc_extract<<<dim3(256, G), kWarps * 32, 0, st>>>(*c, w, info_out, success, n_cw);
+  (iterations == 0 ? k_ldpc_var<true> : k_ldpc_var<false>)<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w,
+                                                                                               iterations & 1);
+  k_ldpc_extract<<<dim3((c->k_eff + kExtractTile - 1) / kExtractTile, G), kWarps * 32, 0, st>>>(
+      *c, w, info_out, success, n_cw);
   return launch_status();
 }
 
