@@ -45,6 +45,8 @@ struct nrx_ldpc_code {
   int32_t* chan_src;   // (n): transmitted index, -1 punctured, -2 shortened
   int32_t* keep_pos;   // (k_eff): mother positions of the kept info bits
   int32_t* tx_pos;     // (ntx)
+  int32_t* skip_pos;   // (n_skip): punctured and shortened positions, or null
+  int n_skip;
   int32_t* info_slot;  // (n): payload index of an info position, -1 shortened, -2 parity
   int32_t* chain_cols; // (m) or null
   int4* edges;         // (n): the column's checks as (row << 8 | slot), -1 padded
@@ -125,16 +127,40 @@ EncWs enc_layout(const nrx_ldpc_code& c, int n_cw, uint8_t* base, size_t* total_
 // ---------------------------------------------------------------------------
 
 // Channel values only: the zero initial messages are never stored, the
-// first iteration's kernels take them as zero (`first_pass`).
-__global__ void k_ldpc_init(nrx_ldpc_code c, const float* llr, int n_cw, DecWs w) {
+// first iteration's kernels take them as zero (`first_pass`).  The received
+// LLRs are transposed through shared memory: read codeword-major (coalesced
+// along the transmitted index), written lane-per-codeword at their mother
+// positions (128 B per position).
+constexpr int kInitTile = 256;
+
+__global__ void __launch_bounds__(kWarps * 32) k_ldpc_init_tx(nrx_ldpc_code c, const float* llr, int n_cw, DecWs w) {
+  __shared__ float tile[kLanes][kInitTile + 1];
   const int g = blockIdx.y;
-  const size_t nv = (size_t)c.n * kLanes;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nv; i += (size_t)gridDim.x * blockDim.x) {
-    const int j = (int)(i / kLanes), cw = g * kLanes + (int)(i % kLanes);
-    const int src = __ldg(c.chan_src + j);
-    float v = 0.f;   // ln(p0/p1) convention: the channel value is the negated logit LLR
-    if (cw < n_cw) v = src >= 0 ? -llr[(size_t)cw * c.ntx + src] : (src == -2 ? kShortenedLlr : 0.f);
-    w.chan[(size_t)g * nv + i] = v;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int base = blockIdx.x * kInitTile;
+  for (int l = warp; l < kLanes; l += kWarps) {
+    const int cw = g * kLanes + l;
+    const float* row = llr + (size_t)cw * c.ntx + base;
+#pragma unroll
+    for (int i = lane; i < kInitTile; i += 32)
+      tile[l][i] = cw < n_cw && base + i < c.ntx ? row[i] : 0.f;
+  }
+  __syncthreads();
+  float* chan = w.chan + (size_t)g * c.n * kLanes + lane;
+  for (int i = warp; i < kInitTile && base + i < c.ntx; i += kWarps)   // ln(p0/p1): the negated logit LLR
+    chan[(size_t)__ldg(c.tx_pos + base + i) * kLanes] = g * kLanes + lane < n_cw ? -tile[lane][i] : 0.f;
+}
+
+// Positions that are not transmitted (punctured: erased, shortened: known
+// zero) and the group's early-exit state.
+__global__ void k_ldpc_init_state(nrx_ldpc_code c, int n_cw, DecWs w) {
+  const int g = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const bool live = g * kLanes + lane < n_cw;
+  float* chan = w.chan + (size_t)g * c.n * kLanes + lane;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < c.n_skip; i += (gridDim.x * blockDim.x) >> 5) {
+    const int j = __ldg(c.skip_pos + i);
+    chan[(size_t)j * kLanes] = live && __ldg(c.chan_src + j) == -2 ? kShortenedLlr : 0.f;
   }
   if (blockIdx.x == 0 && threadIdx.x < kUnsatSlots)   // "iteration -1": no lane newly satisfied
     w.unsat[((size_t)gridDim.y + g) * kUnsatSlots + threadIdx.x] = 0xffffffffu;
@@ -511,6 +537,11 @@ extern "C" int nrx_ldpc_create(const nrx_ldpc_desc* d, nrx_ldpc_code** out) {
   rc = rc ? rc : upload(&c->chan_src, chan_src);
   rc = rc ? rc : upload(&c->keep_pos, keep_pos);
   rc = rc ? rc : upload(&c->tx_pos, tx_pos);
+  std::vector<int32_t> skip_pos;
+  for (int j = 0; j < n; ++j)
+    if (skip[j]) skip_pos.push_back(j);
+  c->n_skip = static_cast<int>(skip_pos.size());
+  rc = rc ? rc : upload(&c->skip_pos, skip_pos);
   rc = rc ? rc : upload(&c->info_slot, info_slot);
   if (!rc && d->chain_cols) rc = upload(&c->chain_cols, std::vector<int32_t>(d->chain_cols, d->chain_cols + m));
   if (!rc) {
@@ -536,7 +567,7 @@ extern "C" int nrx_ldpc_create(const nrx_ldpc_desc* d, nrx_ldpc_code** out) {
 
 extern "C" void nrx_ldpc_destroy(nrx_ldpc_code* c) {
   if (!c) return;
-  int32_t* ptrs[] = {c->row_cols, c->col_rows, c->col_slots, c->chan_src, c->keep_pos, c->tx_pos,
+  int32_t* ptrs[] = {c->row_cols, c->col_rows, c->col_slots, c->chan_src, c->keep_pos, c->tx_pos, c->skip_pos,
                      c->info_slot, c->chain_cols};
   for (int32_t* p : ptrs)
     if (p) cudaFree(p);
@@ -579,7 +610,9 @@ extern "C" int nrx_ldpc_decode(const nrx_ldpc_code* c, int n_cw, const float* ll
                  : (c->dmax == 5 ? k_ldpc_check<5, false> : c->dmax == 6 ? k_ldpc_check<6, false>
                   : c->dmax == 7 ? k_ldpc_check<7, false> : c->dmax == 8 ? k_ldpc_check<8, false> : k_ldpc_check<0, false>);
   };
-  k_ldpc_init<<<dim3(512, G), 256, 0, st>>>(*c, llr, n_cw, w);
+  k_ldpc_init_tx<<<dim3((c->ntx + kInitTile - 1) / kInitTile, G), kWarps * 32, 0, st>>>(*c, llr, n_cw, w);
+  k_ldpc_init_state<<<dim3(std::max(1, std::min(256, (c->n_skip + kWarps - 1) / kWarps)), G), kWarps * 32, 0, st>>>(
+      *c, n_cw, w);
   for (int it = 0; it < iterations; ++it) {
     (it == 0 ? k_ldpc_var<true> : k_ldpc_var<false>)<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w, it & 1);
     check_fn(it == 0)<<<dim3(cb, G), kWarps * 32, 0, st>>>(*c, w, it & 1);
