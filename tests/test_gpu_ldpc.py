@@ -76,6 +76,54 @@ def test_decoder_multi_group_ragged_vs_oracle():
     g.close()
 
 
+def _regular_code(n, m, seed):
+    """Column weight 3, row weight 3n/m (socket permutation, no repeated
+    check in a column), first n - m positions as information, a few
+    punctured / shortened positions: exercises the decoder's row widths other
+    than the IRA codes' 5 and the reference codes' 6."""
+    from paper_2409_02912_b200.ldpc import LdpcCode
+    rng = np.random.default_rng(seed)
+    dr = 3 * n // m
+    while True:
+        sockets = rng.permutation(np.repeat(np.arange(m), dr))[: 3 * n].reshape(n, 3)
+        if all(len(set(r)) == 3 for r in sockets):
+            break
+    row_cols = np.full((m, dr), -1, dtype=np.int32)
+    col_slots = np.zeros((n, 3), dtype=np.int32)
+    fill = np.zeros(m, dtype=np.int64)
+    for j in range(n):
+        for t in range(3):
+            r = sockets[j, t]
+            row_cols[r, fill[r]] = j
+            col_slots[j, t] = fill[r]
+            fill[r] += 1
+    k = n - m
+    return LdpcCode(n, k, row_cols, sockets.astype(np.int32), col_slots, np.arange(k),
+                    punctured=np.array([n - 1, n - 2]), shortened=np.array([0, 3]))
+
+
+@pytest.mark.parametrize("n,m", [(700, 300), (640, 240), (900, 300)])
+def test_decoder_other_row_widths_vs_oracle(n, m):
+    """Row widths 7, 8 (fixed-width check kernels) and 9 (generic): all-zero
+    codeword over AWGN at noise levels across the waterfall, 40 codewords."""
+    torch = _t()
+    from paper_2409_02912_b200.ldpc import GpuLdpc
+    code = _regular_code(n, m, seed=n + m)
+    rng = np.random.default_rng(7)
+    ntx = code.num_tx_bits
+    sig = np.linspace(0.4, 1.0, 40)[:, None]
+    llr = np.clip(2 * (-1 + sig * rng.normal(size=(40, ntx))) / sig ** 2, -20, 20).astype(np.float32)
+    g = GpuLdpc(code)
+    for it in (20, 2):
+        dec, ok = g.decode(torch.from_numpy(llr).cuda(), it)
+        ref_dec, ref_ok = lo.decode(code, llr, it)
+        np.testing.assert_array_equal(ok.cpu().numpy(), ref_ok)
+        np.testing.assert_array_equal(dec.cpu().numpy(), ref_dec)
+        if it == 20:
+            assert 0 < ref_ok.sum() < 40
+    g.close()
+
+
 @pytest.mark.parametrize("e,rate", [(1152, 553 / 1024), (900, 0.33), (3276 * 12 * 4, 553 / 1024)])
 def test_encoder_matches_oracle_and_round_trips(e, rate):
     torch = _t()
