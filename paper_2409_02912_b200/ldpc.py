@@ -297,8 +297,21 @@ def evaluate_coded(engine, source, mcs_per_ue, snr_db_grid, n_slots: int, batch:
     lib = _lib.load()
     sdesc = _lib.slot_desc(cfg)
     orders = [m.modulation_order for m in mcs_per_ue]
-    codes = codes or [slot_code(cfg, m) for m in mcs_per_ue]
-    dec = [GpuLdpc(c, source.device) for c in codes]
+    if not codes:
+        built = {}                                # one code per distinct MCS
+        for m in mcs_per_ue:
+            if (m.modulation_order, m.code_rate) not in built:
+                built[(m.modulation_order, m.code_rate)] = slot_code(cfg, m)
+        codes = [built[(m.modulation_order, m.code_rate)] for m in mcs_per_ue]
+    groups, dec_of = [], {}                       # UEs sharing a code object share a decoder
+    for u, c in enumerate(codes):
+        if id(c) in dec_of:
+            groups[dec_of[id(c)]].append(u)
+        else:
+            dec_of[id(c)] = len(groups)
+            groups.append([u])
+    shared = [GpuLdpc(codes[g[0]], source.device) for g in groups]
+    dec = [shared[dec_of[id(c)]] for c in codes]
     n_it = num_iterations or engine.config.num_iterations
     width = engine.config.m_max if engine.config.variant != "var_io" else max(orders)
     mine = shard_slots(n_slots, rank, world)
@@ -335,14 +348,20 @@ def evaluate_coded(engine, source, mcs_per_ue, snr_db_grid, n_slots: int, batch:
                 extra["h_eff"] = sb.h_eff
             engine.forward_device(cfg, sb.y, sb.pilots, nf[:nb], sb.mod_order, n_it, llr[:nb], chest[:nb], **extra)
             errs.zero_()
-            for u, d in enumerate(dec):
-                cw_llr = torch.empty((nb, d.num_tx_bits), dtype=torch.float32, device=dev)
-                _lib.check(lib.nrx_extract_llrs(ctypes.byref(sdesc), nb, u, orders[u], llr.data_ptr(), width,
-                                                float(llr_clip), cw_llr.data_ptr(), st.cuda_stream),
-                           "nrx_extract_llrs")
-                info_hat, _ = d.decode(cw_llr, decoder_iterations)
-                _lib.check(lib.nrx_count_mismatches(nb, d.k_eff, info_hat.data_ptr(), payload[u].data_ptr(),
-                                                    errs[u].data_ptr(), st.cuda_stream), "nrx_count_mismatches")
+            # UEs that share a code are decoded in one call (their 32-codeword
+            # groups run concurrently); results are per codeword either way.
+            for users in groups:
+                d = dec[users[0]]
+                cw_llr = torch.empty((len(users), nb, d.num_tx_bits), dtype=torch.float32, device=dev)
+                for i, u in enumerate(users):
+                    _lib.check(lib.nrx_extract_llrs(ctypes.byref(sdesc), nb, u, orders[u], llr.data_ptr(), width,
+                                                    float(llr_clip), cw_llr[i].data_ptr(), st.cuda_stream),
+                               "nrx_extract_llrs")
+                info_hat, _ = d.decode(cw_llr.view(len(users) * nb, d.num_tx_bits), decoder_iterations)
+                for i, u in enumerate(users):
+                    _lib.check(lib.nrx_count_mismatches(nb, d.k_eff, info_hat[i * nb:(i + 1) * nb].data_ptr(),
+                                                        payload[u].data_ptr(), errs[u].data_ptr(), st.cuda_stream),
+                               "nrx_count_mismatches")
             e = errs[:, :nb]
             tot += torch.stack([(e > 0).sum(), e.sum()])
         blocks = len(mine) * U
@@ -353,7 +372,7 @@ def evaluate_coded(engine, source, mcs_per_ue, snr_db_grid, n_slots: int, batch:
             c = reduce(c)
         c = [int(x) for x in c.cpu()]
         records.append(MetricsRecord(receiver, float(snr_db), c[0], c[1], c[2], c[3]))
-    for d in dec:
+    for d in shared:
         d.close()
     return records
 

@@ -24,7 +24,11 @@ from paper_2409_02912_b200.slotgen import GpuSlotSource  # noqa: E402
 
 def sweep(label, cfg, mcs, receivers, snrs, n_slots, batch):
     src = GpuSlotSource(cfg)
-    codes = [slot_code(cfg, m) for m in mcs]
+    built = {}                                   # UEs with the same MCS share one code (and one decode call)
+    for m in mcs:
+        if (m.modulation_order, m.code_rate) not in built:
+            built[(m.modulation_order, m.code_rate)] = slot_code(cfg, m)
+    codes = [built[(m.modulation_order, m.code_rate)] for m in mcs]
     out = {"config": label, "num_subcarriers": cfg.num_subcarriers, "ues": cfg.num_ues,
            "mcs": [(m.index, m.modulation_order, round(m.code_rate, 4)) for m in mcs],
            "codeword_bits": codes[0].num_tx_bits, "payload_bits": codes[0].k_eff, "slots_per_point": n_slots,
