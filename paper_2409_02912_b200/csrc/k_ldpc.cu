@@ -14,14 +14,14 @@
 // works on codeword l of its group, so the random gathers of the Tanner
 // graph move 128 contiguous bytes (one value per codeword) instead of a
 // 32-byte sector per 4-byte value.  Per iteration two launches (grid.y =
-// group): k_ldpc_var (warp per variable: totals + hard bits) and k_ldpc_check
-// (warp per check: syndrome, then min-sum messages from two passes over the
-// row; the lanes with an unsatisfied check OR-ed into a per-group mask).  The
-// next variable pass marks the codewords whose checks were all satisfied as
-// done: a done lane is skipped from then on, exactly the reference's
-// per-codeword early exit, and a group with all lanes done returns at once.  A final
-// variable pass gives the hard bits of codewords that never converged (the
-// reference's for-else branch).
+// group): k_ldpc_var (four variables per warp: totals + hard bits) and
+// k_ldpc_check_rows / k_ldpc_check (two rows per warp for row widths 5 and 6,
+// else one: syndrome, then min-sum messages; the lanes with an unsatisfied
+// check OR-ed into a per-group mask).  The next variable pass marks the
+// codewords whose checks were all satisfied as done: a done lane is skipped
+// from then on, exactly the reference's per-codeword early exit, and a group
+// with all lanes done returns at once.  A final variable pass gives the hard
+// bits of codewords that never converged (the reference's for-else branch).
 //
 // Encoder (codes with a staircase parity part): information bits placed,
 // per-check information syndromes s_i, then the Z interleaved accumulator
@@ -125,7 +125,7 @@ EncWs enc_layout(const nrx_ldpc_code& c, int n_cw, uint8_t* base, size_t* total_
 // ---------------------------------------------------------------------------
 
 // Channel values only: the zero initial messages are never stored, the
-// first iteration's kernels take them as zero (`first_pass`).  The received
+// first iteration's kernels take them as zero (template flag FIRST).  The received
 // LLRs are transposed through shared memory: read codeword-major (coalesced
 // along the transmitted index), written lane-per-codeword at their mother
 // positions (128 B per position).
@@ -683,13 +683,13 @@ extern "C" int nrx_ldpc_decode(const nrx_ldpc_code* c, int n_cw, const float* ll
     return first ? (c->dmax == 7 ? k_ldpc_check<7, true> : c->dmax == 8 ? k_ldpc_check<8, true> : k_ldpc_check<0, true>)
                  : (c->dmax == 7 ? k_ldpc_check<7, false> : c->dmax == 8 ? k_ldpc_check<8, false> : k_ldpc_check<0, false>);
   };
-  const int cbk = (c->m + kWarps * kc - 1) / (kWarps * kc);
+  const int cb = (c->m + kWarps * kc - 1) / (kWarps * kc);
   k_ldpc_init_tx<<<dim3((c->ntx + kInitTile - 1) / kInitTile, G), kWarps * 32, 0, st>>>(*c, llr, n_cw, w);
   k_ldpc_init_state<<<dim3(std::max(1, std::min(256, (c->n_skip + kWarps - 1) / kWarps)), G), kWarps * 32, 0, st>>>(
       *c, n_cw, w);
   for (int it = 0; it < iterations; ++it) {
     (it == 0 ? k_ldpc_var<true> : k_ldpc_var<false>)<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w, it & 1);
-    check_fn(it == 0)<<<dim3(cbk, G), kWarps * 32, 0, st>>>(*c, w, it & 1);
+    check_fn(it == 0)<<<dim3(cb, G), kWarps * 32, 0, st>>>(*c, w, it & 1);
   }
   // codewords that never satisfied every check: totals of the final messages
   (iterations == 0 ? k_ldpc_var<true> : k_ldpc_var<false>)<<<dim3(vb, G), kWarps * 32, 0, st>>>(*c, w,
