@@ -49,7 +49,7 @@ struct nrx_ldpc_code {
   int n_skip;
   int32_t* info_slot;  // (n): payload index of an info position, -1 shortened, -2 parity
   int32_t* chain_cols; // (m) or null
-  int4* edges;         // (n): the column's checks as (row << 8 | slot), -1 padded
+  int4* edges;         // (n): the column's messages as row * dmax + slot, -1 padded
 };
 
 namespace nrx_ldpc {
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_ldpc_var(nrx_ldpc_code c, DecWs
     const int e3[3] = {ed[q].x, ed[q].y, ed[q].z};
 #pragma unroll
     for (int t = 0; t < 3; ++t)
-      v[q][t] = !FIRST && e3[t] >= 0 ? c2v[((size_t)(e3[t] >> 8) * c.dmax + (e3[t] & 255)) * kLanes] : 0.f;
+      v[q][t] = !FIRST && e3[t] >= 0 ? c2v[(size_t)e3[t] * kLanes] : 0.f;
     ch[q] = j0 + q < c.n ? w.chan[((size_t)g * c.n + j0 + q) * kLanes + lane] : 0.f;
   }
 #pragma unroll
@@ -538,8 +538,8 @@ extern "C" int nrx_ldpc_create(const nrx_ldpc_desc* d, nrx_ldpc_code** out) {
   if (!d || !out) return NRX_ERR_INVALID;
   *out = nullptr;
   if (d->n < 2 || d->m < 1 || d->k < 1 || d->k >= d->n || d->dmax < 1 || d->cdeg < 1) return NRX_ERR_INVALID;
-  if (d->cdeg > NRX_LDPC_MAX_COL_DEG || d->dmax > NRX_LDPC_MAX_ROW_DEG || d->m >= (1 << 23))
-    return NRX_ERR_UNSUPPORTED;   // edge records pack (row << 8 | slot) into an int32
+  if (d->cdeg > NRX_LDPC_MAX_COL_DEG || d->dmax > NRX_LDPC_MAX_ROW_DEG || (int64_t)d->m * d->dmax >= (int64_t)1 << 31)
+    return NRX_ERR_UNSUPPORTED;   // edge records hold the message index in an int32
   if (!d->row_cols || !d->col_rows || !d->col_slots || !d->info_positions) return NRX_ERR_INVALID;
   if (d->n_punctured < 0 || d->n_shortened < 0 || (d->n_punctured && !d->punctured) ||
       (d->n_shortened && !d->shortened))
@@ -621,7 +621,7 @@ extern "C" int nrx_ldpc_create(const nrx_ldpc_desc* d, nrx_ldpc_code** out) {
       for (int t = 0; t < d->cdeg && t < 3; ++t) {
         const int r = d->col_rows[(size_t)j * d->cdeg + t];
         if (r < 0) break;
-        e[t] = (r << 8) | d->col_slots[(size_t)j * d->cdeg + t];
+        e[t] = r * d->dmax + d->col_slots[(size_t)j * d->cdeg + t];
       }
       edges[j] = make_int4(e[0], e[1], e[2], -1);
     }
