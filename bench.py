@@ -74,28 +74,43 @@ class ClockSampler:
         self.period_ms = period_ms
         self.samples = []
         self._proc = None
+        self._lines = []
+        self._start = 0
+
+    def _read(self):
+        for line in self._proc.stdout:
+            if line.strip():
+                self._lines.append(line)
 
     def __enter__(self):
-        # one long-running nvidia-smi polling at period_ms (spawning per sample is too slow)
+        # one long-running nvidia-smi polling at period_ms (spawning per sample is too slow);
+        # the timed region starts once its first sample has arrived, and only the samples
+        # taken from then until the region ends are kept
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
                  "-lms", str(self.period_ms)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self._proc = None
-        time.sleep(0.3)  # let the first samples arrive before the timed region starts
+        t0 = time.time()
+        while self._proc is not None and not self._lines and time.time() - t0 < 10:
+            time.sleep(0.01)
+        self._start = len(self._lines)
         return self
 
     def __exit__(self, *exc):
         if self._proc is not None:
-            time.sleep(0.1)
+            t0 = time.time()   # a region shorter than one period still gets the next sample
+            while len(self._lines) <= self._start and time.time() - t0 < 2:
+                time.sleep(0.01)
+            lines = self._lines[self._start:]
             self._proc.terminate()
             try:
-                out, _ = self._proc.communicate(timeout=5)
+                self._proc.wait(timeout=5)
             except Exception:
                 self._proc.kill()
-                out = ""
-            self.samples = [[x.strip() for x in line.split(",")] for line in out.splitlines() if line.strip()]
+            self.samples = [[x.strip() for x in line.split(",")] for line in lines]
         return False
 
     def summary(self):
