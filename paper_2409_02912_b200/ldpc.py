@@ -332,15 +332,19 @@ def evaluate_coded(engine, source, mcs_per_ue, snr_db_grid, n_slots: int, batch:
         key = (int(seed) << 20) + (k << 4)
         for start in range(mine.start, mine.stop, cap):
             nb = min(cap, mine.stop - start)
-            payload = []
-            for u, d in enumerate(dec):
-                info = torch.empty((nb, d.k_eff), dtype=torch.uint8, device=dev)
-                _lib.check(lib.nrx_random_bits(key + u, start, nb, d.k_eff, info.data_ptr(), st.cuda_stream),
-                           "nrx_random_bits")
-                tx = d.encode(info)
-                _lib.check(lib.nrx_bits_to_labels(ctypes.byref(sdesc), nb, u, orders[u], tx.data_ptr(),
-                                                  labels.data_ptr(), st.cuda_stream), "nrx_bits_to_labels")
-                payload.append(info)
+            payload = [None] * U
+            for users in groups:                  # one encode call per shared code
+                d = dec[users[0]]
+                info = torch.empty((len(users), nb, d.k_eff), dtype=torch.uint8, device=dev)
+                for i, u in enumerate(users):     # payload bits keyed per UE
+                    _lib.check(lib.nrx_random_bits(key + u, start, nb, d.k_eff, info[i].data_ptr(),
+                                                   st.cuda_stream), "nrx_random_bits")
+                    payload[u] = info[i]
+                tx = d.encode(info.view(len(users) * nb, d.k_eff))
+                for i, u in enumerate(users):
+                    _lib.check(lib.nrx_bits_to_labels(ctypes.byref(sdesc), nb, u, orders[u],
+                                                      tx[i * nb:(i + 1) * nb].data_ptr(), labels.data_ptr(),
+                                                      st.cuda_stream), "nrx_bits_to_labels")
             sb = source.generate(nb, mods[: nb * U], n0_t[:nb], seed=key + 15, first_slot=start,
                                  variates={"labels": labels[:nb]}, with_h_eff=getattr(engine, "needs_h_eff", False))
             extra = {"n0": sb.n0} if getattr(engine, "needs_n0", False) else {}
