@@ -64,8 +64,13 @@ typedef enum nrx_precision {
   NRX_FP32 = 0,  /* fp32 SIMT arithmetic, parity mode (<=1e-5 rel. of ref)   */
   NRX_BF16 = 1,  /* bf16 operands on tcgen05 tensor cores, fp32 accumulate,
                     fp32 residual state stream                               */
-  NRX_FP16 = 2   /* fp16 operands on tcgen05, fp32 accumulate, fp16 state
+  NRX_FP16 = 2,  /* fp16 operands on tcgen05, fp32 accumulate, fp16 state
                     (8x finer operand rounding than bf16, no fp32 stream)    */
+  NRX_FP32X3 = 3 /* fp32-grade on tcgen05: every operand split into fp16
+                    hi + lo planes (a = hi + lo 2^-11, 22 significant bits),
+                    each product as lo*W_hi + hi*W_hi + hi*W_lo (three MMAs,
+                    one fp32 TMEM accumulator via scale-input-d), CTA-pair
+                    (cta_group::2) convolutions; parity gate <=1e-5 rel.    */
 } nrx_precision;
 
 /* NrxConfig (nrx.py:37-89). io_orders: var_io -> io_modulations (sorted);

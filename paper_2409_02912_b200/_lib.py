@@ -12,8 +12,10 @@ import os
 
 NRX_MAX_PILOT_SYMBOLS = 16
 NRX_MAX_IO = 4
-NRX_FP32, NRX_BF16, NRX_FP16 = 0, 1, 2
-PRECISIONS = {"fp32": NRX_FP32, "bf16": NRX_BF16, "fp16": NRX_FP16}
+NRX_FP32, NRX_BF16, NRX_FP16, NRX_FP32X3 = 0, 1, 2, 3
+# "fp32": the reference's fp32 accuracy on the tensor cores (fp16 hi/lo operand
+# split, three MMAs per product); "fp32_simt": the same gate on fp32 FFMA.
+PRECISIONS = {"fp32": NRX_FP32X3, "fp32_simt": NRX_FP32, "bf16": NRX_BF16, "fp16": NRX_FP16}
 VARIANT_IDS = {"single": 0, "masking": 1, "var_io": 2}
 
 LIB_PATH = os.environ.get("NRX_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),

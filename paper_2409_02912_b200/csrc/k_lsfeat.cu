@@ -55,7 +55,9 @@ __device__ __forceinline__ double2 cmul_nofma(double2 a, double2 b) {
 
 // BT > 0: the rx antenna count fixed at compile time, so the feature row
 // stays in registers (BT = 0: runtime B, the row lives in local memory).
-template <typename OutT, typename YT, typename PT, int BT>
+// X3: fp32x3 output, every chunk written as its fp16 hi plane (chunks
+// [0, Cf/8)) and lo plane (chunks [Cf/8, 2 Cf/8)).
+template <typename OutT, typename YT, typename PT, int BT, bool X3 = false>
 __global__ void __launch_bounds__(128) k_ls_feat(Geom g, const YT* __restrict__ y, const PT* __restrict__ pilots,
                                                  int n_pilot_sets, const float* __restrict__ noise_feat,
                                                  OutT* __restrict__ feats) {
@@ -120,12 +122,23 @@ __global__ void __launch_bounds__(128) k_ls_feat(Geom g, const YT* __restrict__ 
     if (g.noise_plane) f[4 * B + 2] = noise_feat[n];
   }
   const int nch = g.Cf / CW;
+  if constexpr (X3) {
 #pragma unroll
-  for (int c = 0; c < 48 / CW; ++c)
-    if (c < nch) store_chunk(chunk_ptr(feats, slab, nch, c, row, g), f + c * CW);
+    for (int c = 0; c < 48 / CW; ++c)
+      if (c < nch) {
+        uint4 hi, lo;
+        split_chunk(f + c * CW, hi, lo);
+        *reinterpret_cast<uint4*>(chunk_ptr(feats, slab, 2 * nch, c, row, g)) = hi;
+        *reinterpret_cast<uint4*>(chunk_ptr(feats, slab, 2 * nch, nch + c, row, g)) = lo;
+      }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 48 / CW; ++c)
+      if (c < nch) store_chunk(chunk_ptr(feats, slab, nch, c, row, g), f + c * CW);
+  }
 }
 
-template <typename OutT>
+template <typename OutT, bool X3 = false>
 int launch_ls_feat_t(const Geom& g, const void* y, int y_c128, const void* pil, int pil_c128, int n_sets,
                      const float* noise, OutT* feats, cudaStream_t st) {
   dim3 grid(cdiv(g.rows_slab, 128), g.NU);
@@ -133,9 +146,9 @@ int launch_ls_feat_t(const Geom& g, const void* y, int y_c128, const void* pil, 
 #define NRX_LSF(YT, PT)                                                                                         \
   do {                                                                                                          \
     if (b4)                                                                                                     \
-      k_ls_feat<OutT, YT, PT, 4><<<grid, 128, 0, st>>>(g, (const YT*)y, (const PT*)pil, n_sets, noise, feats);  \
+      k_ls_feat<OutT, YT, PT, 4, X3><<<grid, 128, 0, st>>>(g, (const YT*)y, (const PT*)pil, n_sets, noise, feats);  \
     else                                                                                                        \
-      k_ls_feat<OutT, YT, PT, 0><<<grid, 128, 0, st>>>(g, (const YT*)y, (const PT*)pil, n_sets, noise, feats);  \
+      k_ls_feat<OutT, YT, PT, 0, X3><<<grid, 128, 0, st>>>(g, (const YT*)y, (const PT*)pil, n_sets, noise, feats);  \
   } while (0)
   if (y_c128 && pil_c128)
     NRX_LSF(double2, double2);
@@ -153,6 +166,8 @@ int launch_ls_feat(const Geom& g, const void* y, int y_c128, const void* pil, in
                    const float* noise, void* feats, cudaStream_t st) {
   if (g.prec == NRX_BF16)
     return launch_ls_feat_t(g, y, y_c128, pil, pil_c128, n_sets, noise, (__nv_bfloat16*)feats, st);
+  if (g.prec == NRX_FP32X3)
+    return launch_ls_feat_t<__half, true>(g, y, y_c128, pil, pil_c128, n_sets, noise, (__half*)feats, st);
   if (g.prec == NRX_FP16)
     return launch_ls_feat_t(g, y, y_c128, pil, pil_c128, n_sets, noise, (__half*)feats, st);
   return launch_ls_feat_t(g, y, y_c128, pil, pil_c128, n_sets, noise, (float*)feats, st);

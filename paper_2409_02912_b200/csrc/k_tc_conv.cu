@@ -63,14 +63,6 @@ struct ConvTcParams {
 __host__ __device__ constexpr int conv_parts(int np) { return np / 16; }
 __host__ __device__ constexpr int conv_epi_threads(int np) { return 128 * conv_parts(np); }
 __host__ __device__ constexpr int conv_threads(int np) { return 64 + conv_epi_threads(np); }
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
-  uint32_t r[8];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
-}
 
 // Shared-memory carve-up (identical on host and device).
 struct ConvSmem {

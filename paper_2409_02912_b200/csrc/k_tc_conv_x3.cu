@@ -1,0 +1,719 @@
+// fp32-grade tensor-core convolution (NRX_FP32X3) on CTA pairs.
+//
+// The reference computes every convolution as an fp32 sgemm over im2col
+// (autodiff.py:315-350).  This path keeps that accuracy on the fp16 tensor
+// cores by splitting both operands:
+//   activation  a = hi + lo 2^-11   (fp16 planes, split_chunk)
+//   weight      W 2^E = Whi + Wlo   (fp16 halves, host packer)
+//   a W 2^E ~= (lo Whi) 2^-11 + hi Whi + hi Wlo
+// The MMA warp first issues every lo*Whi MMA of the tile (partial sums at
+// scale 2^11), then the hi*Wlo MMAs, the first of them with scale-input-d = 11
+// (D = A B + D 2^-11) folding the lo sums in, then the hi*Whi MMAs; the
+// epilogue multiplies by 2^-E (exact) and adds the bias in fp32 as the
+// reference does.  Representation error per operand is <= 2^-23 relative (vs
+// 2^-24 for fp32), the dropped lo*Wlo term is 2^-22 relative.
+//
+// Accumulation: the tensor core's fp32 accumulate truncates, ~0.2 ulp of D
+// towards zero per MMA (scripts/acc_probe.cu: -14.7 ulp mean after 72 MMAs,
+// where round-to-nearest stays at ~0).  Only MMAs at the full magnitude of D
+// matter, so the small lo*Whi / hi*Wlo terms go first and the hi*Whi MMAs are
+// spread over P partial accumulators by tap row (P = 3 for 3x3 kernels: 24
+// instead of 144 full-magnitude MMAs per accumulator for update.conv0), which
+// the epilogue adds in fp32 round-to-nearest.
+//
+// The weights of both halves (2x the fp16 bytes: 295 KB for
+// iteration.update.conv0) do not fit one SM's shared memory, so every layer
+// runs on a CTA pair (cluster of 2, tcgen05.mma.cta_group::2, M = 256): CTA
+// r keeps only output channels [r np/2, (r+1) np/2) of the weights resident
+// (the pair MMA reads B from both CTAs), loads its own 128-row tile + halo of
+// the activations, and receives the accumulator of its own 128 rows in its
+// own TMEM.  Per SM and K=16 step an MMA reads 4 KB of A and 1 KB of B
+// (5 KB instead of 6 KB for a single-CTA N=64 MMA).
+//
+// Roles (both CTAs): warp 0 lane 0 TMA producer (its tile, signalling the
+// leader's full barrier through the .cta_group::2 TMA form), warp 1 the MMA
+// issuer in the leader / the weights-resident relay in the peer, 4*np/32
+// epilogue warps per CTA draining their own TMEM.  Pipeline stages are
+// (tile, plane, source): lo planes of every source first, then hi planes.
+// Layout of the activations: chunk-planar as everywhere (nrx_internal.h),
+// buffers with 2C channels = [C hi | C lo].
+#include "nrx_profile.h"
+#include "tc_common.cuh"
+
+namespace nrx {
+namespace tc {
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// pair MMA D[tmem] (+)= A[smem, both CTAs] * B[smem, both CTAs]^T (fp16, fp32 accumulate)
+__device__ __forceinline__ void mma2_warp(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// D = A B + D 2^-11: folds the lo*Whi partial sums (scale 2^11) into the hi terms
+__device__ __forceinline__ void mma2_warp_fold(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, 1, 11;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc)
+      : "memory");
+}
+// commit to the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void commit2_warp(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// TMA into this CTA's shared memory, completing on the leader CTA's barrier
+__device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// Work of a CTA pair: flat tiles f over the units (slabs) whose IO set is this
+// grid row's (all slabs unless var_io); pair p takes f = 2k, 2k+1 for
+// k = p, p + npairs, ...; rank 0 the even tile, rank 1 the odd one.  When the
+// tile count is odd the last pair's rank 1 recomputes rank 0's tile with its
+// stores suppressed (real = false), so both CTAs always step together.
+struct PairIter {
+  int u, tl, units, tps, n_io, io, rank, pair, npairs;
+  bool first;
+  const int32_t* mod;
+  const Geom* g;
+  __device__ PairIter(const Geom& geo, int n_units, int tiles_per_unit, int n_io_sets, const int32_t* mods,
+                      int r)
+      : u(0), tl(0), units(n_units), tps(tiles_per_unit), n_io(n_io_sets), io(blockIdx.y), rank(r),
+        pair(blockIdx.x >> 1), npairs(gridDim.x >> 1), first(true), mod(mods), g(&geo) {}
+  __device__ bool match(int v) const { return n_io <= 1 || io_index(mod, v, *g) == io; }
+  __device__ int next_match(int v) const {
+    while (v < units && !match(v)) ++v;
+    return v;
+  }
+  __device__ void advance(int n) {
+    tl += n;
+    while (tl >= tps && u < units) {
+      tl -= tps;
+      u = next_match(u + 1);
+    }
+  }
+  __device__ bool next(int& slab, int& tile, bool& real) {
+    if (first) {
+      first = false;
+      u = next_match(0);
+      tl = 0;
+      advance(2 * pair);
+    } else {
+      advance(2 * npairs);
+    }
+    if (u >= units) return false;
+    slab = u;
+    tile = tl;
+    real = true;
+    if (rank == 1) {
+      int u2 = u, t2 = tl + 1;
+      if (t2 >= tps) {
+        t2 = 0;
+        u2 = next_match(u + 1);
+      }
+      if (u2 >= units) {
+        real = false;
+      } else {
+        slab = u2;
+        tile = t2;
+      }
+    }
+    return true;
+  }
+};
+
+struct ConvX3Params {
+  Geom g;
+  int c0, c1;        // channels per plane of source 0 / 1 (buffers hold 2x: [hi | lo])
+  int np;            // pair MMA N = rup(d, 32); each CTA holds np/2 B rows
+  int nacc;          // partial accumulators per tile (hi*Whi MMAs by tap row)
+  int cdst, stages, n_io, src1_xor, hup;
+  uint32_t wbytes;   // one rank's weight block: [hi | lo][taps*ktap/8][np/2][8] fp16
+  uint32_t abytes, tmem_cols, rbox;
+  const uint8_t* wbase;
+  uint64_t w_off[NRX_MAX_IO], b_off[NRX_MAX_IO];
+  const int32_t* mod_order;
+  __half* dst;
+};
+
+struct ConvX3Smem {
+  uint32_t w, a, bars, tmem_ptr, sbias, dt, total;
+};
+__host__ __device__ inline ConvX3Smem conv_x3_smem(const ConvX3Params& p) {
+  ConvX3Smem s;
+  uint32_t off = 0;
+  s.w = off;
+  off = (p.wbytes + 1023u) & ~1023u;
+  s.a = off;
+  off += p.stages * p.abytes;
+  s.bars = off;
+  off += 32 * 8;
+  s.tmem_ptr = off;
+  off += 16;
+  s.sbias = off;
+  off += 80 * 4;
+  s.dt = off;
+  off += 32 * 4;
+  s.total = off;
+  return s;
+}
+
+template <int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0>
+__global__ void __launch_bounds__(64 + 128 * (NP / 32), 1)
+    k_conv_x3(const __grid_constant__ ConvX3Params p, const __grid_constant__ CUtensorMap map0,
+              const __grid_constant__ CUtensorMap map1) {
+  // 32 accumulator columns per epilogue thread: 2 + 4 * NP/32 warps (10 for
+  // NP = 64) leave each SM sub-partition <= 3 warps, i.e. up to 168 registers
+  // for the fully unrolled MMA issue (18 warps would cap it at 96 and spill)
+  constexpr int PARTS = NP / 32;
+  constexpr int EPI_WARPS = 4 * PARTS;
+  constexpr int NPH = NP / 2;  // B rows per CTA
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const Geom& g = p.g;
+  const uint32_t rank = cta_rank();
+  const int io = p.n_io > 1 ? blockIdx.y : 0;
+  const ConvX3Smem L = conv_x3_smem(p);
+  uint8_t* Ws = smem + L.w;
+  const uint32_t As_s = smem_u32(smem + L.a);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* full = bars;         // [8] leader: both CTAs' stage landed
+  uint64_t* empty = bars + 8;    // [8] both: stage consumed
+  uint64_t* tfull = bars + 16;   // [2] both: accumulator ready
+  uint64_t* tempty = bars + 18;  // [2] leader: both CTAs drained the accumulator
+  uint64_t* wbar = bars + 20;    // own weights resident
+  uint64_t* wpeer = bars + 21;   // leader: the peer's weights resident
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L.tmem_ptr);
+  float* sbias = reinterpret_cast<float*>(smem + L.sbias);
+  float* sdt = reinterpret_cast<float*>(smem + L.dt);
+  const uint32_t B_full = smem_u32(full), B_empty = smem_u32(empty), B_tfull = smem_u32(tfull),
+                 B_tempty = smem_u32(tempty), B_wbar = smem_u32(wbar), B_wpeer = smem_u32(wpeer);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_launch_dependents();
+  if (warp == 0) tmem_alloc2(tmem_ptr, p.tmem_cols);
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * EPI_WARPS);
+    }
+    mbar_init(wbar, 1);
+    mbar_init(wpeer, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x >= 64 && threadIdx.x <= 64 + NP)  // bias[0..NP) and the descale 2^-E at [NP]
+    sbias[threadIdx.x - 64] = reinterpret_cast<const float*>(p.wbase + p.b_off[io])[threadIdx.x - 64];
+  if (threadIdx.x < 32) sdt[threadIdx.x] = g.dt[threadIdx.x];
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / TMA
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr;
+  const int R = p.rbox;
+#ifdef NRX_TIMING
+  long long t_a = 0, t_b = 0, t_c = 0, t_all = clock64();
+#endif
+  const int nsrc = p.c1 ? 2 : 1;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      mbar_expect_tx(wbar, p.wbytes);
+      const uint8_t* wsrc = p.wbase + p.w_off[io] + (size_t)rank * p.wbytes;
+      for (uint32_t off = 0; off < p.wbytes; off += 32768u) {
+        const uint32_t n = p.wbytes - off < 32768u ? p.wbytes - off : 32768u;
+        bulk_load(Ws + off, wsrc + off, n, wbar);
+      }
+      const uint32_t full_leader = map_rank(B_full, 0);
+      pdl_wait();
+      PairIter w(g, g.NU, g.tiles, p.n_io, p.mod_order, (int)rank);
+      int slab, tile, st = 0;
+      bool real;
+      uint32_t ph = 0;
+      while (w.next(slab, tile, real)) {
+        const int grp0 = (tile * NRX_TILE_M - p.hup) / 16;
+        for (int pl = 0; pl < 2; ++pl) {  // lo planes first (their MMAs run first), then hi
+          for (int src = 0; src < nsrc; ++src) {
+            const int cs = src ? p.c1 : p.c0;
+            NRX_T(t0);
+            mbar_wait_backoff(B_empty + 8u * st, ph ^ 1, 64);
+            NRX_TADD(t_a, t0);
+            if (rank == 0) mbar_expect_tx(B_full + 8u * st, 2u * (uint32_t)cs * R * 2);
+            tma_load_4d_pair(As_s + st * p.abytes, src ? &map1 : &map0, full_leader + 8u * st, 0, grp0,
+                             pl == 0 ? cs / 8 : 0, src ? (slab ^ p.src1_xor) : slab);
+            if (++st == p.stages) { st = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank != 0) {  // ---------------- peer: tell the leader this CTA's weights are resident
+      if (lane == 0) {
+        mbar_wait(B_wbar, 0);
+        arrive_cluster(map_rank(B_wpeer, 0));
+      }
+    } else {  // ---------------- MMA issuer (leader, whole warp, elect.sync issues)
+      constexpr uint32_t idesc = idesc_f16kind<__half>(2 * NRX_TILE_M, NP);
+      const uint64_t a_desc0 = smem_desc(0, (uint32_t)R * 16, 128);
+      const uint64_t b_hi0 = smem_desc(smem_u32(Ws), NPH * 16, 128);
+      const uint64_t b_lo0 = b_hi0 + (p.wbytes / 2 / 16);
+      const uint32_t a_kstep = 2 * R;
+      const int ktap = p.c0 + p.c1, kch = ktap / 8;
+      mbar_wait(B_wbar, 0);
+      mbar_wait(B_wpeer, 0);
+      tc_fence_after();
+      PairIter w(g, g.NU, g.tiles, p.n_io, p.mod_order, 0);
+      int slab, tile, st = 0, it = 0;
+      bool real;
+      uint32_t ph = 0;
+      const int P = KS > 0 ? KS : p.nacc;  // specialised kernels: one accumulator per tap row
+      int shifts[KS > 0 ? KS * KS : 1];      // tap row offsets (16-B units)
+      if constexpr (KS > 0) {
+#pragma unroll
+        for (int tap = 0; tap < KS * KS; ++tap) shifts[tap] = (tap / KS - KS / 2) * g.Tp + (tap % KS - KS / 2);
+      }
+      while (w.next(slab, tile, real)) {
+        const int acc = it & 1;
+        NRX_T(t0);
+        mbar_wait(B_tempty + 8u * acc, ((it >> 1) & 1) ^ 1);
+        NRX_TADD(t_a, t0);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + acc * P * NP;
+        if constexpr (KS > 0) {
+          // Specialised issue: planes, sources, taps and K steps unrolled, so every
+          // MMA is a straight-line predicated UTCHMMA with constant descriptor offsets.
+          constexpr int KCH = 2 * (NK0 + NK1);
+          constexpr int NSRC = NK1 > 0 ? 2 : 1;
+#pragma unroll
+          for (int pl = 0; pl < 2; ++pl) {
+#pragma unroll
+            for (int src = 0; src < NSRC; ++src) {
+              NRX_T(t1);
+              mbar_wait(B_full + 8u * st, ph);
+              NRX_TADD(t_b, t1);
+              tc_fence_after();
+              const uint64_t a_stage = a_desc0 + (((As_s + st * p.abytes) >> 4) + p.hup);
+              const int nk = src ? NK1 : NK0, kc0 = src ? 2 * NK0 : 0;
+              // pass 0: lo*Whi (plane 0) or hi*Wlo (plane 1) into accumulator 0;
+              // pass 1 (plane 1): hi*Whi into the partial accumulator of the tap row
+#pragma unroll
+              for (int pass = 0; pass < 2; ++pass) {
+                if (pass == 1 && pl == 0) break;
+#pragma unroll
+                for (int tap = 0; tap < KS * KS; ++tap) {
+#pragma unroll
+                  for (int k = 0; k < (NK0 > NK1 ? NK0 : NK1); ++k) {
+                    if (k >= nk) break;
+                    const uint64_t a = a_stage + shifts[tap] + (uint32_t)(k * a_kstep);
+                    const uint32_t boff = (uint32_t)((tap * KCH + kc0 + 2 * k) * NPH);
+                    if (pl == 0) {
+                      mma2_warp(d0, a, b_hi0 + boff, idesc, (src | tap | k) != 0);
+                    } else if (pass == 0) {
+                      if ((src | tap | k) == 0)
+                        mma2_warp_fold(d0, a, b_lo0 + boff, idesc);
+                      else
+                        mma2_warp(d0, a, b_lo0 + boff, idesc, 1);
+                    } else {
+                      const int ra = tap / KS;  // partial accumulator (tap row)
+                      mma2_warp(d0 + ra * NP, a, b_hi0 + boff, idesc, ra == 0 || (src | (tap % KS) | k) != 0);
+                    }
+                  }
+                }
+              }
+              commit2_warp(B_empty + 8u * st);
+              if (++st == p.stages) { st = 0; ph ^= 1; }
+            }
+          }
+        } else {
+          for (int pl = 0; pl < 2; ++pl) {
+            for (int src = 0; src < nsrc; ++src) {
+              NRX_T(t1);
+              mbar_wait(B_full + 8u * st, ph);
+              NRX_TADD(t_b, t1);
+              tc_fence_after();
+              const uint64_t a_stage = a_desc0 + (((As_s + st * p.abytes) >> 4) + p.hup);
+              const int nk = (src ? p.c1 : p.c0) / 16, kc0 = src ? p.c0 / 8 : 0;
+              for (int pass = 0; pass < (pl == 0 ? 1 : 2); ++pass) {
+                for (int tap = 0; tap < g.ks * g.ks; ++tap) {
+                  const int row = tap / g.ks, col = tap % g.ks;
+                  const int shift = (row - g.r) * g.Tp + (col - g.r);
+                  const int ra = row % P;
+                  for (int k = 0; k < nk; ++k) {
+                    const uint64_t a = a_stage + shift + (uint32_t)(k * a_kstep);
+                    const uint32_t boff = (uint32_t)((tap * kch + kc0 + 2 * k) * NPH);
+                    if (pl == 0) {
+                      mma2_warp(d0, a, b_hi0 + boff, idesc, (src | tap | k) != 0);
+                    } else if (pass == 0) {
+                      if ((src | tap | k) == 0)
+                        mma2_warp_fold(d0, a, b_lo0 + boff, idesc);
+                      else
+                        mma2_warp(d0, a, b_lo0 + boff, idesc, 1);
+                    } else {
+                      // first write of partial ra > 0: source 0, first tap of its first row, k = 0
+                      const bool first = ra > 0 && src == 0 && row == ra && col == 0 && k == 0;
+                      mma2_warp(d0 + ra * NP, a, b_hi0 + boff, idesc, !first);
+                    }
+                  }
+                }
+              }
+              commit2_warp(B_empty + 8u * st);
+              if (++st == p.stages) { st = 0; ph ^= 1; }
+            }
+          }
+        }
+        commit2_warp(B_tfull + 8u * acc);
+        ++it;
+      }
+    }
+  } else {  // ---------------- epilogue (both CTAs): warps 2 .. 2 + EPI_WARPS - 1
+    pdl_wait();
+    constexpr int NC = 32;
+    const int q = warp & 3, part = (warp - 2) >> 2;
+    const int r = 32 * q + lane;
+    const int cbase = part * NC;
+    const int nd = p.cdst / 8;              // chunks per plane of the output buffer
+    const int dch = (g.d + 7) / 8;          // chunks holding state channels
+    const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
+    const uint32_t tempty_leader = map_rank(B_tempty, 0);
+    const uint32_t sbias_s = smem_u32(sbias);
+    const float descale = sbias[NP];
+    const size_t dcs = (size_t)g.rows_slab * 8;  // chunk stride
+    PairIter w(g, g.NU, g.tiles, p.n_io, p.mod_order, (int)rank);
+    int slab, tile, it = 0;
+    bool real;
+    while (w.next(slab, tile, real)) {
+      const int acc = it & 1;
+      const int row = tile * NRX_TILE_M + r;
+      int s, t;
+      row_to_st(row, g, s, t);
+      const bool valid = real && row < g.rows_data && t < g.T;
+      __half* const drow = chunk_ptr(p.dst, slab, 2 * nd, 0, row, g);
+      float old[NC];
+      if (MODE == EPI_RESIDUAL) {  // previous state (hi + lo), loads issued before the accumulator wait
+#pragma unroll
+        for (int c8 = 0; c8 < NC / 8; ++c8) {
+          const int cc = cbase / 8 + c8;
+          uint4 hi = make_uint4(0u, 0u, 0u, 0u), lo = hi;
+          if (valid && cc < dch) {
+            hi = *reinterpret_cast<const uint4*>(drow + cc * dcs);
+            lo = *reinterpret_cast<const uint4*>(drow + (nd + cc) * dcs);
+          }
+          unsplit_chunk(hi, lo, old + 8 * c8);
+        }
+      }
+      NRX_T(t0);
+      mbar_wait_backoff(B_tfull + 8u * acc, (it >> 1) & 1, 128);
+      NRX_TADD(t_a, t0);
+      tc_fence_after();
+      float v[NC];
+      const int P = KS > 0 ? KS : p.nacc;
+      const uint32_t taddr = tmem_base + lane_off + acc * P * NP + cbase;
+      tmem_ld16(taddr, v);
+      tmem_ld16(taddr + 16, v + 16);
+      tmem_wait_ld();
+#pragma unroll
+      for (int a = 1; a < 4; ++a) {  // partial accumulators, added in fp32 round-to-nearest
+        if (a >= P) break;
+        float w2[NC];
+        tmem_ld16(taddr + a * NP, w2);
+        tmem_ld16(taddr + a * NP + 16, w2 + 16);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v[c] = __fadd_rn(v[c], w2[c]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_cluster(tempty_leader + 8u * acc);
+      ++it;
+      if (!real) continue;
+
+      const float pdt = (MODE != EPI_RELU && valid) ? sdt[t] : 0.f;
+      const float pdf = (MODE != EPI_RELU && valid) ? pos_df(s, slab % g.U, g) : 0.f;
+#pragma unroll
+      for (int c8 = 0; c8 < NC / 8; ++c8) {
+        const int cc = cbase / 8 + c8;
+        if (MODE == EPI_RESIDUAL && cc >= dch) continue;  // constant positional / zero chunk
+        if (cc >= nd) continue;
+        float bb[8], x[8];
+        ld_shared_f8(sbias_s + 32u * cc, bb);
+        const bool full = 8 * cc + 8 <= g.d;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float y = __fadd_rn(__fmul_rn(v[8 * c8 + e], descale), bb[e]);  // conv (exact 2^-E) + bias, as the reference
+          if (MODE == EPI_RELU) y = fmaxf(y, 0.f);
+          if (MODE == EPI_RESIDUAL) y = old[8 * c8 + e] + y;
+          x[e] = (valid && (full || 8 * cc + e < g.d)) ? y : 0.f;
+        }
+        if (MODE != EPI_RELU && !full) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int c = 8 * cc + e;
+            if (valid && c == g.d) x[e] = pdt;
+            if (valid && c == g.d + 1) x[e] = pdf;
+          }
+        }
+        uint4 hi, lo;
+        split_chunk(x, hi, lo);
+        *reinterpret_cast<uint4*>(drow + cc * dcs) = hi;
+        *reinterpret_cast<uint4*>(drow + (nd + cc) * dcs) = lo;
+      }
+      if (part == PARTS - 1) {  // buffer channels beyond the accumulator: positional / zero only
+        for (int cc = NP / 8; cc < nd; ++cc) {
+          if (MODE == EPI_RESIDUAL) break;  // written once by the state init
+          float o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            o[e] = (valid && MODE != EPI_RELU) ? state_extra(8 * cc + e, s, t, slab % g.U, g) : 0.f;
+          uint4 hi, lo;
+          split_chunk(o, hi, lo);
+          *reinterpret_cast<uint4*>(drow + cc * dcs) = hi;
+          *reinterpret_cast<uint4*>(drow + (nd + cc) * dcs) = lo;
+        }
+      }
+    }
+  }
+#ifdef NRX_TIMING
+  if (blockIdx.x < 2 && blockIdx.y == 0 && (threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 64))
+    printf("x3 NP=%d mode=%d KS=%d c0=%d c1=%d cta=%d tid=%d all=%lld waitA=%lld waitB=%lld\n", NP, MODE, KS, p.c0,
+           p.c1, blockIdx.x, threadIdx.x, clock64() - t_all, t_a, t_b);
+#endif
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the leader's last MMAs read the peer's shared memory / write its TMEM
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc2(tmem_base, p.tmem_cols);
+  }
+}
+
+using X3Fn = void (*)(const ConvX3Params, const CUtensorMap, const CUtensorMap);
+
+template <int NP>
+static X3Fn select_conv_x3(const Geom& g, int mode, int c0, int c1) {
+  static const X3Fn generic[3] = {k_conv_x3<NP, 0>, k_conv_x3<NP, 1>, k_conv_x3<NP, 2>};
+  X3Fn fn = generic[mode];
+  if (NP == 64 && g.ks == 3) {  // fully unrolled issue for the RT / large models' 3x3 layers
+    const int nk0 = c0 / 16, nk1 = c1 / 16;
+    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_x3<64, EPI_RELU, 3, 2, 0>;
+    if (mode == EPI_RELU && nk0 == 4 && nk1 == 4) fn = k_conv_x3<64, EPI_RELU, 3, 4, 4>;
+    if (mode == EPI_STATE_INIT && nk0 == 4 && nk1 == 0) fn = k_conv_x3<64, EPI_STATE_INIT, 3, 4, 0>;
+    if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0) fn = k_conv_x3<64, EPI_RESIDUAL, 3, 4, 0>;
+  }
+  return fn;
+}
+
+// 4-D map over a split buffer [NU][2C/8][rows][8] fp16 whose box covers the
+// C/8 chunks of one plane (the plane is picked by the chunk coordinate).
+static int make_map_plane(CUtensorMap* m, const void* base, const Geom& g, int C, int rbox) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return NRX_ERR_NO_DEVICE;
+  if (rbox % 16 || g.rows_slab % 16) return NRX_ERR_UNSUPPORTED;
+  const cuuint64_t dims[4] = {128, (cuuint64_t)(g.rows_slab / 16), (cuuint64_t)(2 * C / 8), (cuuint64_t)g.NU};
+  const cuuint64_t strides[3] = {256, (cuuint64_t)g.rows_slab * 16, (cuuint64_t)(2 * C / 8) * g.rows_slab * 16};
+  const cuuint32_t box[4] = {128, (cuuint32_t)(rbox / 16), (cuuint32_t)(C / 8), 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? NRX_OK : NRX_ERR_CUDA;
+}
+
+}  // namespace tc
+
+struct ConvX3Launch {
+  const ConvOff* offs;
+  int n_off;
+  const void* src0;
+  int c0;
+  const void* src1;
+  int c1;
+  int src1_xor;
+  void* dst;
+  int cdst;
+  int mode;
+};
+
+static int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, const int32_t* mod_order,
+                          cudaStream_t st) {
+  using namespace tc;
+  ConvX3Params p{};
+  p.g = g;
+  p.c0 = c.c0;
+  p.c1 = c.c1;
+  p.src1_xor = c.src1_xor;
+  p.np = rup(g.d, 32);
+  p.cdst = c.cdst;
+  p.n_io = c.n_off;
+  p.hup = rup(g.H, 16);
+  p.rbox = NRX_TILE_M + 2 * p.hup;
+  const int ktap = c.c0 + c.c1;
+  p.wbytes = (uint32_t)(g.ks * g.ks * ktap * (p.np / 2) * 2 * 2);
+  p.abytes = (uint32_t)((c.c0 > c.c1 ? c.c0 : c.c1) * p.rbox * 2);
+  p.wbase = wb;
+  for (int i = 0; i < p.n_io; ++i) {
+    p.w_off[i] = c.offs[i].w;
+    p.b_off[i] = c.offs[i].b;
+  }
+  p.mod_order = mod_order;
+  p.dst = static_cast<__half*>(c.dst);
+  // partial accumulators: one per tap row, at most 4 and 256 columns per tile
+  p.nacc = g.ks < 4 ? g.ks : 4;
+  while (p.nacc > 1 && p.nacc * p.np > 256) --p.nacc;
+  if (g.ks == 3 && p.np == 64 && p.nacc != 3) return NRX_ERR_UNSUPPORTED;  // specialised kernels assume P = 3
+  const uint32_t cols = 2 * p.nacc * p.np;
+  p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+  p.stages = 8;
+  while (p.stages > 2 && conv_x3_smem(p).total > SMEM_LIMIT) --p.stages;
+  if (conv_x3_smem(p).total > SMEM_LIMIT || p.rbox > 256 || p.np > 64 || c.mode < 0 || c.mode > 2)
+    return NRX_ERR_UNSUPPORTED;
+  const size_t smem = conv_x3_smem(p).total;
+  CUtensorMap m0, m1;
+  int rc = make_map_plane(&m0, c.src0, g, c.c0, p.rbox);
+  if (rc) return rc;
+  rc = make_map_plane(&m1, c.src1 ? c.src1 : c.src0, g, c.c1 ? c.c1 : c.c0, p.rbox);
+  if (rc) return rc;
+  const X3Fn fn = p.np == 64 ? select_conv_x3<64>(g, c.mode, c.c0, c.c1) : select_conv_x3<32>(g, c.mode, c.c0, c.c1);
+  if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
+  const int total = g.NU * g.tiles;
+  const int pairs_max = num_sms() / 2;
+  const int pairs = (total + 1) / 2 < pairs_max ? (total + 1) / 2 : pairs_max;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs, p.n_io);
+  cfg.blockDim = dim3(64 + 128 * (p.np / 32));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  if (cudaLaunchKernelEx(&cfg, fn, p, m0, m1) != cudaSuccess) return NRX_ERR_CUDA;
+  return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
+}
+
+#define NRX_TRY_X3(x)            \
+  do {                           \
+    int _s = (x);                \
+    if (_s != NRX_OK) return _s; \
+  } while (0)
+
+int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const void* state, void* agg,
+               cudaStream_t st);
+int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const void* state,
+                   const int32_t* mod_order, float* llr, float2* chest, cudaStream_t st);
+
+// fp32x3 forward (after K1): state init, per iteration message MLP + sum of
+// the others, update conv0 on [state | agg], update conv1 + residual; readout.
+int launch_forward_x3(const Geom& g, const PackLayout& L, const WsLayout& W, int n_it, const uint8_t* wb,
+                      const int32_t* mod_order, uint8_t* ws, float* llr, float2* chest, cudaStream_t st) {
+  if (g.d > 64 || g.h > 128) return NRX_ERR_UNSUPPORTED;
+  void* feats = ws + W.feats;
+  void* h = ws + W.h;
+  void* state = ws + W.state;
+  void* agg = ws + W.agg;
+  ConvX3Launch c{};
+  c.offs = L.init0;
+  c.n_off = g.n_io;
+  c.src0 = feats;
+  c.c0 = g.Cf;
+  c.dst = h;
+  c.cdst = g.Ch;
+  c.mode = EPI_RELU;
+  {
+    ProfScope ps(KID_INIT0, st);
+    NRX_TRY_X3(launch_conv_x3(g, c, wb, mod_order, st));
+  }
+  c = ConvX3Launch{};
+  c.offs = L.init1;
+  c.n_off = g.n_io;
+  c.src0 = h;
+  c.c0 = g.Ch;
+  c.dst = state;
+  c.cdst = g.Cs;
+  c.mode = EPI_STATE_INIT;
+  {
+    ProfScope ps(KID_INIT1, st);
+    NRX_TRY_X3(launch_conv_x3(g, c, wb, mod_order, st));
+  }
+  for (int it = 0; it < n_it; ++it) {
+    {
+      ProfScope ps(KID_MSG, st);
+      NRX_TRY_X3(launch_msg(g, L, wb, state, agg, st));
+    }
+    c = ConvX3Launch{};
+    c.offs = &L.upd0;
+    c.n_off = 1;
+    c.src0 = state;
+    c.c0 = g.Cs;
+    c.src1 = agg;
+    c.c1 = g.Ca;
+    c.dst = h;
+    c.cdst = g.Ch;
+    c.mode = EPI_RELU;
+    {
+      ProfScope ps(KID_UPD0, st);
+      NRX_TRY_X3(launch_conv_x3(g, c, wb, mod_order, st));
+    }
+    c = ConvX3Launch{};
+    c.offs = &L.upd1;
+    c.n_off = 1;
+    c.src0 = h;
+    c.c0 = g.Ch;
+    c.dst = state;
+    c.cdst = g.Cs;
+    c.mode = EPI_RESIDUAL;
+    ProfScope ps(KID_UPD1, st);
+    NRX_TRY_X3(launch_conv_x3(g, c, wb, mod_order, st));
+  }
+  ProfScope ps(KID_READOUT, st);
+  return launch_readout(g, L, wb, state, mod_order, llr, chest, st);
+}
+
+}  // namespace nrx

@@ -1,4 +1,4 @@
-// bf16 tensor-core per-RE MLPs (NRX_BF16 path).
+// Tensor-core per-RE MLPs (bf16 / fp16 operands, or fp32x3 split operands).
 //
 //  k_msg_tc      message MLP of every UE of a slot on a 128-RE tile followed
 //                by the float64 sum of the other UEs' messages
@@ -16,6 +16,9 @@
 //               (the next GEMM's K-major A operand), double buffered
 //   warps 6-9   output epilogue: sum-of-others / LLR + chest stores
 // "use" j enumerates the (work item, UE) pairs a CTA processes.
+// X3 (NRX_FP32X3): state tiles, hidden layers and weights carry fp16 hi + lo
+// planes; every GEMM is mma_x3_gemm (lo*Whi, then hi*Whi folded by
+// scale-input-d, hi*Wlo) and the epilogues apply the packer's 2^-E descale.
 #include "tc_common.cuh"
 
 namespace nrx {
@@ -25,7 +28,7 @@ namespace tc {
 constexpr int mlp_threads(int hw) { return 64 + 32 * hw + 128; }
 constexpr int MSG_HW = 4, READOUT_HW = 8;
 constexpr int MSG_MAXU = 4;  // UEs per slot on the tensor-core path
-constexpr int A_STAGES = 4;
+constexpr int A_STAGES = 4;  // maximum; fp32x3 uses fewer (p.astages)
 
 struct MlpTcParams {
   Geom g;
@@ -34,6 +37,7 @@ struct MlpTcParams {
   int units;               // work units: slots (msg) or slabs (readout)
   int n_io;
   uint32_t w0bytes, w1bytes, abytes, hbytes, tmem_cols;
+  int astages, nhb;        // A ring stages, hidden shared-memory buffers (1 or 2)
   uint32_t col_h, col_o;   // TMEM column of hidden buffer 0 / output region 0
   const uint8_t* wbase;
   uint64_t w0[NRX_MAX_IO], b0[NRX_MAX_IO], w1[NRX_MAX_IO], b1[NRX_MAX_IO];
@@ -53,8 +57,8 @@ struct MlpSmem {
     W0 = smem;
     W1 = W0 + p.w0bytes;
     As = W1 + p.w1bytes;
-    Hs = As + A_STAGES * p.abytes;
-    uint64_t* b = reinterpret_cast<uint64_t*>(Hs + 2 * p.hbytes);
+    Hs = As + p.astages * p.abytes;
+    uint64_t* b = reinterpret_cast<uint64_t*>(Hs + p.nhb * p.hbytes);
     afull = b;
     aempty = b + A_STAGES;
     hid_full = b + 2 * A_STAGES;
@@ -64,8 +68,8 @@ struct MlpSmem {
     out_free = out_full + 2;
     wbar = out_free + 2;
     sb0 = reinterpret_cast<float*>(wbar + 2);
-    sb1 = sb0 + 256;
-    tmem_ptr = reinterpret_cast<uint32_t*>(sb1 + 64);
+    sb1 = sb0 + 260;
+    tmem_ptr = reinterpret_cast<uint32_t*>(sb1 + 68);
   }
 };
 
@@ -73,7 +77,7 @@ __device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int 
   const int warp = threadIdx.x >> 5;
   if (warp == 0) tmem_alloc(s.tmem_ptr, p.tmem_cols);
   if (threadIdx.x == 32) {
-    for (int i = 0; i < A_STAGES; ++i) {
+    for (int i = 0; i < p.astages; ++i) {
       mbar_init(&s.afull[i], 1);
       mbar_init(&s.aempty[i], 1);
     }
@@ -89,8 +93,10 @@ __device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int 
   }
   const float* b0 = reinterpret_cast<const float*>(p.wbase + p.b0[io]);
   const float* b1 = reinterpret_cast<const float*>(p.wbase + p.b1[io]);
-  for (int i = threadIdx.x; i < p.hp; i += blockDim.x) s.sb0[i] = b0[i];
-  for (int i = threadIdx.x; i < p.op; i += blockDim.x) s.sb1[i] = b1[i];
+  // fp32x3 blobs store the descale 2^-E right after each bias vector
+  const bool x3 = p.g.prec == NRX_FP32X3;
+  for (int i = threadIdx.x; i <= p.hp; i += blockDim.x) s.sb0[i] = i < p.hp || x3 ? b0[i] : 1.f;
+  for (int i = threadIdx.x; i <= p.op; i += blockDim.x) s.sb1[i] = i < p.op || x3 ? b1[i] : 1.f;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -98,7 +104,7 @@ __device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int 
 
 // Producer / MMA / hidden-epilogue roles are identical for both MLPs; the
 // output epilogue is passed in as a functor.
-template <typename ET, int HW, typename OutEpilogue>
+template <typename ET, int HW, bool X3, typename OutEpilogue>
 __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int io, const CUtensorMap* amap,
                                          OutEpilogue&& out_epi) {
   const Geom& g = p.g;
@@ -125,7 +131,7 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
           mbar_expect_tx(&s.afull[st], p.abytes);
           tma_load_4d(s.As + (size_t)st * p.abytes, amap, &s.afull[st], 0, tile * (NRX_TILE_M / 16), 0,
                       unit * U + u);
-          if (++st == A_STAGES) { st = 0; ph ^= 1; }
+          if (++st == p.astages) { st = 0; ph ^= 1; }
         }
       }
     }
@@ -148,14 +154,19 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
         const uint32_t as = smem_u32(s.As + (size_t)st * p.abytes);
         const uint32_t d = tmem_base + p.col_h + (jj & 1) * p.hp;
         uint64_t ad = smem_desc(as, NRX_TILE_M * 16, 128), bd = smem_desc(w0s, p.hp * 16, 128);
-        for (int kc = 0; kc < p.cs / 8; kc += 2) {
-          mma_bf16_warp(d, ad, bd, id0, kc != 0);
-          ad += 2 * NRX_TILE_M;
-          bd += 2 * p.hp;
+        if constexpr (X3) {
+          mma_x3_gemm(d, ad, (p.cs / 8) * NRX_TILE_M, 2 * NRX_TILE_M, bd, (p.cs / 8) * p.hp, 2 * p.hp, p.cs / 16,
+                      id0);
+        } else {
+          for (int kc = 0; kc < p.cs / 8; kc += 2) {
+            mma_bf16_warp(d, ad, bd, id0, kc != 0);
+            ad += 2 * NRX_TILE_M;
+            bd += 2 * p.hp;
+          }
         }
         mma_commit_warp(&s.aempty[st]);
         mma_commit_warp(&s.hid_full[jj & 1]);
-        if (++st == A_STAGES) { st = 0; ph ^= 1; }
+        if (++st == p.astages) { st = 0; ph ^= 1; }
       };
       if (have) fc0(0);
       while (have) {
@@ -166,9 +177,9 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
           bool next_exists = true;
           if (last_u) next_exists = w.next(nunit, ntile);
           if (next_exists) fc0(j + 1);
-          const int hb = j & 1;
+          const int hb = p.nhb == 2 ? (j & 1) : 0;
           NRX_T(t1);
-          mbar_wait(&s.h_ready[hb], (j >> 1) & 1);
+          mbar_wait(&s.h_ready[hb], (p.nhb == 2 ? j >> 1 : j) & 1);
           NRX_TADD(t_b, t1);
           tc_fence_after();
           if (u == 0) {  // output region of this item free again?
@@ -180,10 +191,15 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
           const uint32_t hs = smem_u32(s.Hs + (size_t)hb * p.hbytes);
           const uint32_t d = tmem_base + p.col_o + (item & 1) * (U * p.op) + u * p.op;
           uint64_t ad = smem_desc(hs, NRX_TILE_M * 16, 128), bd = smem_desc(w1s, p.op * 16, 128);
-          for (int kc = 0; kc < p.hp / 8; kc += 2) {
-            mma_bf16_warp(d, ad, bd, id1, kc != 0);
-            ad += 2 * NRX_TILE_M;
-            bd += 2 * p.op;
+          if constexpr (X3) {
+            mma_x3_gemm(d, ad, (p.hp / 8) * NRX_TILE_M, 2 * NRX_TILE_M, bd, (p.hp / 8) * p.op, 2 * p.op, p.hp / 16,
+                        id1);
+          } else {
+            for (int kc = 0; kc < p.hp / 8; kc += 2) {
+              mma_bf16_warp(d, ad, bd, id1, kc != 0);
+              ad += 2 * NRX_TILE_M;
+              bd += 2 * p.op;
+            }
           }
           mma_commit_warp(&s.hs_free[hb]);
           if (last_u) {
@@ -205,28 +221,41 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
     int unit, tile, j = 0;
     while (w.next(unit, tile)) {
       for (int u = 0; u < U; ++u, ++j) {
-        const int hb = j & 1;
+        const int ab = j & 1;                      // TMEM hidden accumulator
+        const int hb = p.nhb == 2 ? ab : 0;         // shared-memory hidden tile
+        const int hk = p.nhb == 2 ? j >> 1 : j;     // its use count
         NRX_T(t0);
-        mbar_wait(&s.hid_full[hb], (j >> 1) & 1);
+        mbar_wait(&s.hid_full[ab], (j >> 1) & 1);
         NRX_TADD(t_a, t0);
         tc_fence_after();
         NRX_T(t1);
-        mbar_wait(&s.hs_free[hb], ((j >> 1) & 1) ^ 1);  // fc1 of use j-2 done with Hs[hb]
+        mbar_wait(&s.hs_free[hb], (hk & 1) ^ 1);  // fc1 of the previous use of Hs[hb] done
         NRX_TADD(t_b, t1);
         NRX_T(t2);
         uint8_t* H = s.Hs + (size_t)hb * p.hbytes;
+        const float dsc = X3 ? s.sb0[p.hp] : 1.f;
         for (int c32 = cbeg; c32 < cbeg + cspan; c32 += 32) {
           float v[32];
-          tmem_ld16(tmem_base + lane_off + p.col_h + hb * p.hp + c32, v);
-          if (c32 + 16 < cbeg + cspan) tmem_ld16(tmem_base + lane_off + p.col_h + hb * p.hp + c32 + 16, v + 16);
+          tmem_ld16(tmem_base + lane_off + p.col_h + ab * p.hp + c32, v);
+          if (c32 + 16 < cbeg + cspan) tmem_ld16(tmem_base + lane_off + p.col_h + ab * p.hp + c32 + 16, v + 16);
           tmem_wait_ld();
 #pragma unroll
           for (int c8 = 0; c8 < 4; ++c8) {
             if (c32 + 8 * c8 >= cbeg + cspan) break;
             float o[8];
+            const int ch = c32 / 8 + c8;
+            if constexpr (X3) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) o[e] = fmaxf(v[8 * c8 + e] + s.sb0[c32 + 8 * c8 + e], 0.f);
-            store_chunk(reinterpret_cast<ET*>(H + ((size_t)(c32 / 8 + c8) * NRX_TILE_M + r) * 16), o);
+              for (int e = 0; e < 8; ++e) o[e] = fmaxf(__fadd_rn(__fmul_rn(v[8 * c8 + e], dsc), s.sb0[8 * ch + e]), 0.f);
+              uint4 hi, lo;
+              split_chunk(o, hi, lo);
+              *reinterpret_cast<uint4*>(H + ((size_t)ch * NRX_TILE_M + r) * 16) = hi;
+              *reinterpret_cast<uint4*>(H + ((size_t)(p.hp / 8 + ch) * NRX_TILE_M + r) * 16) = lo;
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) o[e] = fmaxf(v[8 * c8 + e] + s.sb0[c32 + 8 * c8 + e], 0.f);
+              store_chunk(reinterpret_cast<ET*>(H + ((size_t)ch * NRX_TILE_M + r) * 16), o);
+            }
           }
         }
         fence_proxy_async();  // generic-proxy smem writes -> tensor-core reads
@@ -265,7 +294,7 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
   }
 }
 
-template <typename ET>
+template <typename ET, bool X3>
 __global__ void __launch_bounds__(mlp_threads(MSG_HW), 1)
     k_msg_tc(const __grid_constant__ MlpTcParams p, const __grid_constant__ CUtensorMap smap) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -275,7 +304,8 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW), 1)
   const int U = p.uses_per_item;
   const int nca = g.Ca / 8;
   ET* const agg = static_cast<ET*>(p.agg);
-  mlp_body<ET, MSG_HW>(p, s, 0, &smap, [&](int n, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
+  const float dsc = X3 ? s.sb1[p.op] : 1.f;
+  mlp_body<ET, MSG_HW, X3>(p, s, 0, &smap, [&](int n, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
     const int row = tile * NRX_TILE_M + r;
     const int srow = row / g.Tp, t = row - srow * g.Tp;
     const bool valid = row < g.rows_data && t < g.T;
@@ -298,7 +328,7 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW), 1)
       for (int u = 0; u < MSG_MAXU; ++u)
         if (u < U)
 #pragma unroll
-          for (int e = 0; e < 16; ++e) m[u][e] += s.sb1[c16 + e];
+          for (int e = 0; e < 16; ++e) m[u][e] = X3 ? __fadd_rn(__fmul_rn(m[u][e], dsc), s.sb1[c16 + e]) : m[u][e] + s.sb1[c16 + e];
 #pragma unroll
       for (int u = 0; u < MSG_MAXU; ++u) {
         if (u >= U) break;
@@ -316,14 +346,21 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW), 1)
             const int c = 8 * c8 + e;
             o[e] = (valid && c < g.d) ? a : 0.f;
           }
-          store_chunk(chunk_ptr(agg, n * U + u, nca, c8, row, g), o);
+          if constexpr (X3) {  // [hi | lo] planes of the aggregate
+            uint4 hi, lo;
+            split_chunk(o, hi, lo);
+            *reinterpret_cast<uint4*>(chunk_ptr(agg, n * U + u, 2 * nca, c8, row, g)) = hi;
+            *reinterpret_cast<uint4*>(chunk_ptr(agg, n * U + u, 2 * nca, nca + c8, row, g)) = lo;
+          } else {
+            store_chunk(chunk_ptr(agg, n * U + u, nca, c8, row, g), o);
+          }
         }
       }
     }
   });
 }
 
-template <typename ET>
+template <typename ET, bool X3>
 __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
     k_readout_tc(const __grid_constant__ MlpTcParams p, const __grid_constant__ CUtensorMap smap) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -331,7 +368,8 @@ __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
   const int io = p.n_io > 1 ? blockIdx.y : 0;
   mlp_setup(p, s, io, 32 * READOUT_HW);
   const Geom& g = p.g;
-  mlp_body<ET, READOUT_HW>(p, s, io, &smap, [&](int slab, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
+  const float dsc = X3 ? s.sb1[p.op] : 1.f;
+  mlp_body<ET, READOUT_HW, X3>(p, s, io, &smap, [&](int slab, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
     float o[32];
     tmem_ld16(taddr, o);
     tmem_ld16(taddr + 16, o + 16);
@@ -342,7 +380,7 @@ __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
     const int srow = row / g.Tp, t = row - srow * g.Tp;
     if (row >= g.rows_data || t >= g.T) return;
 #pragma unroll
-    for (int c = 0; c < 32; ++c) o[c] += s.sb1[c];
+    for (int c = 0; c < 32; ++c) o[c] = X3 ? __fadd_rn(__fmul_rn(o[c], dsc), s.sb1[c]) : o[c] + s.sb1[c];
     const int mio = io_index(p.mod_order, slab, g);
     const int width = mio < 0 ? 0 : g.io_width[mio];
     const size_t re = ((size_t)slab * g.S + srow) * g.T + t;
@@ -377,24 +415,34 @@ __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
 
 using namespace tc;
 
+static size_t mlp_smem_bytes(const MlpTcParams& p) {
+  return (size_t)p.w0bytes + p.w1bytes + p.astages * p.abytes + p.nhb * p.hbytes + (2 * A_STAGES + 12) * 8 +
+         (260 + 68) * 4 + 16;
+}
+
 static int mlp_common(MlpTcParams& p, const Geom& g, int hp, int op, int uses, int units, size_t* smem) {
+  const uint32_t planes = g.prec == NRX_FP32X3 ? 2 : 1;  // fp32x3: [hi | lo] everywhere
   p.g = g;
   p.cs = g.Cs;
   p.hp = hp;
   p.op = op;
   p.uses_per_item = uses;
   p.units = units;
-  p.w0bytes = (uint32_t)(p.cs * hp * 2);
-  p.w1bytes = (uint32_t)(hp * op * 2);
-  p.abytes = (uint32_t)(p.cs * NRX_TILE_M * 2);
-  p.hbytes = (uint32_t)(hp * NRX_TILE_M * 2);
+  p.w0bytes = planes * (uint32_t)(p.cs * hp * 2);
+  p.w1bytes = planes * (uint32_t)(hp * op * 2);
+  p.abytes = planes * (uint32_t)(p.cs * NRX_TILE_M * 2);
+  p.hbytes = planes * (uint32_t)(hp * NRX_TILE_M * 2);
+  p.astages = A_STAGES;
+  p.nhb = 2;
+  while (mlp_smem_bytes(p) > SMEM_LIMIT && p.astages > 2) --p.astages;
+  if (mlp_smem_bytes(p) > SMEM_LIMIT) p.nhb = 1;
+  while (mlp_smem_bytes(p) > SMEM_LIMIT && p.astages > 1) --p.astages;
   p.col_h = 0;
   p.col_o = 2 * hp;
   const uint32_t cols = 2 * hp + 2 * uses * op;
   if (cols > 512 || hp > 256) return NRX_ERR_UNSUPPORTED;
   p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
-  *smem = (size_t)p.w0bytes + p.w1bytes + A_STAGES * p.abytes + 2 * p.hbytes + (2 * A_STAGES + 12) * 8 +
-          (256 + 64) * 4 + 16;
+  *smem = mlp_smem_bytes(p);
   return *smem > SMEM_LIMIT ? NRX_ERR_UNSUPPORTED : NRX_OK;
 }
 
@@ -413,9 +461,11 @@ int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const void
   p.b1[0] = L.msg.b1;
   p.agg = agg;
   CUtensorMap m;
-  rc = make_map(&m, state, g, g.Cs, NRX_TILE_M);
+  rc = make_map(&m, state, g, g.prec == NRX_FP32X3 ? 2 * g.Cs : g.Cs, NRX_TILE_M);
   if (rc) return rc;
-  const auto fn = g.prec == NRX_FP16 ? k_msg_tc<__half> : k_msg_tc<__nv_bfloat16>;
+  const auto fn = g.prec == NRX_FP32X3 ? k_msg_tc<__half, true>
+                  : g.prec == NRX_FP16 ? k_msg_tc<__half, false>
+                                       : k_msg_tc<__nv_bfloat16, false>;
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.N * g.tiles;
   const int per_sm = (512 / p.tmem_cols) < 2 || 2 * smem > SMEM_LIMIT ? 1 : 2;
@@ -442,9 +492,11 @@ int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const 
   p.llr = llr;
   p.chest = chest;
   CUtensorMap m;
-  rc = make_map(&m, state, g, g.Cs, NRX_TILE_M);
+  rc = make_map(&m, state, g, g.prec == NRX_FP32X3 ? 2 * g.Cs : g.Cs, NRX_TILE_M);
   if (rc) return rc;
-  const auto fn = g.prec == NRX_FP16 ? k_readout_tc<__half> : k_readout_tc<__nv_bfloat16>;
+  const auto fn = g.prec == NRX_FP32X3 ? k_readout_tc<__half, true>
+                  : g.prec == NRX_FP16 ? k_readout_tc<__half, false>
+                                       : k_readout_tc<__nv_bfloat16, false>;
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.NU * g.tiles;
   const int per_sm = (512 / p.tmem_cols) < 2 || 2 * smem > SMEM_LIMIT ? 1 : 2;

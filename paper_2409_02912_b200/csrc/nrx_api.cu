@@ -22,6 +22,8 @@ void ws_layout(const Geom& g, WsLayout* w);
 int launch_forward_tc(const Geom& g, const PackLayout& L, const WsLayout& W, int n_it, const uint8_t* wb,
                       const int32_t* mod_order, uint8_t* ws, float* llr, float2* chest, cudaStream_t st);
 int tc_launch_count(int n_it, int num_ues);
+int launch_forward_x3(const Geom& g, const PackLayout& L, const WsLayout& W, int n_it, const uint8_t* wb,
+                      const int32_t* mod_order, uint8_t* ws, float* llr, float2* chest, cudaStream_t st);
 }  // namespace nrx
 
 using namespace nrx;
@@ -96,13 +98,16 @@ extern "C" int nrx_forward(const nrx_model_desc* model, const nrx_slot_desc* slo
   }
   if (precision == NRX_FP32)
     return forward_simt(g, L, W, num_iterations, wb, mod_order, ws, llr_out, static_cast<float2*>(chest_out), st);
+  if (precision == NRX_FP32X3)
+    return launch_forward_x3(g, L, W, num_iterations, wb, mod_order, ws, llr_out, static_cast<float2*>(chest_out),
+                             st);
   return launch_forward_tc(g, L, W, num_iterations, wb, mod_order, ws, llr_out, static_cast<float2*>(chest_out), st);
 }
 
 extern "C" int nrx_forward_launch_count(const nrx_model_desc* model, const nrx_slot_desc* slot, int precision,
                                         int num_iterations) {
   if (!model || !slot || num_iterations < 1) return -1;
-  if (precision == NRX_FP32) return 1 + 2 + 3 * num_iterations + 1;
+  if (precision == NRX_FP32 || precision == NRX_FP32X3) return 1 + 2 + 3 * num_iterations + 1;
   return 1 + tc_launch_count(num_iterations, slot->num_ues);
 }
 

@@ -159,6 +159,36 @@ __device__ __forceinline__ void unpack_chunk(uint4 q, const __half*, float* v) {
   }
 }
 
+// fp32x3 operand split (NRX_FP32X3): a = hi + lo 2^-11 with hi = fp16(a) and
+// lo = fp16((a - hi) 2^11).  a - hi is exact in fp32 and |lo| <= |a|, so lo
+// never overflows where hi does not; lo keeps 11 more bits for |a| >= 2^-13.
+constexpr float X3_LO_SCALE = 2048.f;
+constexpr float X3_LO_INV = 1.f / 2048.f;
+__device__ __forceinline__ void split_chunk(const float* v, uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __half2 hh = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+    const float2 hf = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn((v[2 * i] - hf.x) * X3_LO_SCALE, (v[2 * i + 1] - hf.y) * X3_LO_SCALE);
+    h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[i] = *reinterpret_cast<const uint32_t*>(&ll);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+// hi + lo 2^-11 in fp32 (exact: both terms fit the 24-bit significand)
+__device__ __forceinline__ void unsplit_chunk(uint4 hi, uint4 lo, float* v) {
+  const uint32_t h[4] = {hi.x, hi.y, hi.z, hi.w}, l[4] = {lo.x, lo.y, lo.z, lo.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&h[i]));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&l[i]));
+    v[2 * i] = fmaf(b.x, X3_LO_INV, a.x);
+    v[2 * i + 1] = fmaf(b.y, X3_LO_INV, a.y);
+  }
+}
+
 __device__ __forceinline__ int io_index(const int32_t* mod_order, int slab, const Geom& g) {
   if (g.n_io == 1 || mod_order == nullptr) return 0;
   const int m = mod_order[slab];

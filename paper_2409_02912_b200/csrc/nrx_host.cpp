@@ -90,7 +90,7 @@ int make_geom(const nrx_model_desc* m, const nrx_slot_desc* s, int n_slots, int 
   int st = validate(m, s);
   if (st) return st;
   if (n_slots < 1) return NRX_ERR_INVALID;
-  if (prec != NRX_FP32 && prec != NRX_BF16 && prec != NRX_FP16) return NRX_ERR_INVALID;
+  if (prec != NRX_FP32 && prec != NRX_BF16 && prec != NRX_FP16 && prec != NRX_FP32X3) return NRX_ERR_INVALID;
   std::memset(g, 0, sizeof(*g));
   g->N = n_slots;
   g->U = s->num_ues;
@@ -179,6 +179,31 @@ void pack_layout(const nrx_model_desc* m, int prec, PackLayout* L) {
   L->dmax = dmax;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+  if (prec == NRX_FP32X3) {  // fp16 hi/lo operand pairs, CTA-pair convolutions
+    const int npx = rup(m->d_s, 32), np = rup(m->d_s, 16), hp = rup(m->hidden, 16);
+    auto conv = [&](ConvOff& c, int ktap) {
+      c.ktap = ktap;
+      c.w = take((size_t)taps * ktap * npx * 2 * 2);  // [rank][hi|lo][K/8][npx/2][8]
+      c.b = take((size_t)(npx + 4) * 4);              // bias, then the descale 2^-E
+    };
+    auto mlp = [&](MlpOff& o, int k0, int n0, int n1) {
+      o.out = n1;
+      o.w0 = take((size_t)k0 * n0 * 2 * 2);  // [hi|lo][K/8][N][8]
+      o.b0 = take((size_t)(n0 + 4) * 4);
+      o.w1 = take((size_t)n0 * n1 * 2 * 2);
+      o.b1 = take((size_t)(n1 + 4) * 4);
+    };
+    for (int i = 0; i < m->n_io; ++i) {
+      conv(L->init0[i], g.Cf);
+      conv(L->init1[i], g.Ch);
+      mlp(L->llr[i], g.Cs, 2 * hp, 32);
+    }
+    mlp(L->msg, g.Cs, hp, np);
+    conv(L->upd0, g.Cs + g.Ca);
+    conv(L->upd1, g.Ch);
+    L->total = off;
+    return;
+  }
   if (prec != NRX_FP32) {  // bf16 / fp16 tensor-core operands
     const int np = rup(m->d_s, 16), hp = rup(m->hidden, 16);
     auto conv = [&](ConvOff& c, int ktap) {
@@ -313,7 +338,141 @@ void pack_conv_bf16(const Geom& g, int k, const ConvOff& c, int cin_ref, const f
   for (int o = 0; o < np; ++o) db[o] = o < cout ? b[o] : 0.f;
 }
 
+float f16_to_f32(uint16_t b) {
+  _Float16 h;
+  std::memcpy(&h, &b, 2);
+  return (float)h;
+}
+
+// Power-of-two operand scale 2^E with max|W| 2^E in [2^13, 2^14): the hi
+// halves stay far below the fp16 limit and the lo halves (|lo| <= 2^-11 |hi|)
+// keep all 11 bits down to weights 2^-16 of the largest.
+int split_exponent(float maxabs) {
+  if (!(maxabs > 0.f) || !std::isfinite(maxabs)) return 0;
+  int e = 0;
+  std::frexp(maxabs, &e);  // maxabs < 2^e
+  int E = 14 - e;
+  return E < -100 ? -100 : E > 100 ? 100 : E;
+}
+
+// fp32-grade B operand: W 2^E = hi + lo (both fp16), K-major core-matrix
+// layout [K/8][N][8] for each half; `lo_off` elements separate the halves.
+struct SplitB {
+  uint16_t* p;
+  int N;
+  size_t lo_off;
+  float scale;
+  void set(int n, int k, float v) {
+    const float s = v * scale;
+    const uint16_t h = f32_to_f16(s);
+    const size_t i = ((size_t)(k / 8) * N + n) * 8 + (k % 8);
+    p[i] = h;
+    p[lo_off + i] = f32_to_f16(s - f16_to_f32(h));
+  }
+};
+
+// Convolution for the CTA pair: rank r holds output channels
+// [r npx/2, (r+1) npx/2) as its B operand rows ([hi | lo] per rank).
+void pack_conv_x3(const Geom& g, int k, const ConvOff& c, int cin_ref, const float* w, const float* b,
+                  ChanMap map, uint8_t* base) {
+  const int npx = rup(g.d, 32), nh = npx / 2, taps = k * k, cout = g.d;
+  float mx = 0.f;
+  for (size_t i = 0; i < (size_t)taps * cin_ref * cout; ++i) mx = std::fmax(mx, std::fabs(w[i]));
+  const int E = split_exponent(mx);
+  const size_t half = (size_t)taps * c.ktap * nh;  // elements of one hi (or lo) block
+  for (int r = 0; r < 2; ++r) {
+    SplitB B{(uint16_t*)(base + c.w) + (size_t)r * 2 * half, nh, half, std::ldexp(1.f, E)};
+    for (int tap = 0; tap < taps; ++tap)
+      for (int j = 0; j < c.ktap; ++j) {
+        const int src = map(j, g);
+        for (int n = 0; n < nh; ++n) {
+          const int o = r * nh + n;
+          B.set(n, tap * c.ktap + j, (src >= 0 && o < cout) ? w[((size_t)tap * cin_ref + src) * cout + o] : 0.f);
+        }
+      }
+  }
+  float* db = (float*)(base + c.b);
+  for (int o = 0; o < npx; ++o) db[o] = o < cout ? b[o] : 0.f;
+  db[npx] = std::ldexp(1.f, -E);
+}
+
 }  // namespace
+
+// fp32-grade tensor-core packing (NRX_FP32X3): same GEMM shapes as
+// pack_weights_tc, every B operand as scaled fp16 [hi | lo] halves and the
+// descale 2^-E stored after each bias vector.
+int pack_weights_x3(const nrx_model_desc* m, const float* const* t, uint8_t* base) {
+  PackLayout L;
+  pack_layout(m, NRX_FP32X3, &L);
+  std::memset(base, 0, L.total);
+  Geom g;
+  nrx_slot_desc s{};
+  s.num_subcarriers = 64; s.num_symbols = 14; s.num_ues = 1; s.comb_size = 1;
+  s.num_pilot_symbols = 1;
+  make_geom(m, &s, 1, NRX_FP32X3, &g);
+  const int k = m->kernel_size, d = m->d_s, h = m->hidden, B2 = 2 * m->num_rx_ant;
+  const int np = rup(d, 16), hp = rup(h, 16);
+  const int i_msg = 8 * m->n_io, i_upd = i_msg + 4, i_chest = i_upd + 4;
+  auto maxabs = [](const float* a, size_t n) {
+    float mx = 0.f;
+    for (size_t i = 0; i < n; ++i) mx = std::fmax(mx, std::fabs(a[i]));
+    return mx;
+  };
+  for (int io = 0; io < m->n_io; ++io) {
+    const int i = 8 * io;
+    pack_conv_x3(g, k, L.init0[io], g.Cin, t[i], t[i + 1], map_identity_feats, base);
+    pack_conv_x3(g, k, L.init1[io], d, t[i + 2], t[i + 3], map_identity_hidden, base);
+    const MlpOff& o = L.llr[io];
+    const int width = llr_width_of(m, io);
+    const float *lw0 = t[i + 4], *lb0 = t[i + 5], *lw1 = t[i + 6], *lb1 = t[i + 7];
+    const float *cw0 = t[i_chest], *cb0 = t[i_chest + 1], *cw1 = t[i_chest + 2], *cb1 = t[i_chest + 3];
+    const int E0 = split_exponent(std::fmax(maxabs(lw0, (size_t)d * h), maxabs(cw0, (size_t)d * h)));
+    SplitB W0{(uint16_t*)(base + o.w0), 2 * hp, (size_t)g.Cs * 2 * hp, std::ldexp(1.f, E0)};
+    float* b0 = (float*)(base + o.b0);
+    for (int n = 0; n < 2 * hp; ++n) {
+      const bool chest = n >= hp;
+      const int nn = chest ? n - hp : n;
+      for (int kk = 0; kk < g.Cs; ++kk)
+        W0.set(n, kk, (kk < d && nn < h) ? (chest ? cw0 : lw0)[(size_t)kk * h + nn] : 0.f);
+      b0[n] = nn < h ? (chest ? cb0 : lb0)[nn] : 0.f;
+    }
+    b0[2 * hp] = std::ldexp(1.f, -E0);
+    const int E1 = split_exponent(std::fmax(maxabs(lw1, (size_t)h * width), maxabs(cw1, (size_t)h * B2)));
+    SplitB W1{(uint16_t*)(base + o.w1), 32, (size_t)2 * hp * 32, std::ldexp(1.f, E1)};
+    float* b1 = (float*)(base + o.b1);
+    for (int n = 0; n < 32; ++n) {
+      for (int kk = 0; kk < 2 * hp; ++kk) {
+        float v = 0.f;
+        if (n < width && kk < h) v = lw1[(size_t)kk * width + n];
+        if (n >= 8 && n < 8 + B2 && kk >= hp && kk - hp < h) v = cw1[(size_t)(kk - hp) * B2 + (n - 8)];
+        W1.set(n, kk, v);
+      }
+      b1[n] = n < width ? lb1[n] : (n >= 8 && n < 8 + B2) ? cb1[n - 8] : 0.f;
+    }
+    b1[32] = std::ldexp(1.f, -E1);
+  }
+  {
+    const float *w0 = t[i_msg], *b0 = t[i_msg + 1], *w1 = t[i_msg + 2], *b1 = t[i_msg + 3];
+    const int E0 = split_exponent(maxabs(w0, (size_t)d * h)), E1 = split_exponent(maxabs(w1, (size_t)h * d));
+    SplitB W0{(uint16_t*)(base + L.msg.w0), hp, (size_t)g.Cs * hp, std::ldexp(1.f, E0)};
+    float* pb0 = (float*)(base + L.msg.b0);
+    for (int n = 0; n < hp; ++n) {
+      for (int kk = 0; kk < g.Cs; ++kk) W0.set(n, kk, (kk < d && n < h) ? w0[(size_t)kk * h + n] : 0.f);
+      pb0[n] = n < h ? b0[n] : 0.f;
+    }
+    pb0[hp] = std::ldexp(1.f, -E0);
+    SplitB W1{(uint16_t*)(base + L.msg.w1), np, (size_t)hp * np, std::ldexp(1.f, E1)};
+    float* pb1 = (float*)(base + L.msg.b1);
+    for (int n = 0; n < np; ++n) {
+      for (int kk = 0; kk < hp; ++kk) W1.set(n, kk, (kk < h && n < d) ? w1[(size_t)kk * d + n] : 0.f);
+      pb1[n] = n < d ? b1[n] : 0.f;
+    }
+    pb1[np] = std::ldexp(1.f, -E1);
+  }
+  pack_conv_x3(g, k, L.upd0, 2 * d + 2, t[i_upd], t[i_upd + 1], map_update, base);
+  pack_conv_x3(g, k, L.upd1, d, t[i_upd + 2], t[i_upd + 3], map_identity_hidden, base);
+  return NRX_OK;
+}
 
 int pack_weights_tc(const nrx_model_desc* m, int prec, const float* const* t, uint8_t* base) {
   PackLayout L;
@@ -407,7 +566,8 @@ int pack_weights_f32(const nrx_model_desc* m, const float* const* t, uint8_t* ba
 
 void ws_layout(const Geom& g, WsLayout* w) {
   const size_t esz = g.prec == NRX_FP32 ? 4 : 2;
-  const size_t plane = (size_t)g.NU * g.rows_slab * esz;
+  // fp32x3: every activation buffer holds its hi and lo planes (2x channels)
+  const size_t plane = (size_t)g.NU * g.rows_slab * esz * (g.prec == NRX_FP32X3 ? 2 : 1);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
   w->feats = take(plane * g.Cf);
@@ -475,6 +635,10 @@ int nrx_pack_weights(const nrx_model_desc* m, int prec, const float* const* tens
   for (int i = 0; i < n; ++i)
     if (!tensors[i]) return NRX_ERR_INVALID;
   if (prec == NRX_FP32) return pack_weights_f32(m, tensors, (uint8_t*)out);
+  if (prec == NRX_FP32X3) {
+    if (m->hidden > 128) return NRX_ERR_UNSUPPORTED;
+    return pack_weights_x3(m, tensors, (uint8_t*)out);
+  }
   if (prec == NRX_BF16 || prec == NRX_FP16) {
     if (m->hidden > 128) return NRX_ERR_UNSUPPORTED;
     return pack_weights_tc(m, prec, tensors, (uint8_t*)out);

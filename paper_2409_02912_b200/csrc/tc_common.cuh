@@ -79,6 +79,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
   while (!mbar_try_wait(a, parity)) {
   }
 }
+// Long waits of roles that share SM sub-partitions with the MMA warp (the
+// epilogue waiting a whole tile for its accumulator, the producer waiting for
+// a free stage): back off between polls so the spin does not take issue slots
+// from the MMA issuer.
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t a, uint32_t parity, uint32_t ns) {
+  while (!mbar_try_wait(a, parity)) __nanosleep(ns);
+}
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -145,6 +152,30 @@ __device__ __forceinline__ void mma_bf16_warp(uint32_t d_tmem, uint64_t adesc, u
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// fp32x3: D = A B + D 2^-11 (scale-input-d) folds the lo*Whi partial sums,
+// accumulated at scale 2^11, into the hi terms (accumulate always on)
+__device__ __forceinline__ void mma_fold_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1, 11;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc)
+      : "memory");
+}
+// fp32x3 GEMM over nk K=16 steps: lo*Whi for every step, then hi*Wlo (the
+// first one folding the lo sums in), then hi*Whi.  The tensor core's fp32
+// accumulation truncates (~0.2 ulp of D per MMA towards zero,
+// scripts/acc_probe.cu), so the small terms go first and only the last nk
+// MMAs run at the full magnitude of D.  A: [2 planes][K/8 chunks][rows][8]
+// (hi plane first, a_lo = plane distance in 16-B units), B: [hi | lo][K/8][N][8]
+// (b_lo likewise).
+__device__ __forceinline__ void mma_x3_gemm(uint32_t d, uint64_t a_hi, uint32_t a_lo, uint32_t a_k, uint64_t b_hi,
+                                            uint32_t b_lo, uint32_t b_k, int nk, uint32_t idesc) {
+  for (int k = 0; k < nk; ++k) mma_bf16_warp(d, a_hi + a_lo + k * a_k, b_hi + k * b_k, idesc, k != 0);
+  mma_fold_warp(d, a_hi, b_hi + b_lo, idesc);
+  for (int k = 1; k < nk; ++k) mma_bf16_warp(d, a_hi + k * a_k, b_hi + b_lo + k * b_k, idesc, 1);
+  for (int k = 0; k < nk; ++k) mma_bf16_warp(d, a_hi + k * a_k, b_hi + k * b_k, idesc, 1);
+}
 __device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -185,6 +216,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
       : "r"(taddr));
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 

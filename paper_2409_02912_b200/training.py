@@ -235,7 +235,7 @@ def gpu_features(config, cfg, batch, n0):
     from .nrx import noise_features
     lib = _lib.load()
     n, U, S, T = batch.y.shape[0], cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols
-    geo = _lib.buffer_geometry(config, cfg, "fp32")
+    geo = _lib.buffer_geometry(config, cfg, "fp32_simt")
     out = torch.zeros(n * U, geo["Cf"] // 4, geo["rows_slab"], 4, device=batch.y.device)
     nf = torch.as_tensor(noise_features(np.asarray(n0, dtype=np.float64), n), device=batch.y.device)
     st = torch.cuda.current_stream(batch.y.device).cuda_stream

@@ -53,8 +53,11 @@ def test_weight_names_match_expected_shapes(variant, supported, kw):
 def test_pack_weights_deterministic_and_sized():
     config = NrxConfig(d_s=56, num_iterations=2)
     w = init_weights(config, 0)
-    a = pack_weights(config, w, "fp32")
-    b = pack_weights(config, {k: v.copy() for k, v in w.items()}, "fp32")
+    for prec in ("fp32", "bf16", "fp16"):  # tensor-core blobs: deterministic too
+        np.testing.assert_array_equal(pack_weights(config, w, prec),
+                                      pack_weights(config, {k: v.copy() for k, v in w.items()}, prec))
+    a = pack_weights(config, w, "fp32_simt")
+    b = pack_weights(config, {k: v.copy() for k, v in w.items()}, "fp32_simt")
     np.testing.assert_array_equal(a, b)
     # every weight value lands somewhere in the packed blob (no value dropped)
     packed = a.view(np.float32)
@@ -81,12 +84,14 @@ def test_validate_limits():
 def test_workspace_and_geometry():
     config = NrxConfig(d_s=56, num_iterations=2)
     cfg = SlotConfig(num_subcarriers=3276, num_ues=2)
-    geo = _lib.buffer_geometry(config, cfg, "fp32")
-    assert geo["Tp"] == 15 and geo["rows_slab"] % 128 == 0 and geo["rows_slab"] >= 3276 * 15
-    assert geo["Cs"] >= 58 and geo["Cf"] >= 19
     lib = _lib.load()
-    nb = lib.nrx_workspace_bytes(ctypes.byref(_lib.model_desc(config)), ctypes.byref(_lib.slot_desc(cfg)), 4, 0)
-    assert nb >= 4 * 2 * geo["rows_slab"] * 4 * (geo["Cf"] + geo["Cs"] + geo["Ch"] + geo["Ca"])
+    for prec, esz in (("fp32_simt", 4), ("fp32", 4), ("fp16", 2)):  # fp32x3: fp16 hi + lo planes
+        geo = _lib.buffer_geometry(config, cfg, prec)
+        assert geo["Tp"] == 15 and geo["rows_slab"] % 128 == 0 and geo["rows_slab"] >= 3276 * 15
+        assert geo["Cs"] >= 58 and geo["Cf"] >= 19
+        nb = lib.nrx_workspace_bytes(ctypes.byref(_lib.model_desc(config)), ctypes.byref(_lib.slot_desc(cfg)), 4,
+                                     _lib.PRECISIONS[prec])
+        assert nb >= 4 * 2 * geo["rows_slab"] * esz * (geo["Cf"] + geo["Cs"] + geo["Ch"] + geo["Ca"])
 
 
 def test_pilot_comb_values_layout():
@@ -102,7 +107,8 @@ def test_pilot_comb_values_layout():
     ("fp16", 2, 2, 7),   # ls_feat, init.conv0, init.conv1+msg, 2 x (update.conv0, update.conv1+tail)
     ("bf16", 2, 8, 19),
     ("fp16", 1, 2, 9),   # U != 2: standalone message kernel per iteration
-    ("fp32", 2, 2, 10),  # SIMT parity path: ls_feat, 2 init convs, 3 per iteration, readout
+    ("fp32_simt", 2, 2, 10),  # SIMT parity path: ls_feat, 2 init convs, 3 per iteration, readout
+    ("fp32", 2, 2, 10),       # fp32x3 tensor-core path: same sequence on CTA pairs
 ])
 def test_forward_launch_count(precision, num_ues, n_it, expect):
     """nrx_forward_launch_count is the per-forward kernel count bench.py
@@ -111,5 +117,5 @@ def test_forward_launch_count(precision, num_ues, n_it, expect):
     cfg = SlotConfig(num_subcarriers=3276, num_ues=num_ues, comb_size=2)
     lib = _lib.load()
     m, s = _lib.model_desc(config), _lib.slot_desc(cfg)
-    prec = {"fp32": 0, "bf16": 1, "fp16": 2}[precision]
+    prec = _lib.PRECISIONS[precision]
     assert lib.nrx_forward_launch_count(ctypes.byref(m), ctypes.byref(s), prec, n_it) == expect

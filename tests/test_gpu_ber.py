@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CKPT = os.path.join(HERE, "golden", "desk_d16_it2.nrxw")
-BAND = {"fp32": 1e-5, "bf16": 2e-2, "fp16": 5e-3}
+BAND = {"fp32": 1e-5, "fp32_simt": 1e-5, "bf16": 2e-2, "fp16": 5e-3}
 
 
 def _batch(n_slots=24, S=96, snr_db=10.0, seed=21):
@@ -40,7 +40,7 @@ def _errors(llrs, bits, cfg):
     return ber, block, bit_err
 
 
-@pytest.mark.parametrize("precision", ["fp32", "bf16", "fp16"])
+@pytest.mark.parametrize("precision", ["fp32", "fp32_simt", "bf16", "fp16"])
 def test_uncoded_ber_matches_reference(precision):
     from paper_2409_02912_b200.config import checkpoint_load, default_mcs_table
     from paper_2409_02912_b200.nrx import nrx_forward
@@ -66,7 +66,7 @@ def test_uncoded_ber_matches_reference(precision):
     assert abs(ber_got - ber_ref) <= disagree / n_bits + 1e-12
     sigma = np.sqrt(ber_ref * (1 - ber_ref) / n_bits)
     assert abs(ber_got - ber_ref) <= 3 * sigma
-    if precision == "fp32":
+    if precision.startswith("fp32"):
         np.testing.assert_array_equal(blk_got, blk_ref)          # block errors identical
     else:
         assert np.mean(blk_got != blk_ref) <= 0.05

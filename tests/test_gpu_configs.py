@@ -16,7 +16,7 @@ from test_gpu_parity import check_chest, check_llrs
 
 pytestmark = pytest.mark.gpu
 
-PRECISIONS = ["fp32", "bf16", "fp16"]
+PRECISIONS = ["fp32", "fp32_simt", "bf16", "fp16"]
 
 
 def _run(cfg, config, w, mcs, n_slots, seed, precision, num_iterations=None, n0=0.1):

@@ -1,7 +1,7 @@
 """GPU parity of the CUDA path against the reference (golden vectors) and the
 CPU oracle.  Gates (stated per test):
 
-  fp32 mode:  max|dLLR| <= 1e-5 * max|LLR_ref|
+  fp32 mode:  max|dLLR| <= 1e-5 * max|LLR_ref|  (tensor-core fp32x3 and SIMT fp32_simt)
   bf16 mode:  max|dLLR| <= 2e-2 * max|LLR_ref|,  p99|dLLR| <= 5e-3 * max|LLR_ref|
   fp16 mode:  max|dLLR| <= 5e-3 * max|LLR_ref|,  p99|dLLR| <= 1.5e-3 * max|LLR_ref|
   hard bits (LLR > 0) bit-exact wherever |LLR_ref| exceeds the mode's bound.
@@ -19,7 +19,7 @@ from oracle import nrx_oracle as orc
 pytestmark = pytest.mark.gpu
 
 CASES = case_names()
-GATES = {"fp32": dict(max=1e-5, p99=1e-5), "bf16": dict(max=2e-2, p99=5e-3), "fp16": dict(max=5e-3, p99=1.5e-3)}
+GATES = {"fp32": dict(max=1e-5, p99=1e-5), "fp32_simt": dict(max=1e-5, p99=1e-5), "bf16": dict(max=2e-2, p99=5e-3), "fp16": dict(max=5e-3, p99=1.5e-3)}
 
 
 def _gpu():
@@ -56,7 +56,7 @@ def check_chest(got, ref, precision):
     assert np.abs(got - ref).max() <= gate["max"] * scale
 
 
-@pytest.mark.parametrize("precision", ["fp32", "bf16", "fp16"])
+@pytest.mark.parametrize("precision", ["fp32", "fp32_simt", "bf16", "fp16"])
 @pytest.mark.parametrize("name", CASES)
 def test_golden_forward(name, precision):
     """Drop-in nrx_forward vs the reference's own outputs on reference inputs."""
@@ -79,7 +79,7 @@ def test_golden_features(name, exact):
     from paper_2409_02912_b200.nrx import noise_features, stack_pilots
     c = load_case(name)
     n = c.y.shape[0]
-    geo = _lib.buffer_geometry(c.config, c.cfg, "fp32")
+    geo = _lib.buffer_geometry(c.config, c.cfg, "fp32_simt")
     lib = _lib.load()
     cdt = torch.complex128 if exact else torch.complex64
     y = torch.from_numpy(c.y).to(cdt).cuda()
@@ -105,6 +105,42 @@ def test_golden_features(name, exact):
         np.testing.assert_allclose(got, c.features, rtol=0, atol=1e-6 * np.abs(c.features).max())
 
 
+@pytest.mark.parametrize("name", CASES[:3])
+def test_golden_features_fp32x3_split(name):
+    """K1 in the fp32x3 layout: hi plane (chunks [0, Cf/8)) + lo plane
+    (chunks [Cf/8, Cf/4), scaled by 2^11) reconstruct the reference features
+    to 2^-22 relative (+ 2^-25 absolute for the lo plane's subnormal floor)."""
+    torch, _ = _gpu()
+    from paper_2409_02912_b200 import _lib
+    from paper_2409_02912_b200.nrx import noise_features, stack_pilots
+    c = load_case(name)
+    n = c.y.shape[0]
+    geo = _lib.buffer_geometry(c.config, c.cfg, "fp32")
+    assert geo["cw"] == 8
+    lib = _lib.load()
+    y = torch.from_numpy(c.y).to(torch.complex128).cuda()
+    p = torch.from_numpy(stack_pilots(c.books, n, c.cfg)).to(torch.complex128).cuda()
+    nf = torch.from_numpy(noise_features(c.n0, n)).cuda()
+    U = c.cfg.num_ues
+    nch = geo["Cf"] // 8
+    out = torch.zeros(n * U, 2 * nch, geo["rows_slab"], 8, dtype=torch.float16, device="cuda")
+    code = lib.nrx_ls_features(ctypes.byref(_lib.model_desc(c.config)), ctypes.byref(_lib.slot_desc(c.cfg)), n,
+                               _lib.NRX_FP32X3, y.data_ptr(), 1, p.data_ptr(), 1, p.shape[0], nf.data_ptr(),
+                               out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert code == 0
+    torch.cuda.synchronize()
+    o = out.float().cpu().numpy().astype(np.float64)
+    rec = o[:, :nch] + o[:, nch:] / 2048.0
+    f = rec.transpose(0, 2, 1, 3).reshape(n * U, geo["rows_slab"], geo["Cf"])
+    S, T = c.cfg.num_subcarriers, c.cfg.num_symbols
+    f = f[:, :S * geo["Tp"]].reshape(n, U, S, geo["Tp"], geo["Cf"])
+    cin = c.features.shape[-1]
+    assert not f[:, :, :, T:].any() and not f[..., cin:].any()
+    want = c.features.astype(np.float64)
+    err = np.abs(f[:, :, :, :T, :cin] - want)
+    assert np.all(err <= 2.0 ** -22 * np.abs(want) + 2.0 ** -25)
+
+
 def _c2_setup(d=56, n_it=2, U=2, S=3276, variant="single", supported=(14,), seed=0, bias=True):
     from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights
     from paper_2409_02912_b200.synth import synth_slots
@@ -117,7 +153,7 @@ def _c2_setup(d=56, n_it=2, U=2, S=3276, variant="single", supported=(14,), seed
     return cfg, config, w, table
 
 
-@pytest.mark.parametrize("precision", ["fp32", "bf16", "fp16"])
+@pytest.mark.parametrize("precision", ["fp32", "fp32_simt", "bf16", "fp16"])
 def test_c2_rt_slot_vs_oracle(precision):
     """273 PRB / 2 UE / 4 RX / RT model (d=56, N_it=2): the benchmark config."""
     _, gnrx = _gpu()
