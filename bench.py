@@ -37,6 +37,16 @@ DATA = ("synthetic: GPU slot generator on the SURVEY §8d recipe (doubletdl TDL-
 METRIC = "NRX forward slots/s at 273 PRB (2 UE, 4 RX, RT d_s=56 N_it=2); p50/p99 single-slot latency in latency_us"
 
 
+DTYPES = {"fp32": "fp32", "fp32_simt": "fp32", "bf16": "bf16", "fp16": "fp16"}
+PRECISION_NOTES = {
+    "fp32": "fp32x3: every fp32 operand split into fp16 hi + lo (22 significant bits), three tcgen05 kind::f16 "
+            "MMAs per product into fp32 TMEM accumulators; parity gate max|dLLR| <= 1e-5 max|LLR_ref| (the "
+            "reference's fp32 gate)",
+    "fp32_simt": "fp32 FFMA (SIMT), fp64 LS and sum of others; same gate",
+    "bf16": "bf16 operands on tcgen05, fp32 accumulate, fp32 residual stream; gate 2e-2 (max) / 5e-3 (p99)",
+    "fp16": "fp16 operands on tcgen05, fp32 accumulate; gate 5e-3 (max) / 1.5e-3 (p99)"}
+
+
 def c2_setup():
     from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights
     table = default_mcs_table()
@@ -305,13 +315,15 @@ def run_ours(args):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
-    with sampler, _lib.KernelTimer(("conv_update0",), max_records=4 * args.steps * N_IT + 16) as kt:
+    with sampler, _lib.KernelTimer(("conv_update0", "ls_feat"), max_records=4 * args.steps * N_IT + 16) as kt:
         e0.record(stream)
         for i in range(args.steps):
             step(i)
         e1.record(stream)
         torch.cuda.synchronize()
-        kernel_ms = kt.collect().get("conv_update0", [])
+        kt_rec = kt.collect()
+        kernel_ms = kt_rec.get("conv_update0", [])
+        lsfeat_ms = kt_rec.get("ls_feat", [])
     elapsed = e0.elapsed_time(e1) / 1e3
     if world > 1:
         t = torch.tensor([elapsed], device=dev)
@@ -352,11 +364,17 @@ def run_ours(args):
     if args.precision in ("bf16", "fp16"):  # same tcgen05 kind::f16 rate for both
         peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
         peak_note = f"bf16 dense, sustained ({peak_src}); fp16 runs at the same tensor rate"
+    elif args.precision == "fp32":
+        # fp32x3: every fp32 MAC is three fp16 tensor-core MACs (lo*Whi, hi*Whi, hi*Wlo)
+        peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / 3.0
+        peak_note = (f"fp32-equivalent tensor-core ceiling = bf16 dense sustained ({peak_src}) / 3: the "
+                     "fp16 hi/lo split issues three kind::f16 MMAs per fp32 MAC")
     else:
         sm_mhz = peaks.get("sm_max_mhz", 1965.0)
         peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
         peak_note = "fp32 FFMA nominal (148 SM x 128 lanes x 2 x max clock)"
     traffic = traffic_from_profiles("conv_update0", args.precision, B)
+    lsfeat = lsfeat_bandwidth(lsfeat_ms, B, cfg, config, args.precision, peaks, peak_src)
 
     # single-slot latency (device resident), CUDA graph of the whole forward
     lat = latency_single_slot(eng, cfg, dev, args.latency_runs) if rank == 0 else None
@@ -371,10 +389,14 @@ def run_ours(args):
     # the other §8(f) rows on the same slots: LDPC decode / encode, classical baselines
     nxt = next_rows(cfg, B, dev) if rank == 0 and not args.no_precision_sweep else None
 
+    # the C5 job: 4096 independent slots, contiguous shards per rank
+    c5 = c5_job(eng, cfg, args.c5_slots, B, world, rank, dev) if args.c5_slots > 0 else None
+
     # the other precisions on the same device-resident workload (shorter runs)
-    by_prec = {args.precision: {"slots_per_s": round(value, 2), "ms_per_step": round(ms_per_step, 4)}}
+    by_prec = {args.precision: {"slots_per_s": round(value, 2), "ms_per_step": round(ms_per_step, 4),
+                                "latency_us": {k: lat[k] for k in ("p50", "p99")} if lat else None}}
     if not args.no_precision_sweep:
-        for prec in ("fp32", "bf16", "fp16"):
+        for prec in ("fp32", "fp32_simt", "bf16", "fp16"):
             if prec == args.precision:
                 continue
             other = NrxEngine(config, w, precision=prec, device=dev)
@@ -384,7 +406,7 @@ def run_ours(args):
                 y, pil, nf, mods = sets[i & 1]
                 other.forward_device(cfg, y, pil, nf, mods, N_IT, llr, chest, workspace=ows, stream=stream)
 
-            n_steps = max(3, args.steps // (10 if prec == "fp32" else 4))
+            n_steps = max(3, args.steps // (10 if prec == "fp32_simt" else 4))
             for i in range(3):
                 ostep(i)
             torch.cuda.synchronize()
@@ -397,6 +419,9 @@ def run_ours(args):
             t = max_over_ranks(a.elapsed_time(b) / 1e3, dev)
             by_prec[prec] = {"slots_per_s": round(B * n_steps * world / t, 2),
                              "ms_per_step": round(t / n_steps * 1e3, 4), "steps": n_steps}
+            if rank == 0:
+                ol = latency_single_slot(other, cfg, dev, max(200, args.latency_runs // 10))
+                by_prec[prec]["latency_us"] = {k: ol[k] for k in ("p50", "p99")}
             del other, ows
             torch.cuda.empty_cache()
 
@@ -405,7 +430,8 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 2), "unit": "slots/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": args.precision, "data": DATA,
+        "dtype": DTYPES[args.precision], "data": DATA,
+        "precision_note": PRECISION_NOTES[args.precision],
         "config": {"workload": f"C5-style batches of C2 slots: {B} slots/GPU/step of 273 PRB x 14 sym, "
                                f"2 UE 16-QAM, 4 RX; RT NRX d_s=56 N_it=2 (configs[1] geometry)",
                    "slots_per_step_per_gpu": B, "precision": args.precision,
@@ -426,6 +452,8 @@ def run_ours(args):
                      "share_of_step": round(kavg * 1e3 * N_IT / ms_per_step, 4) if kernel_ms else None},
         "whole_path": {"algorithmic_tflops": round(algorithmic_flops_per_slab_re() * U * S * T * value / world / 1e12, 2),
                        "flop_per_slot": algorithmic_flops_per_slab_re() * U * S * T},
+        "memory_bound_stage": lsfeat,
+        "c5_job": c5,
         "by_precision": by_prec,
         "gpu_launches": n_launch * args.steps,
         "launches_per_step": n_launch,
@@ -441,6 +469,85 @@ def run_ours(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def lsfeat_bandwidth(ms_list, B, cfg, config, precision, peaks, peak_src):
+    """Achieved HBM bandwidth of K1 (LS + feature assembly, the HBM-bound stage
+    SURVEY §8d names): bytes it moves per launch / its device time."""
+    if not ms_list:
+        return None
+    from paper_2409_02912_b200 import _lib
+    geo = _lib.buffer_geometry(config, cfg, precision)
+    U, S, T, BR = cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols, config.num_rx_ant
+    F = -(-S // cfg.comb_size)
+    y_bytes = B * S * T * BR * 8
+    pil_bytes = B * U * F * len(cfg.pilot_symbols) * 8
+    planes = 2 if precision == "fp32" else 1
+    esz = 4 if precision == "fp32_simt" else 2
+    written = B * U * geo["rows_slab"] * geo["Cf"] * esz * planes     # every row and channel of the buffer
+    cin = 4 * BR + 2 + int(bool(config.include_noise_plane))
+    alg = y_bytes + pil_bytes + B * U * S * T * cin * esz * planes   # SURVEY §8d: y + pilots + C_in features
+    t = float(np.mean(ms_list)) / 1e3
+    peak = peaks.get("hbm_gbs", 6450.0)
+    return {"kernel": "ls_feat (LS + feature assembly, K1)", "bound": "hbm", "avg_launch_ms": round(t * 1e3, 4),
+            "bytes_moved_per_launch": int(y_bytes + pil_bytes + written), "algorithmic_bytes_per_launch": int(alg),
+            "achieved_gbs": round((y_bytes + pil_bytes + written) / t / 1e9, 1),
+            "algorithmic_gbs": round(alg / t / 1e9, 1), "peak_gbs": peak,
+            "frac": round((y_bytes + pil_bytes + written) / t / 1e9 / peak, 4),
+            "peak_source": f"measured HBM copy bandwidth ({peak_src})", "launches_timed": len(ms_list)}
+
+
+def c5_job(eng, cfg, total, B, world, rank, dev):
+    """BASELINE.json configs[4] / SURVEY §8e: `total` independent C2 slots,
+    contiguous shards (slot i -> rank floor(i world / total)), every slot
+    distinct (GPU generator keyed by the global slot index) and pre-staged in
+    HBM; each rank runs its shard in batches of B.  Timed compute-only and
+    with the gather of every batch's LLRs to rank 0 (NCCL over NVLink), on
+    the device, max over ranks."""
+    import torch
+    from paper_2409_02912_b200.shard import StepGather, max_over_ranks, shard_slots
+    shard = shard_slots(total, rank, world)
+    U, S, T = cfg.num_ues, cfg.num_subcarriers, cfg.num_symbols
+    batches = []
+    for b0 in range(shard.start, shard.stop, B):
+        nb = min(B, shard.stop - b0)
+        batches.append(gpu_batch(cfg, nb, dev, seed=4096, first_slot=b0))
+    llr = torch.empty((B, U, S, T, 4), dtype=torch.float32, device=dev)
+    chest = torch.empty((B, U, S, T, 4), dtype=torch.complex64, device=dev)
+    ws = eng.workspace(cfg, B)
+    st = torch.cuda.current_stream(dev)
+    gat = StepGather(llr) if world > 1 else None
+
+    def run(gather):
+        for y, pil, nf, mods in batches:
+            nb = y.shape[0]
+            eng.forward_device(cfg, y, pil, nf, mods, N_IT, llr[:nb], chest[:nb], workspace=ws, stream=st)
+            if gather and gat is not None:
+                gat(llr)
+
+    out = {"total_slots": total, "slots_this_rank": len(shard), "batches_per_rank": len(batches),
+           "batch_slots": B}
+    run(False)  # warm-up (also the NCCL communicator)
+    if gat is not None:
+        run(True)
+    for name, gather in (("compute_only", False), ("with_gather", True)):
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        run(gather)
+        b.record(st)
+        torch.cuda.synchronize()
+        t = max_over_ranks(a.elapsed_time(b) / 1e3, dev)
+        out[name] = {"job_s": round(t, 5), "slots_per_s": round(total / t, 1)}
+    out["gather_bytes_into_rank0"] = int(llr.numel() * llr.element_size() * len(batches) * max(0, world - 1))
+    out["note"] = ("inputs generated on each rank's GPU before timing; with_gather adds NCCL gathers of every "
+                   "batch's (B,U,S,T,4) float32 LLRs into rank 0 (at N=1 rank 0 already holds them)")
+    del batches
+    torch.cuda.empty_cache()
+    return out
 
 
 def latency_single_slot(eng, cfg, dev, runs: int, n_it: int = N_IT, orders=None, width: int = 4,
@@ -587,7 +694,7 @@ def dropin_latency(cfg, config, w, mcs, runs: int = 20):
     from paper_2409_02912_b200.synth import synth_slots
     y, books, _ = synth_slots(cfg, [4, 4], 2, 0.1, seed=5)
     out = {}
-    for prec in ("fp16", "fp32"):
+    for prec in ("fp32", "fp32_simt", "fp16"):
         for i in range(3):
             nrx_forward(y[i % 2], books[i % 2], cfg, mcs, w, config, 0.1, precision=prec)
         ts = []
@@ -722,13 +829,66 @@ def e2e_throughput(eng, cfg, B, steps, world, dev):
                    "H2D/compute/D2H overlapped across steps; wall clock incl. final sync)"}
 
 
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) without a torchrun environment:
+    re-exec this script as N ranks (one process per GPU) under
+    torch.distributed.run on 127.0.0.1, failing loudly when fewer than N GPUs
+    are visible (the reference arm and --launch-check need no GPUs)."""
+    if args.impl == "ours" and not args.launch_check:
+        import torch
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} requested but only {n} CUDA device(s) are visible")
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def launch_check():
+    """One process per rank joins a process group (NCCL with GPUs, else gloo)
+    and rank 0 prints the world size and the ranks that answered."""
+    import torch
+    import torch.distributed as dist
+    world, rank, local = dist_env()
+    if world > 1:
+        backend = "nccl" if torch.cuda.is_available() and torch.cuda.device_count() >= world else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dev = torch.device("cuda", local)
+        else:
+            dist.init_process_group("gloo")
+            dev = torch.device("cpu")
+        t = torch.tensor([rank], dtype=torch.int64, device=dev)
+        got = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(got, t)
+        ranks = [int(x.item()) for x in got]
+        dist.destroy_process_group()
+    else:
+        backend, ranks = "none", [0]
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "world": world, "ranks": ranks, "backend": backend}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--precision", choices=("bf16", "fp16", "fp32"), default=os.environ.get("NRX_BENCH_PRECISION", "fp16"))
+    ap.add_argument("--precision", choices=("fp32", "fp32_simt", "bf16", "fp16"),
+                    default=os.environ.get("NRX_BENCH_PRECISION", "fp32"),
+                    help="fp32: the reference's fp32 accuracy on the tensor cores (headline); fp32_simt: same "
+                         "gate on FFMA; bf16 / fp16: reduced-precision modes (reported in by_precision)")
+    ap.add_argument("--c5-slots", type=int, default=4096, help="C5 job size (BASELINE.json configs[4]); 0: skip")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="only start the ranks (re-exec under torch.distributed.run for --gpus N > 1), join a "
+                         "process group and print the world size rank 0 sees")
     ap.add_argument("--slots-per-step", type=int, default=32)
     ap.add_argument("--latency-runs", type=int, default=10000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -738,6 +898,14 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and (args.impl == "ours" or args.launch_check):
+        relaunch_under_torchrun(args)  # does not return
+    if world != args.gpus and args.impl == "ours" and not args.launch_check:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
+    if args.launch_check:
+        launch_check()
+        return
     if args.impl == "reference":
         world, rank, _ = dist_env()
         if rank != 0:

@@ -32,12 +32,16 @@ def max_over_ranks(value: float, device=None) -> float:
 
 def gather_slot_results(local: np.ndarray, n_slots: int, device=None, dst: int = 0):
     """Gather per-slot result rows (leading axis = this rank's shard) to
-    `dst` in global slot order; returns the full array on dst, None elsewhere."""
+    `dst` in global slot order; returns the full array on dst, None elsewhere.
+    `device` defaults to the rank's current CUDA device under NCCL and to the
+    host under gloo."""
     import torch
     import torch.distributed as dist
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
         return local
     world, rank = dist.get_world_size(), dist.get_rank()
+    if device is None:  # NCCL moves device tensors only: this rank's GPU; gloo: host memory
+        device = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else "cpu"
     sizes = [len(shard_slots(n_slots, r, world)) for r in range(world)]
     row_shape = local.shape[1:]
     pad = max(sizes)

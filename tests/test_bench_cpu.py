@@ -52,3 +52,34 @@ def test_clock_sampler_without_nvidia_smi(monkeypatch, tmp_path):
     with s:
         pass
     assert s.summary()["reasons"] == ["nvidia-smi unavailable"]
+
+
+def _run_bench(*args, env_extra=None, timeout=240):
+    import subprocess
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env.update(env_extra or {})
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                          env=env, timeout=timeout, cwd=ROOT)
+
+
+def test_gpus_flag_spawns_one_rank_per_gpu():
+    """`bench.py --gpus 2` outside torchrun re-executes itself as 2 ranks
+    (torch.distributed.run on 127.0.0.1) that join one process group."""
+    import json
+    r = _run_bench("--gpus", "2", "--launch-check")
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["world"] == 2 and sorted(out["ranks"]) == [0, 1]
+
+
+def test_gpus_flag_fails_loudly_without_enough_gpus():
+    import torch
+    if torch.cuda.device_count() >= 4:
+        return
+    r = _run_bench("--gpus", "4", "--steps", "1")
+    assert r.returncode != 0 and "CUDA device" in (r.stderr + r.stdout)
+
+
+def test_world_size_must_match_gpus():
+    r = _run_bench("--gpus", "3", "--steps", "1", env_extra={"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode != 0 and "WORLD_SIZE=2" in (r.stderr + r.stdout)
