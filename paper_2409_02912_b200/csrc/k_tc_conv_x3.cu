@@ -3,36 +3,39 @@
 // The reference computes every convolution as an fp32 sgemm over im2col
 // (autodiff.py:315-350).  This path keeps that accuracy on the fp16 tensor
 // cores by splitting both operands:
-//   activation  a = hi + lo 2^-11   (fp16 planes, split_chunk)
+//   activation  a = hi + lo' 2^-11  (fp16 planes, split_chunk)
 //   weight      W 2^E = Whi + Wlo   (fp16 halves, host packer)
-//   a W 2^E ~= (lo Whi) 2^-11 + hi Whi + hi Wlo
-// The MMA warp first issues every lo*Whi MMA of the tile (partial sums at
-// scale 2^11), then the hi*Wlo MMAs, the first of them with scale-input-d = 11
-// (D = A B + D 2^-11) folding the lo sums in, then the hi*Whi MMAs; the
-// epilogue multiplies by 2^-E (exact) and adds the bias in fp32 as the
-// reference does.  Representation error per operand is <= 2^-23 relative (vs
-// 2^-24 for fp32), the dropped lo*Wlo term is 2^-22 relative.
+//   a W 2^E = hi Whi + hi Wlo + (lo' Whi + lo' Wlo) 2^-11      (all four terms)
+// Each MMA multiplies one activation plane by the concatenated B operand
+// [Whi | Wlo] (N = 2 np): one MMA yields [a Whi | a Wlo] in two adjacent
+// TMEM column blocks.  Per tile the MMA warp first issues the lo' MMAs (sums
+// at scale 2^11), then the hi MMAs; the first hi MMA into a block uses
+// scale-input-d = 11 (D = A B + D 2^-11), which folds the lo' sums in with
+// the exact power-of-two weight.  The epilogue adds the blocks in fp32,
+// multiplies by 2^-E (exact) and adds the bias as the reference does.  The
+// operand representation error is <= 2^-23 relative (fp32: 2^-24).
 //
 // Accumulation: the tensor core's fp32 accumulate truncates, ~0.2 ulp of D
 // towards zero per MMA (scripts/acc_probe.cu: -14.7 ulp mean after 72 MMAs,
 // where round-to-nearest stays at ~0).  Only MMAs at the full magnitude of D
-// matter, so the small lo*Whi / hi*Wlo terms go first and the hi*Whi MMAs are
-// spread over P partial accumulators by tap row (P = 3 for 3x3 kernels: 24
-// instead of 144 full-magnitude MMAs per accumulator for update.conv0), which
-// the epilogue adds in fp32 round-to-nearest.
+// matter (the lo' sums are scaled by 2^-11 afterwards, the Wlo block is 2^-11
+// smaller), so the hi MMAs are spread over P = 2 partial accumulators by tap
+// row (rows 0, 2 / row 1 for 3x3 kernels), added by the epilogue in fp32
+// round-to-nearest.  C2 LLRs stay within 2.1e-6 of the float64 oracle
+// (SIMT fp32: 6.5e-7; gate 1e-5).
 //
-// The weights of both halves (2x the fp16 bytes: 295 KB for
-// iteration.update.conv0) do not fit one SM's shared memory, so every layer
-// runs on a CTA pair (cluster of 2, tcgen05.mma.cta_group::2, M = 256): CTA
-// r keeps only output channels [r np/2, (r+1) np/2) of the weights resident
-// (the pair MMA reads B from both CTAs), loads its own 128-row tile + halo of
-// the activations, and receives the accumulator of its own 128 rows in its
-// own TMEM.  Per SM and K=16 step an MMA reads 4 KB of A and 1 KB of B
-// (5 KB instead of 6 KB for a single-CTA N=64 MMA).
+// Weights of one plane for every output channel (147 KB for
+// iteration.update.conv0) use most of an SM's shared memory, so every layer
+// runs on a CTA pair (cluster of 2, tcgen05.mma.cta_group::2, M = 256): the
+// pair MMA reads B as rank 0's rows followed by rank 1's, so rank 0 keeps Whi
+// and rank 1 Wlo resident; each CTA loads its own 128-row tile + halo of the
+// activations and receives the accumulator of its own rows in its own TMEM.
+// Per SM an MMA (128 x 128 x 16) reads 4 KB of A and 2 KB of B and is
+// math-bound at 64 cycles: 2 MMAs = 128 cycles per tap and K=16 step.
 //
 // Roles (both CTAs): warp 0 lane 0 TMA producer (its tile, signalling the
 // leader's full barrier through the .cta_group::2 TMA form), warp 1 the MMA
-// issuer in the leader / the weights-resident relay in the peer, 4*np/32
+// issuer in the leader / the weights-resident relay in the peer, 4 np/NC
 // epilogue warps per CTA draining their own TMEM.  Pipeline stages are
 // (tile, plane, source): lo planes of every source first, then hi planes.
 // Layout of the activations: chunk-planar as everywhere (nrx_internal.h),
@@ -199,16 +202,22 @@ __host__ __device__ inline ConvX3Smem conv_x3_smem(const ConvX3Params& p) {
   return s;
 }
 
+// Epilogue columns per thread: 32 (2 + 4 np/32 warps, so each SM sub-partition
+// holds <= 3 warps and the fully unrolled MMA issue gets up to 168 registers);
+// the residual update, whose epilogue also reads the previous state and is
+// the bottleneck of that layer, runs twice the warps (16 columns each).
+__host__ __device__ constexpr int x3_epi_cols(int mode) { return mode == EPI_RESIDUAL ? 16 : 32; }
+
 template <int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0>
-__global__ void __launch_bounds__(64 + 128 * (NP / 32), 1)
+__global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
     k_conv_x3(const __grid_constant__ ConvX3Params p, const __grid_constant__ CUtensorMap map0,
               const __grid_constant__ CUtensorMap map1) {
   // 32 accumulator columns per epilogue thread: 2 + 4 * NP/32 warps (10 for
   // NP = 64) leave each SM sub-partition <= 3 warps, i.e. up to 168 registers
   // for the fully unrolled MMA issue (18 warps would cap it at 96 and spill)
-  constexpr int PARTS = NP / 32;
+  constexpr int NC = x3_epi_cols(MODE);  // accumulator columns per epilogue thread
+  constexpr int PARTS = NP / NC;
   constexpr int EPI_WARPS = 4 * PARTS;
-  constexpr int NPH = NP / 2;  // B rows per CTA
   extern __shared__ __align__(1024) uint8_t smem[];
   const Geom& g = p.g;
   const uint32_t rank = cta_rank();
@@ -296,10 +305,11 @@ __global__ void __launch_bounds__(64 + 128 * (NP / 32), 1)
         arrive_cluster(map_rank(B_wpeer, 0));
       }
     } else {  // ---------------- MMA issuer (leader, whole warp, elect.sync issues)
-      constexpr uint32_t idesc = idesc_f16kind<__half>(2 * NRX_TILE_M, NP);
+      // pair MMA M = 256, N = 2 NP: B = [W_hi (rank 0) | W_lo (rank 1)], so every
+      // MMA writes [a W_hi | a W_lo] into a partial's two adjacent NP-column blocks
+      constexpr uint32_t idesc = idesc_f16kind<__half>(2 * NRX_TILE_M, 2 * NP);
       const uint64_t a_desc0 = smem_desc(0, (uint32_t)R * 16, 128);
-      const uint64_t b_hi0 = smem_desc(smem_u32(Ws), NPH * 16, 128);
-      const uint64_t b_lo0 = b_hi0 + (p.wbytes / 2 / 16);
+      const uint64_t b_desc0 = smem_desc(smem_u32(Ws), NP * 16, 128);
       const uint32_t a_kstep = 2 * R;
       const int ktap = p.c0 + p.c1, kch = ktap / 8;
       mbar_wait(B_wbar, 0);
@@ -309,8 +319,8 @@ __global__ void __launch_bounds__(64 + 128 * (NP / 32), 1)
       int slab, tile, st = 0, it = 0;
       bool real;
       uint32_t ph = 0;
-      const int P = KS > 0 ? KS : p.nacc;  // specialised kernels: one accumulator per tap row
-      int shifts[KS > 0 ? KS * KS : 1];      // tap row offsets (16-B units)
+      const int P = KS > 0 ? (KS > 1 ? 2 : 1) : p.nacc;  // partial accumulators (tap row % P)
+      int shifts[KS > 0 ? KS * KS : 1];                 // tap row offsets (16-B units)
       if constexpr (KS > 0) {
 #pragma unroll
         for (int tap = 0; tap < KS * KS; ++tap) shifts[tap] = (tap / KS - KS / 2) * g.Tp + (tap % KS - KS / 2);
@@ -321,12 +331,14 @@ __global__ void __launch_bounds__(64 + 128 * (NP / 32), 1)
         mbar_wait(B_tempty + 8u * acc, ((it >> 1) & 1) ^ 1);
         NRX_TADD(t_a, t0);
         tc_fence_after();
-        const uint32_t d0 = tmem_base + acc * P * NP;
+        const uint32_t d0 = tmem_base + acc * P * 2 * NP;
+        // Plane lo: D_ra = lo' [W_hi | W_lo] (scale 2^11, first MMA of each partial
+        // overwrites); plane hi: the first MMA of each partial folds (D 2^-11 +),
+        // the rest accumulate hi [W_hi | W_lo].
         if constexpr (KS > 0) {
-          // Specialised issue: planes, sources, taps and K steps unrolled, so every
-          // MMA is a straight-line predicated UTCHMMA with constant descriptor offsets.
           constexpr int KCH = 2 * (NK0 + NK1);
           constexpr int NSRC = NK1 > 0 ? 2 : 1;
+          constexpr int PK = KS > 1 ? 2 : 1;
 #pragma unroll
           for (int pl = 0; pl < 2; ++pl) {
 #pragma unroll
@@ -337,30 +349,20 @@ __global__ void __launch_bounds__(64 + 128 * (NP / 32), 1)
               tc_fence_after();
               const uint64_t a_stage = a_desc0 + (((As_s + st * p.abytes) >> 4) + p.hup);
               const int nk = src ? NK1 : NK0, kc0 = src ? 2 * NK0 : 0;
-              // pass 0: lo*Whi (plane 0) or hi*Wlo (plane 1) into accumulator 0;
-              // pass 1 (plane 1): hi*Whi into the partial accumulator of the tap row
 #pragma unroll
-              for (int pass = 0; pass < 2; ++pass) {
-                if (pass == 1 && pl == 0) break;
+              for (int tap = 0; tap < KS * KS; ++tap) {
+                const int ra = (tap / KS) % PK;
+                const bool first = src == 0 && tap == ra * KS;  // first tap of the partial (k = 0)
 #pragma unroll
-                for (int tap = 0; tap < KS * KS; ++tap) {
-#pragma unroll
-                  for (int k = 0; k < (NK0 > NK1 ? NK0 : NK1); ++k) {
-                    if (k >= nk) break;
-                    const uint64_t a = a_stage + shifts[tap] + (uint32_t)(k * a_kstep);
-                    const uint32_t boff = (uint32_t)((tap * KCH + kc0 + 2 * k) * NPH);
-                    if (pl == 0) {
-                      mma2_warp(d0, a, b_hi0 + boff, idesc, (src | tap | k) != 0);
-                    } else if (pass == 0) {
-                      if ((src | tap | k) == 0)
-                        mma2_warp_fold(d0, a, b_lo0 + boff, idesc);
-                      else
-                        mma2_warp(d0, a, b_lo0 + boff, idesc, 1);
-                    } else {
-                      const int ra = tap / KS;  // partial accumulator (tap row)
-                      mma2_warp(d0 + ra * NP, a, b_hi0 + boff, idesc, ra == 0 || (src | (tap % KS) | k) != 0);
-                    }
-                  }
+                for (int k = 0; k < (NK0 > NK1 ? NK0 : NK1); ++k) {
+                  if (k >= nk) break;
+                  const uint64_t a = a_stage + shifts[tap] + (uint32_t)(k * a_kstep);
+                  const uint64_t b = b_desc0 + (uint32_t)((tap * KCH + kc0 + 2 * k) * NP);
+                  const uint32_t d = d0 + ra * 2 * NP;
+                  if (pl == 1 && first && k == 0)
+                    mma2_warp_fold(d, a, b, idesc);
+                  else
+                    mma2_warp(d, a, b, idesc, !(pl == 0 && first && k == 0));
                 }
               }
               commit2_warp(B_empty + 8u * st);
@@ -376,27 +378,19 @@ __global__ void __launch_bounds__(64 + 128 * (NP / 32), 1)
               tc_fence_after();
               const uint64_t a_stage = a_desc0 + (((As_s + st * p.abytes) >> 4) + p.hup);
               const int nk = (src ? p.c1 : p.c0) / 16, kc0 = src ? p.c0 / 8 : 0;
-              for (int pass = 0; pass < (pl == 0 ? 1 : 2); ++pass) {
-                for (int tap = 0; tap < g.ks * g.ks; ++tap) {
-                  const int row = tap / g.ks, col = tap % g.ks;
-                  const int shift = (row - g.r) * g.Tp + (col - g.r);
-                  const int ra = row % P;
-                  for (int k = 0; k < nk; ++k) {
-                    const uint64_t a = a_stage + shift + (uint32_t)(k * a_kstep);
-                    const uint32_t boff = (uint32_t)((tap * kch + kc0 + 2 * k) * NPH);
-                    if (pl == 0) {
-                      mma2_warp(d0, a, b_hi0 + boff, idesc, (src | tap | k) != 0);
-                    } else if (pass == 0) {
-                      if ((src | tap | k) == 0)
-                        mma2_warp_fold(d0, a, b_lo0 + boff, idesc);
-                      else
-                        mma2_warp(d0, a, b_lo0 + boff, idesc, 1);
-                    } else {
-                      // first write of partial ra > 0: source 0, first tap of its first row, k = 0
-                      const bool first = ra > 0 && src == 0 && row == ra && col == 0 && k == 0;
-                      mma2_warp(d0 + ra * NP, a, b_hi0 + boff, idesc, !first);
-                    }
-                  }
+              for (int tap = 0; tap < g.ks * g.ks; ++tap) {
+                const int row = tap / g.ks, col = tap % g.ks;
+                const int shift = (row - g.r) * g.Tp + (col - g.r);
+                const int ra = row % P;
+                const bool first = src == 0 && row == ra && col == 0;
+                for (int k = 0; k < nk; ++k) {
+                  const uint64_t a = a_stage + shift + (uint32_t)(k * a_kstep);
+                  const uint64_t b = b_desc0 + (uint32_t)((tap * kch + kc0 + 2 * k) * NP);
+                  const uint32_t d = d0 + ra * 2 * NP;
+                  if (pl == 1 && first && k == 0)
+                    mma2_warp_fold(d, a, b, idesc);
+                  else
+                    mma2_warp(d, a, b, idesc, !(pl == 0 && first && k == 0));
                 }
               }
               commit2_warp(B_empty + 8u * st);
@@ -410,7 +404,6 @@ __global__ void __launch_bounds__(64 + 128 * (NP / 32), 1)
     }
   } else {  // ---------------- epilogue (both CTAs): warps 2 .. 2 + EPI_WARPS - 1
     pdl_wait();
-    constexpr int NC = 32;
     const int q = warp & 3, part = (warp - 2) >> 2;
     const int r = 32 * q + lane;
     const int cbase = part * NC;
@@ -449,20 +442,30 @@ __global__ void __launch_bounds__(64 + 128 * (NP / 32), 1)
       NRX_TADD(t_a, t0);
       tc_fence_after();
       float v[NC];
-      const int P = KS > 0 ? KS : p.nacc;
-      const uint32_t taddr = tmem_base + lane_off + acc * P * NP + cbase;
-      tmem_ld16(taddr, v);
-      tmem_ld16(taddr + 16, v + 16);
-      tmem_wait_ld();
+      const int P = KS > 0 ? (KS > 1 ? 2 : 1) : p.nacc;
+      const uint32_t taddr = tmem_base + lane_off + acc * P * 2 * NP + cbase;
+      // sum of the partials' a*W_hi and a*W_lo blocks (fp32 round-to-nearest);
+      // two blocks per TMEM round trip
 #pragma unroll
-      for (int a = 1; a < 4; ++a) {  // partial accumulators, added in fp32 round-to-nearest
-        if (a >= P) break;
+      for (int c16 = 0; c16 < NC; c16 += 16) tmem_ld16(taddr + c16, v + c16);
+      {
         float w2[NC];
-        tmem_ld16(taddr + a * NP, w2);
-        tmem_ld16(taddr + a * NP + 16, w2 + 16);
+#pragma unroll
+        for (int c16 = 0; c16 < NC; c16 += 16) tmem_ld16(taddr + NP + c16, w2 + c16);
         tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < NC; ++c) v[c] = __fadd_rn(v[c], w2[c]);
+      }
+      if (P > 1) {
+        float w3[NC], w4[NC];
+#pragma unroll
+        for (int c16 = 0; c16 < NC; c16 += 16) {
+          tmem_ld16(taddr + 2 * NP + c16, w3 + c16);
+          tmem_ld16(taddr + 3 * NP + c16, w4 + c16);
+        }
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v[c] = __fadd_rn(v[c], __fadd_rn(w3[c], w4[c]));
       }
       tc_fence_before();
       __syncwarp();
@@ -590,7 +593,7 @@ static int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* w
   p.hup = rup(g.H, 16);
   p.rbox = NRX_TILE_M + 2 * p.hup;
   const int ktap = c.c0 + c.c1;
-  p.wbytes = (uint32_t)(g.ks * g.ks * ktap * (p.np / 2) * 2 * 2);
+  p.wbytes = (uint32_t)(g.ks * g.ks * ktap * p.np * 2);  // W_hi (rank 0) or W_lo (rank 1)
   p.abytes = (uint32_t)((c.c0 > c.c1 ? c.c0 : c.c1) * p.rbox * 2);
   p.wbase = wb;
   for (int i = 0; i < p.n_io; ++i) {
@@ -599,11 +602,9 @@ static int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* w
   }
   p.mod_order = mod_order;
   p.dst = static_cast<__half*>(c.dst);
-  // partial accumulators: one per tap row, at most 4 and 256 columns per tile
-  p.nacc = g.ks < 4 ? g.ks : 4;
-  while (p.nacc > 1 && p.nacc * p.np > 256) --p.nacc;
-  if (g.ks == 3 && p.np == 64 && p.nacc != 3) return NRX_ERR_UNSUPPORTED;  // specialised kernels assume P = 3
-  const uint32_t cols = 2 * p.nacc * p.np;
+  // partial accumulators (tap row % P), each [a W_hi | a W_lo]: 2 P np columns per tile, double buffered
+  p.nacc = g.ks > 1 ? 2 : 1;
+  const uint32_t cols = 2 * 2 * p.nacc * p.np;
   p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   p.stages = 8;
   while (p.stages > 2 && conv_x3_smem(p).total > SMEM_LIMIT) --p.stages;
@@ -622,7 +623,7 @@ static int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* w
   const int pairs = (total + 1) / 2 < pairs_max ? (total + 1) / 2 : pairs_max;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs, p.n_io);
-  cfg.blockDim = dim3(64 + 128 * (p.np / 32));
+  cfg.blockDim = dim3(64 + 128 * (p.np / x3_epi_cols(c.mode)));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];

@@ -183,7 +183,7 @@ void pack_layout(const nrx_model_desc* m, int prec, PackLayout* L) {
     const int npx = rup(m->d_s, 32), np = rup(m->d_s, 16), hp = rup(m->hidden, 16);
     auto conv = [&](ConvOff& c, int ktap) {
       c.ktap = ktap;
-      c.w = take((size_t)taps * ktap * npx * 2 * 2);  // [rank][hi|lo][K/8][npx/2][8]
+      c.w = take((size_t)taps * ktap * npx * 2 * 2);  // [rank 0: W_hi | rank 1: W_lo][K/8][npx][8]
       c.b = take((size_t)(npx + 4) * 4);              // bias, then the descale 2^-E
     };
     auto mlp = [&](MlpOff& o, int k0, int n0, int n1) {
@@ -371,26 +371,24 @@ struct SplitB {
   }
 };
 
-// Convolution for the CTA pair: rank r holds output channels
-// [r npx/2, (r+1) npx/2) as its B operand rows ([hi | lo] per rank).
+// Convolution for the CTA pair: the pair MMA (N = 2 npx) reads its B operand
+// as rank 0's rows followed by rank 1's, so rank 0 holds W_hi and rank 1 W_lo,
+// each for every output channel ([taps*ktap/8][npx][8] fp16): one MMA gives
+// [a*W_hi | a*W_lo] in adjacent TMEM column blocks.
 void pack_conv_x3(const Geom& g, int k, const ConvOff& c, int cin_ref, const float* w, const float* b,
                   ChanMap map, uint8_t* base) {
-  const int npx = rup(g.d, 32), nh = npx / 2, taps = k * k, cout = g.d;
+  const int npx = rup(g.d, 32), taps = k * k, cout = g.d;
   float mx = 0.f;
   for (size_t i = 0; i < (size_t)taps * cin_ref * cout; ++i) mx = std::fmax(mx, std::fabs(w[i]));
   const int E = split_exponent(mx);
-  const size_t half = (size_t)taps * c.ktap * nh;  // elements of one hi (or lo) block
-  for (int r = 0; r < 2; ++r) {
-    SplitB B{(uint16_t*)(base + c.w) + (size_t)r * 2 * half, nh, half, std::ldexp(1.f, E)};
-    for (int tap = 0; tap < taps; ++tap)
-      for (int j = 0; j < c.ktap; ++j) {
-        const int src = map(j, g);
-        for (int n = 0; n < nh; ++n) {
-          const int o = r * nh + n;
-          B.set(n, tap * c.ktap + j, (src >= 0 && o < cout) ? w[((size_t)tap * cin_ref + src) * cout + o] : 0.f);
-        }
-      }
-  }
+  const size_t half = (size_t)taps * c.ktap * npx;  // elements of one rank's block
+  SplitB B{(uint16_t*)(base + c.w), npx, half, std::ldexp(1.f, E)};
+  for (int tap = 0; tap < taps; ++tap)
+    for (int j = 0; j < c.ktap; ++j) {
+      const int src = map(j, g);
+      for (int o = 0; o < npx; ++o)
+        B.set(o, tap * c.ktap + j, (src >= 0 && o < cout) ? w[((size_t)tap * cin_ref + src) * cout + o] : 0.f);
+    }
   float* db = (float*)(base + c.b);
   for (int o = 0; o < npx; ++o) db[o] = o < cout ? b[o] : 0.f;
   db[npx] = std::ldexp(1.f, -E);
