@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       for (int c = 0; c < NC / 8; ++c) tmem_ld8(taddr + 8 * c, v + 8 * c);
       tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(B_tempty + 8u * (acc));
+      mbar_arrive_relaxed(B_tempty + 8u * (acc));
 
       // positional channels only where a written chunk holds them
       const int clo = cbase / 8, chi = cbase / 8 + NC / 8;

@@ -63,6 +63,13 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Arrive without release semantics: the epilogue's "accumulator drained"
+// signal orders only its completed tcgen05.ld reads (tcgen05.wait::ld), not
+// its global stores; a .release.cluster arrive compiles to MEMBAR.ALL.GPU and
+// would wait for every store of the previous tile still in flight.
+__device__ __forceinline__ void arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 __device__ __forceinline__ void tmem_alloc2(uint32_t* dst, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
                : "memory");
@@ -469,7 +476,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) arrive_cluster(tempty_leader + 8u * acc);
+      if (lane == 0) arrive_cluster_relaxed(tempty_leader + 8u * acc);
       ++it;
       if (!real) continue;
 

@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW), 1)
       tmem_wait_ld();
       if (c16 + 16 >= p.op) {  // all messages are in registers: release TMEM
         tc_fence_before();
-        mbar_arrive(free_bar);
+        mbar_arrive_relaxed(free_bar);
       }
 #pragma unroll
       for (int u = 0; u < MSG_MAXU; ++u)
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
     tmem_ld16(taddr + 16, o + 16);
     tmem_wait_ld();
     tc_fence_before();
-    mbar_arrive(free_bar);
+    mbar_arrive_relaxed(free_bar);
     const int row = tile * NRX_TILE_M + r;
     const int srow = row / g.Tp, t = row - srow * g.Tp;
     if (row >= g.rows_data || t >= g.T) return;
