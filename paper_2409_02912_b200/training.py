@@ -33,6 +33,27 @@ def _torch():
     return torch
 
 
+def fp32_math():
+    """Context for the reference's fp32 arithmetic on the device: cuDNN
+    convolutions default to TF32 on tensor cores (torch.backends.cudnn.
+    allow_tf32), which would silently change the training graph's numerics;
+    this turns TF32 off for convolutions and matmuls (forward and backward
+    run inside it in train_step)."""
+    import contextlib
+    torch = _torch()
+
+    @contextlib.contextmanager
+    def ctx():
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
+        try:
+            with torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
+                yield
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
+    return ctx()
+
+
 class TorchNrxGraph:
     """The NRX graph on torch tensors.  ``params`` maps the reference's weight
     names to leaf tensors (float32, requires_grad)."""
@@ -207,10 +228,11 @@ def train_step(graph: TorchNrxGraph, adam: Adam, feats, labels, label_mask, ches
     torch = _torch()
     for p in graph.params.values():
         p.grad = None
-    total, bce, mse = training_loss(graph, feats, labels, label_mask, chest_target, active, mods, gamma)
-    if not torch.isfinite(total):
-        raise RuntimeError(f"non-finite training loss {float(total)}")
-    total.backward()
+    with fp32_math():
+        total, bce, mse = training_loss(graph, feats, labels, label_mask, chest_target, active, mods, gamma)
+        if not torch.isfinite(total):
+            raise RuntimeError(f"non-finite training loss {float(total)}")
+        total.backward()
     touched = [k for k, p in graph.params.items() if p.grad is not None]
     adam.step(graph.params, touched)
     for p in graph.params.values():
@@ -218,7 +240,7 @@ def train_step(graph: TorchNrxGraph, adam: Adam, feats, labels, label_mask, ches
     return {"total": float(total.detach()), "bce": float(bce.detach()), "mse": float(mse.detach())}
 
 
-__all__ = ["TorchNrxGraph", "training_loss", "train_step", "Adam"]
+__all__ = ["TorchNrxGraph", "training_loss", "train_step", "Adam", "fp32_math"]
 
 
 # ---------------------------------------------------------------------------
