@@ -62,3 +62,28 @@ def load_case(name: str) -> GoldenCase:
     bits = [z[f"bits{u}"] for u in range(cfg.num_ues)]
     return GoldenCase(name, cfg, config, mcs, z["y"], books, n0, n0_arg, meta["squeeze"],
                       weights, z["features"], llrs, z["chest"], bits)
+
+
+C2_REF273_SEED = 2409
+
+
+def c2_ref273_case():
+    """The full-size C2 case of tests/golden/c2_ref273.npz (regenerable without
+    the reference): (cfg, config, weights, mcs, y (1,S,T,B), books)."""
+    from oracle.nrx_oracle import perturb_biases
+    from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights
+    from paper_2409_02912_b200.synth import synth_slots
+    table = default_mcs_table()
+    cfg = SlotConfig(num_subcarriers=3276, num_ues=2, comb_size=2)
+    config = NrxConfig.from_table(table, (14,), d_s=56, num_iterations=2)
+    w = perturb_biases(init_weights(config, seed=0))
+    y, books, _ = synth_slots(cfg, [4, 4], 1, 0.1, seed=C2_REF273_SEED)
+    y = y.astype(np.complex64).astype(np.complex128)
+    return cfg, config, w, (table[14], table[14]), y, books
+
+
+def load_c2_ref273():
+    """c2_ref273_case() + the reference's outputs on it (every 8th subcarrier)."""
+    with np.load(os.path.join(GOLDEN, "c2_ref273.npz")) as z:
+        gold = {k: z[k] for k in z.files}
+    return c2_ref273_case() + (gold,)

@@ -98,3 +98,17 @@ def test_positional_encoding_hand_value():
     for s in cfg.comb_subcarriers(0):
         for t in cfg.pilot_symbols:
             assert pe[s, t, 0] == 0 and pe[s, t, 1] == 0
+
+
+def test_oracle_matches_reference_at_273prb():
+    """The oracle against the reference's own C2 outputs (273 PRB, RT model):
+    every 8th subcarrier of the LLR / chest grids, fp32 rounding level."""
+    from golden_cases import load_c2_ref273
+    cfg, config, w, mcs, y, books, gold = load_c2_ref273()
+    llrs, chest = orc.nrx_forward(y[0], books[0], cfg, mcs, w, config, 0.1)
+    st = int(gold["stride"])
+    got = np.stack(llrs)[:, ::st]
+    scale = float(gold["llr_absmax"])
+    assert got.shape == gold["llr"].shape
+    assert np.abs(got - gold["llr"]).max() <= 2e-6 * scale
+    assert np.abs(chest[:, ::st] - gold["chest"]).max() <= 2e-6 * float(gold["chest_absmax"])
