@@ -424,25 +424,43 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
     PairIter w(g, g.NU, g.tiles, p.n_io, p.mod_order, (int)rank);
     int slab, tile, it = 0;
     bool real;
-    while (w.next(slab, tile, real)) {
+    // residual update: the previous state of the NEXT tile is loaded while this
+    // tile is processed (latency-bound loads: one tile in flight ahead)
+    uint4 rhi[NC / 8], rlo[NC / 8];
+    auto load_residual = [&](int sl, int tl, bool re) {
+      const int rw = tl * NRX_TILE_M + r;
+      int s2, t2;
+      row_to_st(rw, g, s2, t2);
+      const bool ok = re && rw < g.rows_data && t2 < g.T;
+      const __half* src = chunk_ptr(p.dst, sl, 2 * nd, 0, rw, g);
+#pragma unroll
+      for (int c8 = 0; c8 < NC / 8; ++c8) {
+        const int cc = cbase / 8 + c8;
+        rhi[c8] = rlo[c8] = make_uint4(0u, 0u, 0u, 0u);
+        if (ok && cc < dch) {
+          rhi[c8] = *reinterpret_cast<const uint4*>(src + cc * dcs);
+          rlo[c8] = *reinterpret_cast<const uint4*>(src + (nd + cc) * dcs);
+        }
+      }
+    };
+    bool have = w.next(slab, tile, real);
+    if (MODE == EPI_RESIDUAL && have) load_residual(slab, tile, real);
+    while (have) {
       const int acc = it & 1;
       const int row = tile * NRX_TILE_M + r;
       int s, t;
       row_to_st(row, g, s, t);
       const bool valid = real && row < g.rows_data && t < g.T;
       __half* const drow = chunk_ptr(p.dst, slab, 2 * nd, 0, row, g);
+      const int cslab = slab;
       float old[NC];
-      if (MODE == EPI_RESIDUAL) {  // previous state (hi + lo), loads issued before the accumulator wait
+      int nslab = 0, ntile = 0;
+      bool nreal = false;
+      const bool nhave = w.next(nslab, ntile, nreal);
+      if (MODE == EPI_RESIDUAL) {
 #pragma unroll
-        for (int c8 = 0; c8 < NC / 8; ++c8) {
-          const int cc = cbase / 8 + c8;
-          uint4 hi = make_uint4(0u, 0u, 0u, 0u), lo = hi;
-          if (valid && cc < dch) {
-            hi = *reinterpret_cast<const uint4*>(drow + cc * dcs);
-            lo = *reinterpret_cast<const uint4*>(drow + (nd + cc) * dcs);
-          }
-          unsplit_chunk(hi, lo, old + 8 * c8);
-        }
+        for (int c8 = 0; c8 < NC / 8; ++c8) unsplit_chunk(rhi[c8], rlo[c8], old + 8 * c8);
+        if (nhave) load_residual(nslab, ntile, nreal);
       }
       NRX_T(t0);
       mbar_wait_backoff(B_tfull + 8u * acc, (it >> 1) & 1, 128);
@@ -478,10 +496,15 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
       __syncwarp();
       if (lane == 0) arrive_cluster_relaxed(tempty_leader + 8u * acc);
       ++it;
-      if (!real) continue;
+      const bool cur_real = real;
+      have = nhave;
+      slab = nslab;
+      tile = ntile;
+      real = nreal;
+      if (!cur_real) continue;
 
       const float pdt = (MODE != EPI_RELU && valid) ? sdt[t] : 0.f;
-      const float pdf = (MODE != EPI_RELU && valid) ? pos_df(s, slab % g.U, g) : 0.f;
+      const float pdf = (MODE != EPI_RELU && valid) ? pos_df(s, cslab % g.U, g) : 0.f;
 #pragma unroll
       for (int c8 = 0; c8 < NC / 8; ++c8) {
         const int cc = cbase / 8 + c8;
@@ -516,7 +539,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
           float o[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            o[e] = (valid && MODE != EPI_RELU) ? state_extra(8 * cc + e, s, t, slab % g.U, g) : 0.f;
+            o[e] = (valid && MODE != EPI_RELU) ? state_extra(8 * cc + e, s, t, cslab % g.U, g) : 0.f;
           uint4 hi, lo;
           split_chunk(o, hi, lo);
           *reinterpret_cast<uint4*>(drow + cc * dcs) = hi;
