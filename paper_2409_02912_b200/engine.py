@@ -26,11 +26,17 @@ from . import _lib
 from .config import weight_array
 
 
+_TORCH = None
+
+
 def _require_cuda():
-    import torch
-    if not torch.cuda.is_available():
-        raise _lib.NrxLibraryError("no CUDA device: the NRX B200 path has no CPU fallback")
-    return torch
+    global _TORCH
+    if _TORCH is None:
+        import torch
+        if not torch.cuda.is_available():
+            raise _lib.NrxLibraryError("no CUDA device: the NRX B200 path has no CPU fallback")
+        _TORCH = torch
+    return _TORCH
 
 
 def pack_weights(config, weights, precision: str = "fp32") -> np.ndarray:
@@ -66,10 +72,18 @@ def pilot_comb_values(book_values: np.ndarray, cfg) -> np.ndarray:
     valid RE and are ignored by the kernel."""
     S, comb, U = cfg.num_subcarriers, cfg.comb_size, cfg.num_ues
     F = -(-S // comb)
-    ps = np.asarray(cfg.pilot_symbols)
-    u_idx = np.arange(U)[:, None]
-    s_idx = np.minimum(u_idx % comb + np.arange(F)[None, :] * comb, S - 1)       # (U, F)
-    return np.ascontiguousarray(book_values[..., u_idx[:, :, None], s_idx[:, :, None], ps[None, None, :]])
+    ps = list(cfg.pilot_symbols)
+    book_values = np.asarray(book_values)
+    out = np.empty(book_values.shape[:-3] + (U, F, len(ps)), dtype=book_values.dtype)
+    for u in range(U):  # strided slices: no fancy-index gather over the grid
+        o = u % comb
+        sub = book_values[..., u, o::comb, :]            # (..., n_u, T)
+        n_u = sub.shape[-2]
+        for k, t in enumerate(ps):
+            out[..., u, :n_u, k] = sub[..., t]
+        if n_u < F:
+            out[..., u, n_u:, :] = out[..., u, n_u - 1:n_u, :]
+    return out
 
 
 class NrxEngine:
@@ -270,6 +284,13 @@ class NrxEngine:
         inputs as the reference).  Inputs are converted while being written
         into pinned staging (one pass); the results are pinned-memory arrays
         (see _pinned_outputs)."""
+        return self.finish(self.enqueue_arrays(cfg, y, pilot_vals, noise_feat, mod_order, num_iterations,
+                                               llr_width, exact_inputs))
+
+    def enqueue_arrays(self, cfg, y, pilot_vals, noise_feat, mod_order, num_iterations, llr_width,
+                       exact_inputs=False):
+        """First half of run_arrays: stage the inputs, enqueue H2D, the forward
+        and the D2H on this thread's stream; returns a handle for finish()."""
         torch = _require_cuda()
         cdt = torch.complex128 if exact_inputs else torch.complex64
         n = y.shape[0]
@@ -296,5 +317,10 @@ class NrxEngine:
             h_llr, h_chest, llr_np, chest_np = self._pinned_outputs(d_llr.shape, d_chest.shape)
             h_llr.copy_(d_llr, non_blocking=True)
             h_chest.copy_(d_chest, non_blocking=True)
-        tls.stream.synchronize()
+        return tls.stream, llr_np, chest_np
+
+    @staticmethod
+    def finish(handle):
+        stream, llr_np, chest_np = handle
+        stream.synchronize()
         return llr_np, chest_np
