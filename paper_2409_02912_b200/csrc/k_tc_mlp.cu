@@ -24,9 +24,11 @@
 namespace nrx {
 namespace tc {
 
-// warps: 0 producer, 1 MMA, HW hidden-epilogue warps, 4 output-epilogue warps
-constexpr int mlp_threads(int hw) { return 64 + 32 * hw + 128; }
+// warps: 0 producer, 1 MMA, HW hidden-epilogue warps, OW output-epilogue warps
+// (OW / 4 groups per TMEM lane quarter, each draining a share of the columns)
+constexpr int mlp_threads(int hw, int ow = 4) { return 64 + 32 * hw + 32 * ow; }
 constexpr int MSG_HW = 4, READOUT_HW = 8;
+constexpr int MSG_OW = 8;  // the message epilogue (2 UEs x 64 columns, split planes) is the long pole
 constexpr int MSG_MAXU = 4;  // UEs per slot on the tensor-core path
 constexpr int A_STAGES = 4;  // maximum; fp32x3 uses fewer (p.astages)
 
@@ -73,7 +75,8 @@ struct MlpSmem {
   }
 };
 
-__device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int io, int hidden_threads) {
+__device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int io, int hidden_threads,
+                                          int output_threads = 128) {
   const int warp = threadIdx.x >> 5;
   if (warp == 0) tmem_alloc(s.tmem_ptr, p.tmem_cols);
   if (threadIdx.x == 32) {
@@ -86,7 +89,7 @@ __device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int 
       mbar_init(&s.h_ready[i], hidden_threads);
       mbar_init(&s.hs_free[i], 1);
       mbar_init(&s.out_full[i], 1);
-      mbar_init(&s.out_free[i], 128);
+      mbar_init(&s.out_free[i], output_threads);
     }
     mbar_init(s.wbar, 1);
     fence_barrier_init();
@@ -104,7 +107,7 @@ __device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int 
 
 // Producer / MMA / hidden-epilogue roles are identical for both MLPs; the
 // output epilogue is passed in as a functor.
-template <typename ET, int HW, bool X3, typename OutEpilogue>
+template <typename ET, int HW, bool X3, int OW = 4, typename OutEpilogue>
 __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int io, const CUtensorMap* amap,
                                          OutEpilogue&& out_epi) {
   const Geom& g = p.g;
@@ -277,7 +280,7 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
       tc_fence_after();
       const uint32_t taddr = tmem_base + lane_off + p.col_o + (item & 1) * (U * p.op);
       NRX_T(t1);
-      out_epi(unit, tile, r, taddr, &s.out_free[item & 1]);
+      out_epi(unit, tile, r, taddr, &s.out_free[item & 1], (warp - 2 - HW) >> 2, OW / 4);
       NRX_TADD(t_b, t1);
       ++item;
     }
@@ -295,17 +298,18 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
 }
 
 template <typename ET, bool X3>
-__global__ void __launch_bounds__(mlp_threads(MSG_HW), 1)
+__global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
     k_msg_tc(const __grid_constant__ MlpTcParams p, const __grid_constant__ CUtensorMap smap) {
   extern __shared__ __align__(1024) uint8_t smem[];
   MlpSmem s(smem, p);
-  mlp_setup(p, s, 0, 32 * MSG_HW);
+  mlp_setup(p, s, 0, 32 * MSG_HW, 32 * MSG_OW);
   const Geom& g = p.g;
   const int U = p.uses_per_item;
   const int nca = g.Ca / 8;
   ET* const agg = static_cast<ET*>(p.agg);
   const float dsc = X3 ? s.sb1[p.op] : 1.f;
-  mlp_body<ET, MSG_HW, X3>(p, s, 0, &smap, [&](int n, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
+  mlp_body<ET, MSG_HW, X3, MSG_OW>(p, s, 0, &smap, [&](int n, int tile, int r, uint32_t taddr, uint64_t* free_bar,
+                                                       int grp, int ngrp) {
     const int row = tile * NRX_TILE_M + r;
     const int srow = row / g.Tp, t = row - srow * g.Tp;
     const bool valid = row < g.rows_data && t < g.T;
@@ -314,13 +318,21 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW), 1)
     // f32(f64 total - f64 own) whenever that float64 sum is exact (message
     // exponents within 29 bits); the bf16 rounding of the stored aggregate
     // dominates any difference for U>2.  The fp32 parity path keeps fp64.
-    for (int c16 = 0; c16 < p.op; c16 += 16) {
+    // this warp group's share of the output columns (16-column blocks); when
+    // the width does not split evenly the first group drains everything
+    const int ng = p.op % (16 * ngrp) == 0 ? ngrp : 1;
+    if (grp >= ng) {
+      mbar_arrive_relaxed(free_bar);
+      return;
+    }
+    const int cspan = p.op / ng;
+    for (int c16 = grp * cspan; c16 < (grp + 1) * cspan; c16 += 16) {
       float m[MSG_MAXU][16];
 #pragma unroll
       for (int u = 0; u < MSG_MAXU; ++u)
         if (u < U) tmem_ld16(taddr + u * p.op + c16, m[u]);
       tmem_wait_ld();
-      if (c16 + 16 >= p.op) {  // all messages are in registers: release TMEM
+      if (c16 + 16 >= (grp + 1) * cspan) {  // this group's messages are in registers: release TMEM
         tc_fence_before();
         mbar_arrive_relaxed(free_bar);
       }
@@ -369,7 +381,8 @@ __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
   mlp_setup(p, s, io, 32 * READOUT_HW);
   const Geom& g = p.g;
   const float dsc = X3 ? s.sb1[p.op] : 1.f;
-  mlp_body<ET, READOUT_HW, X3>(p, s, io, &smap, [&](int slab, int tile, int r, uint32_t taddr, uint64_t* free_bar) {
+  mlp_body<ET, READOUT_HW, X3>(p, s, io, &smap, [&](int slab, int tile, int r, uint32_t taddr, uint64_t* free_bar,
+                                                    int, int) {
     float o[32];
     tmem_ld16(taddr, o);
     tmem_ld16(taddr + 16, o + 16);
@@ -470,7 +483,7 @@ int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const void
   const int total = g.N * g.tiles;
   const int per_sm = (512 / p.tmem_cols) < 2 || 2 * smem > SMEM_LIMIT ? 1 : 2;
   const int cap = num_sms() * per_sm;
-  fn<<<total < cap ? total : cap, mlp_threads(MSG_HW), smem, st>>>(p, m);
+  fn<<<total < cap ? total : cap, mlp_threads(MSG_HW, MSG_OW), smem, st>>>(p, m);
   return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
 }
 

@@ -177,8 +177,28 @@ __device__ __forceinline__ void mma_fold_warp(uint32_t d_tmem, uint64_t adesc, u
 // MMAs run at the full magnitude of D.  A: [2 planes][K/8 chunks][rows][8]
 // (hi plane first, a_lo = plane distance in 16-B units), B: [hi | lo][K/8][N][8]
 // (b_lo likewise).
+template <int NK>
+__device__ __forceinline__ void mma_x3_gemm_t(uint32_t d, uint64_t a_hi, uint32_t a_lo, uint32_t a_k, uint64_t b_hi,
+                                              uint32_t b_lo, uint32_t b_k, uint32_t idesc) {
+#pragma unroll
+  for (int k = 0; k < NK; ++k) mma_bf16_warp(d, a_hi + a_lo + k * a_k, b_hi + k * b_k, idesc, k != 0);
+  mma_fold_warp(d, a_hi, b_hi + b_lo, idesc);
+#pragma unroll
+  for (int k = 1; k < NK; ++k) mma_bf16_warp(d, a_hi + k * a_k, b_hi + b_lo + k * b_k, idesc, 1);
+#pragma unroll
+  for (int k = 0; k < NK; ++k) mma_bf16_warp(d, a_hi + k * a_k, b_hi + k * b_k, idesc, 1);
+}
+// Unrolled issue for the K sizes of the per-RE MLPs (a runtime loop of
+// elect-per-MMA issues costs ~3x per MMA); other sizes fall back to the loop.
 __device__ __forceinline__ void mma_x3_gemm(uint32_t d, uint64_t a_hi, uint32_t a_lo, uint32_t a_k, uint64_t b_hi,
                                             uint32_t b_lo, uint32_t b_k, int nk, uint32_t idesc) {
+  switch (nk) {
+    case 1: mma_x3_gemm_t<1>(d, a_hi, a_lo, a_k, b_hi, b_lo, b_k, idesc); return;
+    case 2: mma_x3_gemm_t<2>(d, a_hi, a_lo, a_k, b_hi, b_lo, b_k, idesc); return;
+    case 4: mma_x3_gemm_t<4>(d, a_hi, a_lo, a_k, b_hi, b_lo, b_k, idesc); return;
+    case 8: mma_x3_gemm_t<8>(d, a_hi, a_lo, a_k, b_hi, b_lo, b_k, idesc); return;
+    default: break;
+  }
   for (int k = 0; k < nk; ++k) mma_bf16_warp(d, a_hi + a_lo + k * a_k, b_hi + k * b_k, idesc, k != 0);
   mma_fold_warp(d, a_hi, b_hi + b_lo, idesc);
   for (int k = 1; k < nk; ++k) mma_bf16_warp(d, a_hi + k * a_k, b_hi + b_lo + k * b_k, idesc, 1);
