@@ -36,7 +36,7 @@ def main():
     ap.add_argument("--traffic", default=os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                                        "profiles", "traffic.json"))
     args = ap.parse_args()
-    raw = subprocess.run(["ncu", "-i", args.report, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+    raw = subprocess.run(["ncu", "-i", args.report, "--page", "raw", "--csv"],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     head, units = rows[0], rows[1]
@@ -46,8 +46,9 @@ def main():
         u = dict(zip(head, units))
         k = {"Kernel Name": d["Kernel Name"]}
         for m in METRICS:
-            if m in d:
-                k[m] = f"{d[m]} {u.get(m, '')}".strip()
+            col = m if m in d else next((h for h in head if h.endswith("." + m)), None)  # section-prefixed names
+            if col is not None:
+                k[m] = f"{d[col]} {u.get(col, '')}".strip()
         kernels.append(k)
     with open(args.out, "w") as fh:
         json.dump({"command": args.command, "slots_per_launch": args.slots, "precision": args.precision,
