@@ -154,6 +154,18 @@ def conv_update0_flops_per_slab_re(d=D_S, k=3):
     return 2 * k * k * (2 * d + 2) * d
 
 
+def executed_flops(precision, B, S=S_C2, U=U_C2, T=14, d=D_S):
+    """Tensor-core FLOPs update.conv0 actually issues per launch (padded
+    shapes: 128-row tiles over S*(T+1) rows, K = 128 per tap, N = rup(d, 16);
+    fp32x3: two N = 2 rup(d, 32) MMAs per tap and K step, fp32_simt: none)."""
+    if precision == "fp32_simt":
+        return 0
+    rows = -(-S * (T + 1) // 128) * 128
+    if precision == "fp32":
+        return 2 * rows * U * B * 9 * 128 * 2 * (2 * (-(-d // 32) * 32))
+    return 2 * rows * U * B * 9 * 128 * (-(-d // 16) * 16)
+
+
 def algorithmic_flops_per_slab_re(d=D_S, h=D_S, n_it=N_IT, m=4, B=4, cin=19, k=3):
     """MAC = 9 Cin d + 9 d^2 + N_it (2 d h + 9 (2d+2) d + 9 d^2) + (d h + h m) + (d h + h 2B)."""
     kk = k * k
@@ -365,10 +377,13 @@ def run_ours(args):
         peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
         peak_note = f"bf16 dense, sustained ({peak_src}); fp16 runs at the same tensor rate"
     elif args.precision == "fp32":
-        # fp32x3: every fp32 MAC is three fp16 tensor-core MACs (lo*Whi, hi*Whi, hi*Wlo)
+        # fp32x3: a two-piece fp16 split needs at least three fp16 MACs per fp32 MAC (hi*Whi, hi*Wlo,
+        # lo*Whi); the kernel issues four (two N = 2 np MMAs on [W_hi | W_lo]), i.e. runs at most at
+        # bf16 / 4 -- the conservative / 3 ceiling is the one reported as `peak`
         peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / 3.0
-        peak_note = (f"fp32-equivalent tensor-core ceiling = bf16 dense sustained ({peak_src}) / 3: the "
-                     "fp16 hi/lo split issues three kind::f16 MMAs per fp32 MAC")
+        peak_note = (f"fp32-equivalent tensor-core ceiling = bf16 dense sustained ({peak_src}) / 3 (the minimum "
+                     "of three fp16 MACs per fp32 MAC for a two-piece split); the kernel issues four "
+                     "(scheme ceiling = / 4, see frac_of_scheme_ceiling)")
     else:
         sm_mhz = peaks.get("sm_max_mhz", 1965.0)
         peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
@@ -449,6 +464,10 @@ def run_ours(args):
                      "traffic": traffic, "peak_source": peak_note,
                      "algorithmic_flops_per_launch": flops_launch,
                      "avg_launch_ms": round(kavg * 1e3, 4), "launches_timed": len(kernel_ms),
+                     "frac_of_scheme_ceiling": round(achieved / (peak * 3.0 / 4.0), 4) if args.precision == "fp32"
+                     else None,
+                     "executed_tensor_tflops": round(executed_flops(args.precision, B) / kavg / 1e12, 1)
+                     if kernel_ms else None,
                      "share_of_step": round(kavg * 1e3 * N_IT / ms_per_step, 4) if kernel_ms else None},
         "whole_path": {"algorithmic_tflops": round(algorithmic_flops_per_slab_re() * U * S * T * value / world / 1e12, 2),
                        "flop_per_slot": algorithmic_flops_per_slab_re() * U * S * T},
