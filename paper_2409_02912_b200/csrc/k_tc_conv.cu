@@ -138,7 +138,8 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   float* stb1 = reinterpret_cast<float*>(smem + L.tb1);
   float* sdt = reinterpret_cast<float*>(smem + L.dt);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // lane-0 shuffles: provably warp-uniform values keep the MMA issue on the uniform datapath
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
   pdl_launch_dependents();  // the next layer's prologue may run on SMs this grid frees
   if (warp == 0) tmem_alloc(tmem_ptr, p.tmem_cols);
   if (threadIdx.x == 32) {
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_ptr;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_ptr, 0);
   // tail TMEM regions (double buffered): hidden at col_h + b*thp, outputs at col_o + b*top
   const uint32_t col_h = 2 * NP, col_o = 2 * NP + 2 * p.thp;
   const uint32_t ta_bytes = (uint32_t)g.Cs * NRX_TILE_M * 2, th_bytes = (uint32_t)p.thp * NRX_TILE_M * 2;
@@ -744,6 +745,14 @@ int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const 
 // update conv's second source; any U: readout fused into the last conv1.
 bool tc_fused_messages(const Geom& g) { return g.U == 2; }
 
+static bool pair16_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("NRX_PAIR16");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 int launch_forward_tc(const Geom& g, const PackLayout& L, const WsLayout& W, int n_it, const uint8_t* wb,
                       const int32_t* mod_order, uint8_t* ws, float* llr, float2* chest, cudaStream_t st) {
   using namespace tc;
@@ -756,6 +765,26 @@ int launch_forward_tc(const Geom& g, const PackLayout& L, const WsLayout& W, int
   float* state32 = g.prec == NRX_BF16 ? reinterpret_cast<float*>(ws + W.state32) : nullptr;
   const bool fused = tc_fused_messages(g);
 
+  // update.conv0 (tail-less ReLU) on CTA pairs when the blob carries the pair
+  // copies (np 32 / 64); NRX_PAIR16=0 keeps it single-CTA
+  const bool pair = L.upd0p.w != 0 && pair16_enabled();
+  auto relu_layer = [&](const ConvLaunch& c1, const ConvOff* pair_offs) -> int {
+    if (!pair) return launch_conv(g, c1, wb, mod_order, st);
+    ConvX3Launch x{};
+    x.offs = pair_offs;
+    x.n_off = c1.n_off;
+    x.src0 = c1.src0;
+    x.c0 = c1.c0;
+    x.src1 = c1.src1;
+    x.c1 = c1.c1;
+    x.src1_xor = c1.src1_xor;
+    x.dst = c1.dst;
+    x.cdst = c1.cdst;
+    x.mode = EPI_RELU;
+    x.prec = g.prec;
+    const int rc = launch_conv_x3(g, x, wb, mod_order, st);
+    return rc == NRX_ERR_UNSUPPORTED ? launch_conv(g, c1, wb, mod_order, st) : rc;
+  };
   ConvLaunch c{};
   c.offs = L.init0;
   c.n_off = g.n_io;
@@ -765,6 +794,7 @@ int launch_forward_tc(const Geom& g, const PackLayout& L, const WsLayout& W, int
   c.cdst = g.Ch;
   c.mode = EPI_RELU;
   {
+    // state_init.conv0 (K = 32) stays single-CTA: its pair version is slower (0.160 vs 0.138 ms / 32 slots)
     ProfScope ps(KID_INIT0, st);
     NRX_TRY_TC(launch_conv(g, c, wb, mod_order, st));
   }
@@ -805,7 +835,7 @@ int launch_forward_tc(const Geom& g, const PackLayout& L, const WsLayout& W, int
     c.mode = EPI_RELU;
     {
       ProfScope ps(KID_UPD0, st);
-      NRX_TRY_TC(launch_conv(g, c, wb, mod_order, st));
+      NRX_TRY_TC(relu_layer(c, &L.upd0p));
     }
     const bool last = it + 1 == n_it;
     c = ConvLaunch{};

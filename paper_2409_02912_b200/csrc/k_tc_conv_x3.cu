@@ -215,10 +215,22 @@ __host__ __device__ inline ConvX3Smem conv_x3_smem(const ConvX3Params& p) {
 // the bottleneck of that layer, runs twice the warps (16 columns each).
 __host__ __device__ constexpr int x3_epi_cols(int mode) { return mode == EPI_RESIDUAL ? 16 : 32; }
 
-template <int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0>
+// PREC = NRX_FP32X3: the split-operand kernel described above.  PREC =
+// NRX_FP16 / NRX_BF16: the same CTA-pair pipeline for one half-precision plane
+// (the bf16 / fp16 modes' ReLU convolutions without a tail: state_init.conv0
+// and iteration.update.conv0): each CTA holds the weights of np/2 output
+// channels, an N = np pair MMA reads 4 KB of A and 1 KB of B per SM (5 KB
+// instead of 6 KB single-CTA: 40 instead of 48 cycles per K=16 step).
+template <int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0, int PREC = NRX_FP32X3>
 __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
     k_conv_x3(const __grid_constant__ ConvX3Params p, const __grid_constant__ CUtensorMap map0,
               const __grid_constant__ CUtensorMap map1) {
+  constexpr bool SPLIT = PREC == NRX_FP32X3;
+  using ET = typename std::conditional<PREC == NRX_BF16, __nv_bfloat16, __half>::type;
+  constexpr int NPL = SPLIT ? 2 : 1;         // activation planes
+  constexpr int NB = SPLIT ? 2 * NP : NP;     // pair MMA N (accumulator block)
+  constexpr int BROWS = SPLIT ? NP : NP / 2;  // B rows held by each CTA
+  static_assert(SPLIT || MODE == EPI_RELU, "half-precision pair kernels: ReLU layers only");
   // 32 accumulator columns per epilogue thread: 2 + 4 * NP/32 warps (10 for
   // NP = 64) leave each SM sub-partition <= 3 warps, i.e. up to 168 registers
   // for the fully unrolled MMA issue (18 warps would cap it at 96 and spill)
@@ -245,7 +257,9 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
   const uint32_t B_full = smem_u32(full), B_empty = smem_u32(empty), B_tfull = smem_u32(tfull),
                  B_tempty = smem_u32(tempty), B_wbar = smem_u32(wbar), B_wpeer = smem_u32(wpeer);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index and TMEM base through a lane-0 shuffle: provably warp-uniform, so the
+  // MMA issue keeps its descriptors on the uniform datapath (no R2UR per MMA)
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
   pdl_launch_dependents();
   if (warp == 0) tmem_alloc2(tmem_ptr, p.tmem_cols);
   if (threadIdx.x == 32) {
@@ -268,7 +282,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
   __syncthreads();
   cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / TMA
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_ptr;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_ptr, 0);
   const int R = p.rbox;
 #ifdef NRX_TIMING
   long long t_a = 0, t_b = 0, t_c = 0, t_all = clock64();
@@ -291,7 +305,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
       uint32_t ph = 0;
       while (w.next(slab, tile, real)) {
         const int grp0 = (tile * NRX_TILE_M - p.hup) / 16;
-        for (int pl = 0; pl < 2; ++pl) {  // lo planes first (their MMAs run first), then hi
+        for (int pl = 0; pl < NPL; ++pl) {  // lo planes first (their MMAs run first), then hi
           for (int src = 0; src < nsrc; ++src) {
             const int cs = src ? p.c1 : p.c0;
             NRX_T(t0);
@@ -299,7 +313,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
             NRX_TADD(t_a, t0);
             if (rank == 0) mbar_expect_tx(B_full + 8u * st, 2u * (uint32_t)cs * R * 2);
             tma_load_4d_pair(As_s + st * p.abytes, src ? &map1 : &map0, full_leader + 8u * st, 0, grp0,
-                             pl == 0 ? cs / 8 : 0, src ? (slab ^ p.src1_xor) : slab);
+                             SPLIT && pl == 0 ? cs / 8 : 0, src ? (slab ^ p.src1_xor) : slab);
             if (++st == p.stages) { st = 0; ph ^= 1; }
           }
         }
@@ -314,9 +328,9 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
     } else {  // ---------------- MMA issuer (leader, whole warp, elect.sync issues)
       // pair MMA M = 256, N = 2 NP: B = [W_hi (rank 0) | W_lo (rank 1)], so every
       // MMA writes [a W_hi | a W_lo] into a partial's two adjacent NP-column blocks
-      constexpr uint32_t idesc = idesc_f16kind<__half>(2 * NRX_TILE_M, 2 * NP);
+      constexpr uint32_t idesc = idesc_f16kind<ET>(2 * NRX_TILE_M, NB);
       const uint64_t a_desc0 = smem_desc(0, (uint32_t)R * 16, 128);
-      const uint64_t b_desc0 = smem_desc(smem_u32(Ws), NP * 16, 128);
+      const uint64_t b_desc0 = smem_desc(smem_u32(Ws), BROWS * 16, 128);
       const uint32_t a_kstep = 2 * R;
       const int ktap = p.c0 + p.c1, kch = ktap / 8;
       mbar_wait(B_wbar, 0);
@@ -326,8 +340,8 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
       int slab, tile, st = 0, it = 0;
       bool real;
       uint32_t ph = 0;
-      const int P = KS > 0 ? (KS > 1 ? 2 : 1) : p.nacc;  // partial accumulators (tap row % P)
-      int shifts[KS > 0 ? KS * KS : 1];                 // tap row offsets (16-B units)
+      const int P = !SPLIT ? 1 : KS > 0 ? (KS > 1 ? 2 : 1) : p.nacc;  // partial accumulators (tap row % P)
+      int shifts[KS > 0 ? KS * KS : 1];                               // tap row offsets (16-B units)
       if constexpr (KS > 0) {
 #pragma unroll
         for (int tap = 0; tap < KS * KS; ++tap) shifts[tap] = (tap / KS - KS / 2) * g.Tp + (tap % KS - KS / 2);
@@ -338,16 +352,16 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
         mbar_wait(B_tempty + 8u * acc, ((it >> 1) & 1) ^ 1);
         NRX_TADD(t_a, t0);
         tc_fence_after();
-        const uint32_t d0 = tmem_base + acc * P * 2 * NP;
+        const uint32_t d0 = tmem_base + acc * P * NB;
         // Plane lo: D_ra = lo' [W_hi | W_lo] (scale 2^11, first MMA of each partial
         // overwrites); plane hi: the first MMA of each partial folds (D 2^-11 +),
         // the rest accumulate hi [W_hi | W_lo].
         if constexpr (KS > 0) {
           constexpr int KCH = 2 * (NK0 + NK1);
           constexpr int NSRC = NK1 > 0 ? 2 : 1;
-          constexpr int PK = KS > 1 ? 2 : 1;
+          constexpr int PK = SPLIT && KS > 1 ? 2 : 1;
 #pragma unroll
-          for (int pl = 0; pl < 2; ++pl) {
+          for (int pl = 0; pl < NPL; ++pl) {
 #pragma unroll
             for (int src = 0; src < NSRC; ++src) {
               NRX_T(t1);
@@ -364,9 +378,9 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
                 for (int k = 0; k < (NK0 > NK1 ? NK0 : NK1); ++k) {
                   if (k >= nk) break;
                   const uint64_t a = a_stage + shifts[tap] + (uint32_t)(k * a_kstep);
-                  const uint64_t b = b_desc0 + (uint32_t)((tap * KCH + kc0 + 2 * k) * NP);
-                  const uint32_t d = d0 + ra * 2 * NP;
-                  if (pl == 1 && first && k == 0)
+                  const uint64_t b = b_desc0 + (uint32_t)((tap * KCH + kc0 + 2 * k) * BROWS);
+                  const uint32_t d = d0 + ra * NB;
+                  if (SPLIT && pl == 1 && first && k == 0)
                     mma2_warp_fold(d, a, b, idesc);
                   else
                     mma2_warp(d, a, b, idesc, !(pl == 0 && first && k == 0));
@@ -377,7 +391,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
             }
           }
         } else {
-          for (int pl = 0; pl < 2; ++pl) {
+          for (int pl = 0; pl < NPL; ++pl) {
             for (int src = 0; src < nsrc; ++src) {
               NRX_T(t1);
               mbar_wait(B_full + 8u * st, ph);
@@ -392,9 +406,9 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
                 const bool first = src == 0 && row == ra && col == 0;
                 for (int k = 0; k < nk; ++k) {
                   const uint64_t a = a_stage + shift + (uint32_t)(k * a_kstep);
-                  const uint64_t b = b_desc0 + (uint32_t)((tap * kch + kc0 + 2 * k) * NP);
-                  const uint32_t d = d0 + ra * 2 * NP;
-                  if (pl == 1 && first && k == 0)
+                  const uint64_t b = b_desc0 + (uint32_t)((tap * kch + kc0 + 2 * k) * BROWS);
+                  const uint32_t d = d0 + ra * NB;
+                  if (SPLIT && pl == 1 && first && k == 0)
                     mma2_warp_fold(d, a, b, idesc);
                   else
                     mma2_warp(d, a, b, idesc, !(pl == 0 && first && k == 0));
@@ -419,7 +433,8 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
     const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
     const uint32_t tempty_leader = map_rank(B_tempty, 0);
     const uint32_t sbias_s = smem_u32(sbias);
-    const float descale = sbias[NP];
+    const float descale = SPLIT ? sbias[NP] : 1.f;
+    const int ndb = SPLIT ? 2 * nd : nd;  // chunks of the output buffer (both planes)
     const size_t dcs = (size_t)g.rows_slab * 8;  // chunk stride
     PairIter w(g, g.NU, g.tiles, p.n_io, p.mod_order, (int)rank);
     int slab, tile, it = 0;
@@ -432,7 +447,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
       int s2, t2;
       row_to_st(rw, g, s2, t2);
       const bool ok = re && rw < g.rows_data && t2 < g.T;
-      const __half* src = chunk_ptr(p.dst, sl, 2 * nd, 0, rw, g);
+      const __half* src = chunk_ptr(p.dst, sl, ndb, 0, rw, g);
 #pragma unroll
       for (int c8 = 0; c8 < NC / 8; ++c8) {
         const int cc = cbase / 8 + c8;
@@ -451,7 +466,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
       int s, t;
       row_to_st(row, g, s, t);
       const bool valid = real && row < g.rows_data && t < g.T;
-      __half* const drow = chunk_ptr(p.dst, slab, 2 * nd, 0, row, g);
+      __half* const drow = chunk_ptr(p.dst, slab, ndb, 0, row, g);
       const int cslab = slab;
       float old[NC];
       int nslab = 0, ntile = 0;
@@ -467,13 +482,14 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
       NRX_TADD(t_a, t0);
       tc_fence_after();
       float v[NC];
-      const int P = KS > 0 ? (KS > 1 ? 2 : 1) : p.nacc;
-      const uint32_t taddr = tmem_base + lane_off + acc * P * 2 * NP + cbase;
+      const int P = !SPLIT ? 1 : KS > 0 ? (KS > 1 ? 2 : 1) : p.nacc;
+      const uint32_t taddr = tmem_base + lane_off + acc * P * NB + cbase;
       // sum of the partials' a*W_hi and a*W_lo blocks (fp32 round-to-nearest);
       // two blocks per TMEM round trip
 #pragma unroll
       for (int c16 = 0; c16 < NC; c16 += 16) tmem_ld16(taddr + c16, v + c16);
-      {
+      if (!SPLIT) tmem_wait_ld();
+      if (SPLIT) {
         float w2[NC];
 #pragma unroll
         for (int c16 = 0; c16 < NC; c16 += 16) tmem_ld16(taddr + NP + c16, w2 + c16);
@@ -481,7 +497,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
 #pragma unroll
         for (int c = 0; c < NC; ++c) v[c] = __fadd_rn(v[c], w2[c]);
       }
-      if (P > 1) {
+      if (SPLIT && P > 1) {
         float w3[NC], w4[NC];
 #pragma unroll
         for (int c16 = 0; c16 < NC; c16 += 16) {
@@ -528,10 +544,14 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
             if (valid && c == g.d + 1) x[e] = pdf;
           }
         }
-        uint4 hi, lo;
-        split_chunk(x, hi, lo);
-        *reinterpret_cast<uint4*>(drow + cc * dcs) = hi;
-        *reinterpret_cast<uint4*>(drow + (nd + cc) * dcs) = lo;
+        if constexpr (SPLIT) {
+          uint4 hi, lo;
+          split_chunk(x, hi, lo);
+          *reinterpret_cast<uint4*>(drow + cc * dcs) = hi;
+          *reinterpret_cast<uint4*>(drow + (nd + cc) * dcs) = lo;
+        } else {
+          *reinterpret_cast<uint4*>(drow + cc * dcs) = pack_chunk(x, static_cast<const ET*>(nullptr));
+        }
       }
       if (part == PARTS - 1) {  // buffer channels beyond the accumulator: positional / zero only
         for (int cc = NP / 8; cc < nd; ++cc) {
@@ -540,10 +560,14 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e)
             o[e] = (valid && MODE != EPI_RELU) ? state_extra(8 * cc + e, s, t, cslab % g.U, g) : 0.f;
-          uint4 hi, lo;
-          split_chunk(o, hi, lo);
-          *reinterpret_cast<uint4*>(drow + cc * dcs) = hi;
-          *reinterpret_cast<uint4*>(drow + (nd + cc) * dcs) = lo;
+          if constexpr (SPLIT) {
+            uint4 hi, lo;
+            split_chunk(o, hi, lo);
+            *reinterpret_cast<uint4*>(drow + cc * dcs) = hi;
+            *reinterpret_cast<uint4*>(drow + (nd + cc) * dcs) = lo;
+          } else {
+            *reinterpret_cast<uint4*>(drow + cc * dcs) = pack_chunk(o, static_cast<const ET*>(nullptr));
+          }
         }
       }
     }
@@ -565,7 +589,16 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
 using X3Fn = void (*)(const ConvX3Params, const CUtensorMap, const CUtensorMap);
 
 template <int NP>
-static X3Fn select_conv_x3(const Geom& g, int mode, int c0, int c1) {
+static X3Fn select_conv_x3(const Geom& g, int mode, int c0, int c1, int prec) {
+  if (prec != NRX_FP32X3) {  // half-precision pair kernels: ReLU layers only
+    const bool f16 = prec == NRX_FP16;
+    if (mode != EPI_RELU) return nullptr;
+    if (NP == 64 && g.ks == 3 && c0 == 32 && c1 == 0)
+      return f16 ? k_conv_x3<64, EPI_RELU, 3, 2, 0, NRX_FP16> : k_conv_x3<64, EPI_RELU, 3, 2, 0, NRX_BF16>;
+    if (NP == 64 && g.ks == 3 && c0 == 64 && c1 == 64)
+      return f16 ? k_conv_x3<64, EPI_RELU, 3, 4, 4, NRX_FP16> : k_conv_x3<64, EPI_RELU, 3, 4, 4, NRX_BF16>;
+    return f16 ? k_conv_x3<NP, EPI_RELU, 0, 0, 0, NRX_FP16> : k_conv_x3<NP, EPI_RELU, 0, 0, 0, NRX_BF16>;
+  }
   static const X3Fn generic[3] = {k_conv_x3<NP, 0>, k_conv_x3<NP, 1>, k_conv_x3<NP, 2>};
   X3Fn fn = generic[mode];
   if (NP == 64 && g.ks == 3) {  // fully unrolled issue for the RT / large models' 3x3 layers
@@ -596,34 +629,24 @@ static int make_map_plane(CUtensorMap* m, const void* base, const Geom& g, int C
 
 }  // namespace tc
 
-struct ConvX3Launch {
-  const ConvOff* offs;
-  int n_off;
-  const void* src0;
-  int c0;
-  const void* src1;
-  int c1;
-  int src1_xor;
-  void* dst;
-  int cdst;
-  int mode;
-};
-
-static int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, const int32_t* mod_order,
-                          cudaStream_t st) {
+int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, const int32_t* mod_order,
+                   cudaStream_t st) {
   using namespace tc;
+  const bool split = c.prec == NRX_FP32X3;
   ConvX3Params p{};
   p.g = g;
   p.c0 = c.c0;
   p.c1 = c.c1;
   p.src1_xor = c.src1_xor;
-  p.np = rup(g.d, 32);
+  p.np = split ? rup(g.d, 32) : rup(g.d, 16);
+  if (!split && p.np != 32 && p.np != 64) return NRX_ERR_UNSUPPORTED;
   p.cdst = c.cdst;
   p.n_io = c.n_off;
   p.hup = rup(g.H, 16);
   p.rbox = NRX_TILE_M + 2 * p.hup;
   const int ktap = c.c0 + c.c1;
-  p.wbytes = (uint32_t)(g.ks * g.ks * ktap * p.np * 2);  // W_hi (rank 0) or W_lo (rank 1)
+  // split: W_hi (rank 0) or W_lo (rank 1) for every output channel; else np/2 output channels
+  p.wbytes = (uint32_t)(g.ks * g.ks * ktap * (split ? p.np : p.np / 2) * 2);
   p.abytes = (uint32_t)((c.c0 > c.c1 ? c.c0 : c.c1) * p.rbox * 2);
   p.wbase = wb;
   for (int i = 0; i < p.n_io; ++i) {
@@ -633,8 +656,8 @@ static int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* w
   p.mod_order = mod_order;
   p.dst = static_cast<__half*>(c.dst);
   // partial accumulators (tap row % P), each [a W_hi | a W_lo]: 2 P np columns per tile, double buffered
-  p.nacc = g.ks > 1 ? 2 : 1;
-  const uint32_t cols = 2 * 2 * p.nacc * p.np;
+  p.nacc = split && g.ks > 1 ? 2 : 1;
+  const uint32_t cols = split ? 2 * 2 * p.nacc * p.np : 2 * p.np;
   p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   p.stages = 8;
   while (p.stages > 2 && conv_x3_smem(p).total > SMEM_LIMIT) --p.stages;
@@ -642,11 +665,15 @@ static int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* w
     return NRX_ERR_UNSUPPORTED;
   const size_t smem = conv_x3_smem(p).total;
   CUtensorMap m0, m1;
-  int rc = make_map_plane(&m0, c.src0, g, c.c0, p.rbox);
+  int rc = split ? make_map_plane(&m0, c.src0, g, c.c0, p.rbox) : make_map(&m0, c.src0, g, c.c0, p.rbox);
   if (rc) return rc;
-  rc = make_map_plane(&m1, c.src1 ? c.src1 : c.src0, g, c.c1 ? c.c1 : c.c0, p.rbox);
+  const void* s1 = c.src1 ? c.src1 : c.src0;
+  const int cc1 = c.c1 ? c.c1 : c.c0;
+  rc = split ? make_map_plane(&m1, s1, g, cc1, p.rbox) : make_map(&m1, s1, g, cc1, p.rbox);
   if (rc) return rc;
-  const X3Fn fn = p.np == 64 ? select_conv_x3<64>(g, c.mode, c.c0, c.c1) : select_conv_x3<32>(g, c.mode, c.c0, c.c1);
+  const X3Fn fn = p.np == 64 ? select_conv_x3<64>(g, c.mode, c.c0, c.c1, c.prec)
+                             : select_conv_x3<32>(g, c.mode, c.c0, c.c1, c.prec);
+  if (!fn) return NRX_ERR_UNSUPPORTED;
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.NU * g.tiles;
   const int pairs_max = num_sms() / 2;

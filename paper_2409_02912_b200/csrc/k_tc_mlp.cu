@@ -111,8 +111,9 @@ template <typename ET, int HW, bool X3, int OW = 4, typename OutEpilogue>
 __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int io, const CUtensorMap* amap,
                                          OutEpilogue&& out_epi) {
   const Geom& g = p.g;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t tmem_base = *s.tmem_ptr;
+  // lane-0 shuffles: provably warp-uniform values keep the MMA issue on the uniform datapath
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *s.tmem_ptr, 0);
   const int U = p.uses_per_item;
 #ifdef NRX_TIMING
   long long t_a = 0, t_b = 0, t_c = 0, t_d = 0, t_all = clock64();

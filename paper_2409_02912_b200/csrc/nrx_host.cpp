@@ -226,6 +226,10 @@ void pack_layout(const nrx_model_desc* m, int prec, PackLayout* L) {
     mlp(L->msg, g.Cs, hp, np);
     conv(L->upd0, g.Cs + g.Ca);
     conv(L->upd1, g.Ch);
+    if (np >= 32) {  // pair copies (same byte size: two ranks of np/2 columns)
+      for (int i = 0; i < m->n_io; ++i) conv(L->init0p[i], g.Cf);
+      conv(L->upd0p, g.Cs + g.Ca);
+    }
     L->total = off;
     return;
   }
@@ -394,6 +398,28 @@ void pack_conv_x3(const Geom& g, int k, const ConvOff& c, int cin_ref, const flo
   db[npx] = std::ldexp(1.f, -E);
 }
 
+// Half-precision convolution for the CTA pair: rank r holds output channels
+// [r np/2, (r+1) np/2) as [K/8][np/2][8] (the pair MMA reads B as rank 0's
+// rows followed by rank 1's).
+void pack_conv_pair16(const Geom& g, int k, const ConvOff& c, int cin_ref, const float* w, const float* b,
+                      ChanMap map, uint8_t* base) {
+  const int np = rup(g.d, 16), nh = np / 2, taps = k * k, cout = g.d;
+  const size_t block = (size_t)taps * c.ktap * nh;
+  for (int r = 0; r < 2; ++r) {
+    BOperand B{(uint16_t*)(base + c.w) + (size_t)r * block, nh, g.prec == NRX_FP16};
+    for (int tap = 0; tap < taps; ++tap)
+      for (int j = 0; j < c.ktap; ++j) {
+        const int src = map(j, g);
+        for (int n = 0; n < nh; ++n) {
+          const int o = r * nh + n;
+          B.set(n, tap * c.ktap + j, (src >= 0 && o < cout) ? w[((size_t)tap * cin_ref + src) * cout + o] : 0.f);
+        }
+      }
+  }
+  float* db = (float*)(base + c.b);
+  for (int o = 0; o < np; ++o) db[o] = o < cout ? b[o] : 0.f;
+}
+
 }  // namespace
 
 // fp32-grade tensor-core packing (NRX_FP32X3): same GEMM shapes as
@@ -533,6 +559,11 @@ int pack_weights_tc(const nrx_model_desc* m, int prec, const float* const* t, ui
   }
   pack_conv_bf16(g, k, L.upd0, 2 * d + 2, t[i_upd], t[i_upd + 1], map_update, base);
   pack_conv_bf16(g, k, L.upd1, d, t[i_upd + 2], t[i_upd + 3], map_identity_hidden, base);
+  if (L.upd0p.w) {
+    for (int io = 0; io < m->n_io; ++io)
+      pack_conv_pair16(g, k, L.init0p[io], g.Cin, t[8 * io], t[8 * io + 1], map_identity_feats, base);
+    pack_conv_pair16(g, k, L.upd0p, 2 * d + 2, t[i_upd], t[i_upd + 1], map_update, base);
+  }
   return NRX_OK;
 }
 

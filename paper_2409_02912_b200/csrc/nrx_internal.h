@@ -61,6 +61,9 @@ struct PackLayout {
   MlpOff llr[NRX_MAX_IO];
   MlpOff msg;
   ConvOff upd0, upd1;
+  // bf16 / fp16: CTA-pair copies of the tail-less ReLU convolutions (rank r's
+  // block holds output channels [r np/2, (r+1) np/2)); w == 0 when absent
+  ConvOff init0p[NRX_MAX_IO], upd0p;
   MlpOff chest;
   size_t total;
   int dmax;                   // padded state depth for the SIMT MLP kernels

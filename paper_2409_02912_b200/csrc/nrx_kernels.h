@@ -21,6 +21,24 @@ struct ConvArgs {
   int mode;                          // ConvEpilogue
 };
 
+// One CTA-pair convolution (k_tc_conv_x3.cu): the fp32x3 layers, or a
+// bf16 / fp16 ReLU layer without a tail (prec = NRX_FP16 / NRX_BF16).
+struct ConvX3Launch {
+  const ConvOff* offs;
+  int n_off;
+  const void* src0;
+  int c0;
+  const void* src1;
+  int c1;
+  int src1_xor;
+  void* dst;
+  int cdst;
+  int mode;
+  int prec = NRX_FP32X3;
+};
+int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, const int32_t* mod_order,
+                   cudaStream_t st);
+
 int launch_ls_feat(const Geom& g, const void* y, int y_c128, const void* pil, int pil_c128, int n_sets,
                    const float* noise, void* feats, cudaStream_t st);
 
