@@ -446,11 +446,16 @@ static int mlp_common(MlpTcParams& p, const Geom& g, int hp, int op, int uses, i
   p.w1bytes = planes * (uint32_t)(hp * op * 2);
   p.abytes = planes * (uint32_t)(p.cs * NRX_TILE_M * 2);
   p.hbytes = planes * (uint32_t)(hp * NRX_TILE_M * 2);
+  // double-buffered hidden tiles before A stages: a single hidden tile
+  // serialises the hidden epilogue with fc1 of the previous use
   p.astages = A_STAGES;
   p.nhb = 2;
-  while (mlp_smem_bytes(p) > SMEM_LIMIT && p.astages > 2) --p.astages;
-  if (mlp_smem_bytes(p) > SMEM_LIMIT) p.nhb = 1;
   while (mlp_smem_bytes(p) > SMEM_LIMIT && p.astages > 1) --p.astages;
+  if (mlp_smem_bytes(p) > SMEM_LIMIT) {
+    p.nhb = 1;
+    p.astages = A_STAGES;
+    while (mlp_smem_bytes(p) > SMEM_LIMIT && p.astages > 1) --p.astages;
+  }
   p.col_h = 0;
   p.col_o = 2 * hp;
   const uint32_t cols = 2 * hp + 2 * uses * op;
