@@ -222,7 +222,7 @@ __host__ __device__ constexpr int x3_epi_cols(int mode) { return mode == EPI_RES
 // channels, an N = np pair MMA reads 4 KB of A and 1 KB of B per SM (5 KB
 // instead of 6 KB single-CTA: 40 instead of 48 cycles per K=16 step).
 template <int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0, int PREC = NRX_FP32X3>
-__global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
+__global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_epi_cols(MODE)), 1)
     k_conv_x3(const __grid_constant__ ConvX3Params p, const __grid_constant__ CUtensorMap map0,
               const __grid_constant__ CUtensorMap map1) {
   constexpr bool SPLIT = PREC == NRX_FP32X3;
@@ -230,12 +230,13 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
   constexpr int NPL = SPLIT ? 2 : 1;         // activation planes
   constexpr int NB = SPLIT ? 2 * NP : NP;     // pair MMA N (accumulator block)
   constexpr int BROWS = SPLIT ? NP : NP / 2;  // B rows held by each CTA
+  constexpr int DST = SPLIT ? (NB + 31) / 32 * 32 : NB;  // TMEM columns per partial accumulator
   static_assert(SPLIT || MODE == EPI_RELU, "half-precision pair kernels: ReLU layers only");
   // 32 accumulator columns per epilogue thread: 2 + 4 * NP/32 warps (10 for
   // NP = 64) leave each SM sub-partition <= 3 warps, i.e. up to 168 registers
   // for the fully unrolled MMA issue (18 warps would cap it at 96 and spill)
   constexpr int NC = x3_epi_cols(MODE);  // accumulator columns per epilogue thread
-  constexpr int PARTS = NP / NC;
+  constexpr int PARTS = (NP + NC - 1) / NC;  // NP = 56: the last part's columns past NP are ignored
   constexpr int EPI_WARPS = 4 * PARTS;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Geom& g = p.g;
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
         mbar_wait(B_tempty + 8u * acc, ((it >> 1) & 1) ^ 1);
         NRX_TADD(t_a, t0);
         tc_fence_after();
-        const uint32_t d0 = tmem_base + acc * P * NB;
+        const uint32_t d0 = tmem_base + acc * P * DST;
         // Plane lo: D_ra = lo' [W_hi | W_lo] (scale 2^11, first MMA of each partial
         // overwrites); plane hi: the first MMA of each partial folds (D 2^-11 +),
         // the rest accumulate hi [W_hi | W_lo].
@@ -379,7 +380,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
                   if (k >= nk) break;
                   const uint64_t a = a_stage + shifts[tap] + (uint32_t)(k * a_kstep);
                   const uint64_t b = b_desc0 + (uint32_t)((tap * KCH + kc0 + 2 * k) * BROWS);
-                  const uint32_t d = d0 + ra * NB;
+                  const uint32_t d = d0 + ra * DST;
                   if (SPLIT && pl == 1 && first && k == 0)
                     mma2_warp_fold(d, a, b, idesc);
                   else
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
                 for (int k = 0; k < nk; ++k) {
                   const uint64_t a = a_stage + shift + (uint32_t)(k * a_kstep);
                   const uint64_t b = b_desc0 + (uint32_t)((tap * kch + kc0 + 2 * k) * BROWS);
-                  const uint32_t d = d0 + ra * NB;
+                  const uint32_t d = d0 + ra * DST;
                   if (SPLIT && pl == 1 && first && k == 0)
                     mma2_warp_fold(d, a, b, idesc);
                   else
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
       tc_fence_after();
       float v[NC];
       const int P = !SPLIT ? 1 : KS > 0 ? (KS > 1 ? 2 : 1) : p.nacc;
-      const uint32_t taddr = tmem_base + lane_off + acc * P * NB + cbase;
+      const uint32_t taddr = tmem_base + lane_off + acc * P * DST + cbase;
       // sum of the partials' a*W_hi and a*W_lo blocks (fp32 round-to-nearest);
       // two blocks per TMEM round trip
 #pragma unroll
@@ -501,8 +502,8 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
         float w3[NC], w4[NC];
 #pragma unroll
         for (int c16 = 0; c16 < NC; c16 += 16) {
-          tmem_ld16(taddr + 2 * NP + c16, w3 + c16);
-          tmem_ld16(taddr + 3 * NP + c16, w4 + c16);
+          tmem_ld16(taddr + DST + c16, w3 + c16);
+          tmem_ld16(taddr + DST + NP + c16, w4 + c16);
         }
         tmem_wait_ld();
 #pragma unroll
@@ -525,7 +526,7 @@ __global__ void __launch_bounds__(64 + 128 * (NP / x3_epi_cols(MODE)), 1)
       for (int c8 = 0; c8 < NC / 8; ++c8) {
         const int cc = cbase / 8 + c8;
         if (MODE == EPI_RESIDUAL && cc >= dch) continue;  // constant positional / zero chunk
-        if (cc >= nd) continue;
+        if (cc >= nd || 8 * cc >= NP) continue;         // past the buffer / the accumulator
         float bb[8], x[8];
         ld_shared_f8(sbias_s + 32u * cc, bb);
         const bool full = 8 * cc + 8 <= g.d;
@@ -590,23 +591,26 @@ using X3Fn = void (*)(const ConvX3Params, const CUtensorMap, const CUtensorMap);
 
 template <int NP>
 static X3Fn select_conv_x3(const Geom& g, int mode, int c0, int c1, int prec) {
-  if (prec != NRX_FP32X3) {  // half-precision pair kernels: ReLU layers only
-    const bool f16 = prec == NRX_FP16;
-    if (mode != EPI_RELU) return nullptr;
-    if (NP == 64 && g.ks == 3 && c0 == 32 && c1 == 0)
-      return f16 ? k_conv_x3<64, EPI_RELU, 3, 2, 0, NRX_FP16> : k_conv_x3<64, EPI_RELU, 3, 2, 0, NRX_BF16>;
-    if (NP == 64 && g.ks == 3 && c0 == 64 && c1 == 64)
-      return f16 ? k_conv_x3<64, EPI_RELU, 3, 4, 4, NRX_FP16> : k_conv_x3<64, EPI_RELU, 3, 4, 4, NRX_BF16>;
-    return f16 ? k_conv_x3<NP, EPI_RELU, 0, 0, 0, NRX_FP16> : k_conv_x3<NP, EPI_RELU, 0, 0, 0, NRX_BF16>;
+  if (prec != NRX_FP32X3) {  // half-precision pair kernels: ReLU layers only, np 32 / 64
+    if constexpr (NP == 32 || NP == 64) {
+      const bool f16 = prec == NRX_FP16;
+      if (mode != EPI_RELU) return nullptr;
+      if (NP == 64 && g.ks == 3 && c0 == 32 && c1 == 0)
+        return f16 ? k_conv_x3<64, EPI_RELU, 3, 2, 0, NRX_FP16> : k_conv_x3<64, EPI_RELU, 3, 2, 0, NRX_BF16>;
+      if (NP == 64 && g.ks == 3 && c0 == 64 && c1 == 64)
+        return f16 ? k_conv_x3<64, EPI_RELU, 3, 4, 4, NRX_FP16> : k_conv_x3<64, EPI_RELU, 3, 4, 4, NRX_BF16>;
+      return f16 ? k_conv_x3<NP, EPI_RELU, 0, 0, 0, NRX_FP16> : k_conv_x3<NP, EPI_RELU, 0, 0, 0, NRX_BF16>;
+    }
+    return nullptr;
   }
   static const X3Fn generic[3] = {k_conv_x3<NP, 0>, k_conv_x3<NP, 1>, k_conv_x3<NP, 2>};
   X3Fn fn = generic[mode];
-  if (NP == 64 && g.ks == 3) {  // fully unrolled issue for the RT / large models' 3x3 layers
+  if (NP == 56 && g.ks == 3) {  // fully unrolled issue for the RT / large models' 3x3 layers
     const int nk0 = c0 / 16, nk1 = c1 / 16;
-    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_x3<64, EPI_RELU, 3, 2, 0>;
-    if (mode == EPI_RELU && nk0 == 4 && nk1 == 4) fn = k_conv_x3<64, EPI_RELU, 3, 4, 4>;
-    if (mode == EPI_STATE_INIT && nk0 == 4 && nk1 == 0) fn = k_conv_x3<64, EPI_STATE_INIT, 3, 4, 0>;
-    if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0) fn = k_conv_x3<64, EPI_RESIDUAL, 3, 4, 0>;
+    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_x3<56, EPI_RELU, 3, 2, 0>;
+    if (mode == EPI_RELU && nk0 == 4 && nk1 == 4) fn = k_conv_x3<56, EPI_RELU, 3, 4, 4>;
+    if (mode == EPI_STATE_INIT && nk0 == 4 && nk1 == 0) fn = k_conv_x3<56, EPI_STATE_INIT, 3, 4, 0>;
+    if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0) fn = k_conv_x3<56, EPI_RESIDUAL, 3, 4, 0>;
   }
   return fn;
 }
@@ -638,7 +642,7 @@ int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, cons
   p.c0 = c.c0;
   p.c1 = c.c1;
   p.src1_xor = c.src1_xor;
-  p.np = split ? rup(g.d, 32) : rup(g.d, 16);
+  p.np = split ? x3_np(g.d) : rup(g.d, 16);
   if (!split && p.np != 32 && p.np != 64) return NRX_ERR_UNSUPPORTED;
   p.cdst = c.cdst;
   p.n_io = c.n_off;
@@ -657,7 +661,7 @@ int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, cons
   p.dst = static_cast<__half*>(c.dst);
   // partial accumulators (tap row % P), each [a W_hi | a W_lo]: 2 P np columns per tile, double buffered
   p.nacc = split && g.ks > 1 ? 2 : 1;
-  const uint32_t cols = split ? 2 * 2 * p.nacc * p.np : 2 * p.np;
+  const uint32_t cols = split ? 2 * p.nacc * ((2 * p.np + 31) / 32 * 32) : 2 * p.np;
   p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   p.stages = 8;
   while (p.stages > 2 && conv_x3_smem(p).total > SMEM_LIMIT) --p.stages;
@@ -671,8 +675,15 @@ int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, cons
   const int cc1 = c.c1 ? c.c1 : c.c0;
   rc = split ? make_map_plane(&m1, s1, g, cc1, p.rbox) : make_map(&m1, s1, g, cc1, p.rbox);
   if (rc) return rc;
-  const X3Fn fn = p.np == 64 ? select_conv_x3<64>(g, c.mode, c.c0, c.c1, c.prec)
-                             : select_conv_x3<32>(g, c.mode, c.c0, c.c1, c.prec);
+  X3Fn fn = nullptr;
+  switch (p.np) {
+    case 16: fn = select_conv_x3<16>(g, c.mode, c.c0, c.c1, c.prec); break;
+    case 32: fn = select_conv_x3<32>(g, c.mode, c.c0, c.c1, c.prec); break;
+    case 48: fn = select_conv_x3<48>(g, c.mode, c.c0, c.c1, c.prec); break;
+    case 56: fn = select_conv_x3<56>(g, c.mode, c.c0, c.c1, c.prec); break;
+    case 64: fn = select_conv_x3<64>(g, c.mode, c.c0, c.c1, c.prec); break;
+    default: return NRX_ERR_UNSUPPORTED;
+  }
   if (!fn) return NRX_ERR_UNSUPPORTED;
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.NU * g.tiles;
@@ -680,7 +691,7 @@ int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, cons
   const int pairs = (total + 1) / 2 < pairs_max ? (total + 1) / 2 : pairs_max;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs, p.n_io);
-  cfg.blockDim = dim3(64 + 128 * (p.np / x3_epi_cols(c.mode)));
+  cfg.blockDim = dim3(64 + 128 * ((p.np + x3_epi_cols(c.mode) - 1) / x3_epi_cols(c.mode)));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];

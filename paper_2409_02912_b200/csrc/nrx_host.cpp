@@ -180,7 +180,7 @@ void pack_layout(const nrx_model_desc* m, int prec, PackLayout* L) {
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
   if (prec == NRX_FP32X3) {  // fp16 hi/lo operand pairs, CTA-pair convolutions
-    const int npx = rup(m->d_s, 32), np = rup(m->d_s, 16), hp = rup(m->hidden, 16);
+    const int npx = x3_np(m->d_s), np = rup(m->d_s, 16), hp = rup(m->hidden, 16);
     auto conv = [&](ConvOff& c, int ktap) {
       c.ktap = ktap;
       c.w = take((size_t)taps * ktap * npx * 2 * 2);  // [rank 0: W_hi | rank 1: W_lo][K/8][npx][8]
@@ -381,7 +381,7 @@ struct SplitB {
 // [a*W_hi | a*W_lo] in adjacent TMEM column blocks.
 void pack_conv_x3(const Geom& g, int k, const ConvOff& c, int cin_ref, const float* w, const float* b,
                   ChanMap map, uint8_t* base) {
-  const int npx = rup(g.d, 32), taps = k * k, cout = g.d;
+  const int npx = x3_np(g.d), taps = k * k, cout = g.d;
   float mx = 0.f;
   for (size_t i = 0; i < (size_t)taps * cin_ref * cout; ++i) mx = std::fmax(mx, std::fabs(w[i]));
   const int E = split_exponent(mx);

@@ -29,6 +29,11 @@ namespace nrx {
 inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 inline int rup(int a, int b) { return cdiv(a, b) * b; }
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+// fp32x3 pair-convolution width: output channels of one [W_hi | W_lo] half
+// (the pair MMA's N is twice it, a multiple of 16): d rounded up to 16, but
+// 56 for d in (48, 56] (the RT model: N = 112 instead of 128 skips 12.5 % of
+// the tensor work).
+inline int x3_np(int d) { return (d + 7) / 8 * 8 == 56 ? 56 : rup(d, 16); }
 
 // Geometry + channel bookkeeping, passed by value to kernels.
 struct Geom {
