@@ -35,7 +35,9 @@ EXPORTED = ("nrx_abi_version", "nrx_status_string", "nrx_validate", "nrx_weight_
             "nrx_ldpc_decode", "nrx_ldpc_encode", "nrx_random_bits", "nrx_bits_to_labels",
             "nrx_extract_llrs", "nrx_count_mismatches",
             # include/nrx_classical.h
-            "nrx_ls_lmmse", "nrx_kbest")
+            "nrx_ls_lmmse", "nrx_kbest",
+            # include/nrx_train.h
+            "nrx_train_conv_fwd", "nrx_train_conv_dgrad", "nrx_train_conv_wgrad", "nrx_train_adam")
 KERNEL_IDS = {"ls_feat": 0, "conv_state_init0": 1, "conv_state_init1": 2, "msg_agg": 3,
               "conv_update0": 4, "conv_update1": 5, "readout": 6}
 
@@ -146,6 +148,11 @@ def load() -> ctypes.CDLL:
     lib.nrx_count_mismatches.argtypes = [I, I, V, V, V, V]
     lib.nrx_ls_lmmse.argtypes = [P(SlotDesc), I, I, V, I, V, I, I, V, V, V, ctypes.c_float, V, I, V]
     lib.nrx_kbest.argtypes = [P(SlotDesc), I, I, V, I, V, I, V, V, V, I, I, ctypes.c_float, V, I, V]
+    F32 = ctypes.c_float
+    lib.nrx_train_conv_fwd.argtypes = [I, I, I, I, I, I, V, V, V, V, V]
+    lib.nrx_train_conv_dgrad.argtypes = [I, I, I, I, I, I, V, V, V, V]
+    lib.nrx_train_conv_wgrad.argtypes = [I, I, I, I, I, I, V, V, V, V, V]
+    lib.nrx_train_adam.argtypes = [I, V, V, V, V, F32, F32, F32, F32, I, V]
     if lib.nrx_abi_version() != 1:
         raise NrxLibraryError("libnrx_b200.so ABI version mismatch")
     _LIB = lib

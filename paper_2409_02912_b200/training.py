@@ -54,14 +54,86 @@ def fp32_math():
     return ctx()
 
 
+def _nrx_lib():
+    from . import _lib
+    return _lib.load()
+
+
+_CONV_FN = None
+
+
+def _nrx_conv_fn():
+    """torch.autograd.Function over the hand-written fp32 kernels of
+    csrc/k_train.cu (include/nrx_train.h): 'same' convolution / dense layer
+    forward, input gradient and kernel gradient (autodiff.py:302-350 and the
+    matmul VJPs)."""
+    global _CONV_FN
+    if _CONV_FN is not None:
+        return _CONV_FN
+    torch = _torch()
+
+    def _stream(t):
+        return torch.cuda.current_stream(t.device).cuda_stream
+
+    class NrxConv(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, x, w):
+            # x (n, S, T, cin) NHWC, w (k, k, cin, cout)
+            x = x.contiguous()
+            w = w.contiguous()
+            n, S, T, cin = x.shape
+            k, cout = w.shape[0], w.shape[3]
+            y = torch.empty((n, S, T, cout), dtype=torch.float32, device=x.device)
+            code = _nrx_lib().nrx_train_conv_fwd(n, S, T, cin, cout, k, x.data_ptr(), w.data_ptr(), None,
+                                                 y.data_ptr(), _stream(x))
+            if code:
+                raise RuntimeError(f"nrx_train_conv_fwd failed ({code})")
+            ctx.save_for_backward(x, w)
+            return y
+
+        @staticmethod
+        def backward(ctx, dy):
+            x, w = ctx.saved_tensors
+            dy = dy.contiguous()
+            n, S, T, cin = x.shape
+            k, cout = w.shape[0], w.shape[3]
+            lib = _nrx_lib()
+            dx = dw = None
+            if ctx.needs_input_grad[0]:
+                dx = torch.empty_like(x)
+                code = lib.nrx_train_conv_dgrad(n, S, T, cin, cout, k, dy.data_ptr(), w.data_ptr(), dx.data_ptr(),
+                                                _stream(dy))
+                if code:
+                    raise RuntimeError(f"nrx_train_conv_dgrad failed ({code})")
+            if ctx.needs_input_grad[1]:
+                dw = torch.empty_like(w)
+                code = lib.nrx_train_conv_wgrad(n, S, T, cin, cout, k, x.data_ptr(), dy.data_ptr(), dw.data_ptr(),
+                                                None, _stream(dy))
+                if code:
+                    raise RuntimeError(f"nrx_train_conv_wgrad failed ({code})")
+            return dx, dw
+
+    _CONV_FN = NrxConv
+    return NrxConv
+
+
 class TorchNrxGraph:
     """The NRX graph on torch tensors.  ``params`` maps the reference's weight
-    names to leaf tensors (float32, requires_grad)."""
+    names to leaf tensors (float32, requires_grad).
 
-    def __init__(self, config, weights: dict, device="cpu"):
+    kernels="nrx" (default on CUDA devices) runs every convolution and dense
+    layer, forward and backward, on the hand-written fp32 kernels of
+    csrc/k_train.cu; torch autograd only sequences them and does the
+    elementwise glue (bias, ReLU, residual, concat, sum of others, losses).
+    kernels="torch" uses cuDNN / cuBLAS (with TF32 off, see fp32_math)."""
+
+    def __init__(self, config, weights: dict, device="cpu", kernels=None):
         torch = _torch()
         self.config = config
         self.device = torch.device(device)
+        self.kernels = kernels or ("nrx" if self.device.type == "cuda" else "torch")
+        if self.kernels == "nrx" and self.device.type != "cuda":
+            raise ValueError("kernels='nrx' needs a CUDA device")
         self.params = {k: torch.tensor(np.asarray(getattr(v, "data", v), dtype=np.float32), device=self.device,
                                        requires_grad=True) for k, v in weights.items()}
 
@@ -72,11 +144,23 @@ class TorchNrxGraph:
     def _conv(self, x, name):
         """'same' k x k convolution of NHWC x (H = subcarrier, W = symbol)
         with a (k, k, Cin, Cout) kernel (autodiff.py:324-350)."""
-        F = _torch().nn.functional
         w = self.params[name]
+        if self.kernels == "nrx":
+            return _nrx_conv_fn().apply(x, w)
+        F = _torch().nn.functional
         k = w.shape[0]
         y = F.conv2d(x.permute(0, 3, 1, 2), w.permute(3, 2, 0, 1), padding=k // 2)
         return y.permute(0, 2, 3, 1)
+
+    def _dense(self, x, name):
+        """x (..., cin) @ W (cin, cout): a 1x1 convolution of the flattened rows."""
+        w = self.params[name]
+        if self.kernels != "nrx":
+            return x @ w
+        lead = x.shape[:-1]
+        rows = x.reshape(-1, 1, 1, x.shape[-1])
+        y = _nrx_conv_fn().apply(rows, w.reshape(1, 1, w.shape[0], w.shape[1]))
+        return y.reshape(lead + (w.shape[1],))
 
     def _conv_block(self, x, prefix):
         torch = _torch()
@@ -86,8 +170,8 @@ class TorchNrxGraph:
     def _mlp(self, x, prefix):
         torch = _torch()
         p = self.params
-        h = torch.relu(x @ p[f"{prefix}.fc0.w"] + p[f"{prefix}.fc0.b"])
-        return h @ p[f"{prefix}.fc1.w"] + p[f"{prefix}.fc1.b"]
+        h = torch.relu(self._dense(x, f"{prefix}.fc0.w") + p[f"{prefix}.fc0.b"])
+        return self._dense(h, f"{prefix}.fc1.w") + p[f"{prefix}.fc1.b"]
 
     def _groups(self, mods):
         c = self.config
@@ -215,6 +299,13 @@ class Adam:
                     self.m[k] = torch.zeros_like(p)
                     self.v[k] = torch.zeros_like(p)
                 m, v = self.m[k], self.v[k]
+                if p.is_cuda:  # hand-written update kernel (csrc/k_train.cu)
+                    code = _nrx_lib().nrx_train_adam(p.numel(), p.data_ptr(), g.contiguous().data_ptr(),
+                                                     m.data_ptr(), v.data_ptr(), self.lr, self.beta1, self.beta2,
+                                                     self.epsilon, self.t, torch.cuda.current_stream(p.device).cuda_stream)
+                    if code:
+                        raise RuntimeError(f"nrx_train_adam failed ({code})")
+                    continue
                 m.mul_(self.beta1).add_((1.0 - self.beta1) * g)
                 v.mul_(self.beta2).add_((1.0 - self.beta2) * g * g)
                 p.sub_((self.lr / c1) * m / (torch.sqrt(v / c2) + self.epsilon))
