@@ -16,7 +16,7 @@
  *
  * All pointers are device pointers; each call enqueues on `stream` (a
  * cudaStream_t) and returns 0, 1 (bad argument / shape beyond the limits:
- * cin, cout <= 128, odd k) or 4 (CUDA error).
+ * cin, cout <= 128 with ceil(cin/8) * ceil(cout/4) <= 256, odd k) or 4 (CUDA error).
  */
 #ifndef NRX_TRAIN_H_
 #define NRX_TRAIN_H_

@@ -56,11 +56,18 @@ __global__ void __launch_bounds__(THREADS) k_conv_tile(Shape g, const float* __r
   const int cj = DGRAD ? g.cout : g.cin;   // contraction channels
   const int co = DGRAD ? g.cin : g.cout;   // output channels
   const int cop = (co + 3) & ~3;           // padded to a float4
+  const int cjp = cj | 1;                  // odd row stride: a thread's 4 pixels hit distinct banks (<= 2-way)
   float* Ws = sm;                          // [cj][cop]
-  float* Xs = sm + cj * cop;               // [cj][TP]  (pixel-contiguous)
+  float* Xs = sm + cj * cop;               // [TP][cjp]
+  __shared__ int s_st[TP];                 // (s << 16 | t) of the block's pixels, -1 past the end
   const int pg = threadIdx.x & 15, og = threadIdx.x >> 4;  // 16 pixel groups x 16 channel groups
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int P = g.pixels();
   const int pbase = blockIdx.x * TP;
+  if (threadIdx.x < TP) {
+    const int pp = pbase + threadIdx.x;
+    s_st[threadIdx.x] = pp < P ? (((pp / g.T) % g.S) << 16) | (pp % g.T) : -1;
+  }
   float acc[PPT][CPT];
 #pragma unroll
   for (int a = 0; a < PPT; ++a)
@@ -70,23 +77,25 @@ __global__ void __launch_bounds__(THREADS) k_conv_tile(Shape g, const float* __r
     for (int bb = 0; bb < g.k; ++bb) {
       __syncthreads();
       const float* wt = w + (size_t)(a * g.k + bb) * g.cin * g.cout;
-      for (int e = threadIdx.x; e < cj * cop; e += THREADS) {
-        const int j = e / cop, c = e - j * cop;
-        float v = 0.f;
-        if (c < co) v = DGRAD ? wt[(size_t)c * g.cout + j] : wt[(size_t)j * g.cout + c];
-        Ws[e] = v;
-      }
+      // staging without integer division: warps over rows, lanes over channels
+      for (int j = warp; j < cj; j += THREADS / 32)
+        for (int c = lane; c < cop; c += 32) {
+          float v = 0.f;
+          if (c < co) v = DGRAD ? wt[(size_t)c * g.cout + j] : wt[(size_t)j * g.cout + c];
+          Ws[j * cop + c] = v;
+        }
       const int ds = DGRAD ? g.r - a : a - g.r, dt = DGRAD ? g.r - bb : bb - g.r;
-      for (int e = threadIdx.x; e < TP * cj; e += THREADS) {  // coalesced along j
-        const int px = e / cj, j = e - px * cj;
-        const int pp = pbase + px;
-        const int src = pp < P ? shifted(g, pp, ds, dt) : -1;
-        Xs[j * TP + px] = src >= 0 ? in[(size_t)src * cj + j] : 0.f;
+      for (int px = warp; px < TP; px += THREADS / 32) {
+        const int st = s_st[px];
+        const int s2 = (st >> 16) + ds, t2 = (st & 0xffff) + dt;
+        const bool ok = st >= 0 && s2 >= 0 && s2 < g.S && t2 >= 0 && t2 < g.T;
+        const float* src = in + (size_t)(pbase + px + ds * g.T + dt) * cj;
+        for (int j = lane; j < cj; j += 32) Xs[px * cjp + j] = ok ? src[j] : 0.f;  // coalesced, conflict-free
       }
       __syncthreads();
 #pragma unroll 2
       for (int j = 0; j < cj; ++j) {
-        const float4 xv = *reinterpret_cast<const float4*>(Xs + j * TP + 4 * pg);
+        const float* xr = Xs + 4 * pg * cjp + j;
         float wv[CPT];
 #pragma unroll
         for (int c4 = 0; c4 < CPT; c4 += 4) {
@@ -96,7 +105,7 @@ __global__ void __launch_bounds__(THREADS) k_conv_tile(Shape g, const float* __r
           wv[c4 + 2] = t4.z;
           wv[c4 + 3] = t4.w;
         }
-        const float xa[PPT] = {xv.x, xv.y, xv.z, xv.w};
+        const float xa[PPT] = {xr[0], xr[cjp], xr[2 * cjp], xr[3 * cjp]};
 #pragma unroll
         for (int a2 = 0; a2 < PPT; ++a2)
 #pragma unroll
@@ -115,13 +124,13 @@ __global__ void __launch_bounds__(THREADS) k_conv_tile(Shape g, const float* __r
   }
 }
 
-constexpr int WCHUNK = 1024;  // pixels per wgrad block
+constexpr int WCHUNK = 1024;  // max pixels per wgrad block (fewer when there are few taps)
 constexpr int WTP = 32;       // pixels staged per step
 
 // dw[tap] (+)= sum over a pixel chunk of x[p + shift(tap)] (outer) dy[p]; thread
 // (ti, to) owns i in [8 ti, 8 ti + 8), o in [4 to, 4 to + 4).  Tap-0 blocks
 // also accumulate db.  Partials are added with fp32 atomics.
-__global__ void __launch_bounds__(THREADS) k_conv_wgrad(Shape g, const float* __restrict__ x,
+__global__ void __launch_bounds__(THREADS) k_conv_wgrad(Shape g, int chunk, const float* __restrict__ x,
                                                         const float* __restrict__ dy, float* __restrict__ dw,
                                                         float* __restrict__ db) {
   extern __shared__ __align__(16) float sm[];
@@ -130,25 +139,25 @@ __global__ void __launch_bounds__(THREADS) k_conv_wgrad(Shape g, const float* __
   float* Ds = sm + WTP * cip;      // [WTP][cop]
   const int tap = blockIdx.y, a = tap / g.k, bb = tap % g.k;
   const int P = g.pixels();
-  const int p0 = blockIdx.x * WCHUNK;
+  const int p0 = blockIdx.x * chunk;  // chunk: a multiple of WTP
   const int ti = threadIdx.x >> 4, to = threadIdx.x & 15;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ds = a - g.r, dt = bb - g.r;
   const bool active = 8 * ti < g.cin && 4 * to < g.cout;
   float acc[8][4], bacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int o = 0; o < 4; ++o) acc[i][o] = 0.f;
-  for (int pt = p0; pt < p0 + WCHUNK && pt < P; pt += WTP) {
+  for (int pt = p0; pt < p0 + chunk && pt < P; pt += WTP) {
     __syncthreads();
-    for (int e = threadIdx.x; e < WTP * cip; e += THREADS) {
-      const int px = e / cip, i = e - px * cip;
+    for (int px = warp; px < WTP; px += THREADS / 32) {  // warps over pixels, lanes over channels
       const int pp = pt + px;
-      const int src = (pp < P && i < g.cin) ? shifted(g, pp, a - g.r, bb - g.r) : -1;
-      Xs[e] = src >= 0 ? x[(size_t)src * g.cin + i] : 0.f;
-    }
-    for (int e = threadIdx.x; e < WTP * cop; e += THREADS) {
-      const int px = e / cop, o = e - px * cop;
-      Ds[e] = (pt + px < P && o < g.cout) ? dy[(size_t)(pt + px) * g.cout + o] : 0.f;
+      const int src = pp < P ? shifted(g, pp, ds, dt) : -1;
+      for (int i = lane; i < cip; i += 32)
+        Xs[px * cip + i] = (src >= 0 && i < g.cin) ? x[(size_t)src * g.cin + i] : 0.f;
+      for (int o = lane; o < cop; o += 32)
+        Ds[px * cop + o] = (pp < P && o < g.cout) ? dy[(size_t)pp * g.cout + o] : 0.f;
     }
     __syncthreads();
     if (!active) continue;
@@ -201,7 +210,7 @@ static int launch_tile(const Shape& g, const float* in, const float* w, const fl
                        cudaStream_t st) {
   const int co = DGRAD ? g.cin : g.cout, cj = DGRAD ? g.cout : g.cin;
   const int cop = (co + 3) & ~3;
-  const size_t smem = (size_t)(cj * cop + cj * TP) * 4;
+  const size_t smem = (size_t)(cj * cop + TP * (cj | 1)) * 4;
   const int blocks = (g.pixels() + TP - 1) / TP;
   auto run = [&](auto kern) -> int {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 4;
@@ -247,8 +256,14 @@ int nrx_train_conv_wgrad(int n, int S, int T, int cin, int cout, int k, const fl
   if (db && cudaMemsetAsync(db, 0, (size_t)cout * 4, st) != cudaSuccess) return 4;
   const int cip = (cin + 7) & ~7, cop = (cout + 3) & ~3;
   const size_t smem = (size_t)WTP * (cip + cop) * 4;
-  dim3 grid((g.pixels() + WCHUNK - 1) / WCHUNK, k * k);
-  k_conv_wgrad<<<grid, THREADS, smem, st>>>(g, x, dy, dw, db);
+  // >= ~4 blocks per SM: chunks of WCHUNK pixels, smaller (multiples of WTP) for few taps
+  const int want = (4 * 148 + k * k - 1) / (k * k);
+  int chunks = (g.pixels() + WCHUNK - 1) / WCHUNK;
+  if (chunks < want) chunks = want;
+  const int per = ((g.pixels() + chunks - 1) / chunks + WTP - 1) / WTP * WTP;
+  chunks = (g.pixels() + per - 1) / per;
+  dim3 grid(chunks, k * k);
+  k_conv_wgrad<<<grid, THREADS, smem, st>>>(g, per, x, dy, dw, db);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 4;
 }
 
