@@ -47,6 +47,11 @@ extern "C" {
 #define NRX_ABI_VERSION 1
 #define NRX_MAX_PILOT_SYMBOLS 16
 #define NRX_MAX_IO 4
+/* Byte offset in the workspace of a uint32 the tensor-core modes set to
+ * nonzero when a readout produced a non-finite LLR / channel value (fp16
+ * operand planes overflow above 65504); nrx_forward zeroes it first.  The
+ * drop-in re-runs such a call on the fp32 SIMT kernels. */
+#define NRX_WS_FLAG_OFFSET 0
 
 typedef enum nrx_status {
   NRX_OK = 0,

@@ -13,6 +13,8 @@
 //
 // HBM-bound: per RE-slab it reads 8*B bytes of y (c64) and writes
 // Cf * sizeof(out) bytes; pilot samples are re-read from L1/L2.
+#include <type_traits>
+
 #include "nrx_device.cuh"
 #include "nrx_kernels.h"
 
@@ -123,18 +125,26 @@ __global__ void __launch_bounds__(128) k_ls_feat(Geom g, const YT* __restrict__ 
   }
   const int nch = g.Cf / CW;
   if constexpr (X3) {
+    uint32_t bad = 0;
 #pragma unroll
     for (int c = 0; c < 48 / CW; ++c)
       if (c < nch) {
         uint4 hi, lo;
-        split_chunk(f + c * CW, hi, lo);
+        split_chunk(f + c * CW, hi, lo, bad);
         *reinterpret_cast<uint4*>(chunk_ptr(feats, slab, 2 * nch, c, row, g)) = hi;
         *reinterpret_cast<uint4*>(chunk_ptr(feats, slab, 2 * nch, nch + c, row, g)) = lo;
       }
+    report_range(bad, g.flag);
   } else {
 #pragma unroll
     for (int c = 0; c < 48 / CW; ++c)
       if (c < nch) store_chunk(chunk_ptr(feats, slab, nch, c, row, g), f + c * CW);
+    if (std::is_same<OutT, __half>::value) {  // fp16 features: the same range guard
+      uint32_t bad = 0;
+#pragma unroll
+      for (int c = 0; c < 48; ++c) bad |= (__float_as_uint(f[c]) & 0x7fffffffu) > 0x477fe000u;
+      report_range(bad, g.flag);
+    }
   }
 }
 

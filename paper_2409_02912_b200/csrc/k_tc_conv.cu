@@ -424,8 +424,13 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         tmem_ld16(tcol + 16, o + 16);
         tmem_wait_ld();
         if (valid) {
+          uint32_t bad = 0;
 #pragma unroll
-          for (int c = 0; c < 32; ++c) o[c] += stb1[c];
+          for (int c = 0; c < 32; ++c) {
+            o[c] += stb1[c];
+            bad |= (__float_as_uint(o[c]) & 0x7f800000u) == 0x7f800000u;
+          }
+          if (bad && g.flag) atomicOr(g.flag, 1u);
           const int mio = io_index(p.mod_order, jslab, g);
           const int width = mio < 0 ? 0 : g.io_width[mio];
           const size_t re = ((size_t)jslab * g.S + s) * g.T + t;

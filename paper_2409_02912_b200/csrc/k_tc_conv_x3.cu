@@ -520,6 +520,7 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_
       real = nreal;
       if (!cur_real) continue;
 
+      uint32_t bad = 0;  // range guard (fp16 planes)
       const float pdt = (MODE != EPI_RELU && valid) ? sdt[t] : 0.f;
       const float pdf = (MODE != EPI_RELU && valid) ? pos_df(s, cslab % g.U, g) : 0.f;
 #pragma unroll
@@ -547,13 +548,14 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_
         }
         if constexpr (SPLIT) {
           uint4 hi, lo;
-          split_chunk(x, hi, lo);
+          split_chunk(x, hi, lo, bad);
           *reinterpret_cast<uint4*>(drow + cc * dcs) = hi;
           *reinterpret_cast<uint4*>(drow + (nd + cc) * dcs) = lo;
         } else {
           *reinterpret_cast<uint4*>(drow + cc * dcs) = pack_chunk(x, static_cast<const ET*>(nullptr));
         }
       }
+      report_range(bad, g.flag);
       if (part == PARTS - 1) {  // buffer channels beyond the accumulator: positional / zero only
         for (int cc = NP / 8; cc < nd; ++cc) {
           if (MODE == EPI_RESIDUAL) break;  // written once by the state init

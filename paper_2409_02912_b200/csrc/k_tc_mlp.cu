@@ -252,7 +252,9 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
 #pragma unroll
               for (int e = 0; e < 8; ++e) o[e] = fmaxf(__fadd_rn(__fmul_rn(v[8 * c8 + e], dsc), s.sb0[8 * ch + e]), 0.f);
               uint4 hi, lo;
-              split_chunk(o, hi, lo);
+              uint32_t bad = 0;
+              split_chunk(o, hi, lo, bad);
+              report_range(bad, g.flag);
               *reinterpret_cast<uint4*>(H + ((size_t)ch * NRX_TILE_M + r) * 16) = hi;
               *reinterpret_cast<uint4*>(H + ((size_t)(p.hp / 8 + ch) * NRX_TILE_M + r) * 16) = lo;
             } else {
@@ -361,7 +363,9 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
           }
           if constexpr (X3) {  // [hi | lo] planes of the aggregate
             uint4 hi, lo;
-            split_chunk(o, hi, lo);
+            uint32_t bad = 0;
+            split_chunk(o, hi, lo, bad);
+            report_range(bad, g.flag);
             *reinterpret_cast<uint4*>(chunk_ptr(agg, n * U + u, 2 * nca, c8, row, g)) = hi;
             *reinterpret_cast<uint4*>(chunk_ptr(agg, n * U + u, 2 * nca, nca + c8, row, g)) = lo;
           } else {
@@ -393,8 +397,13 @@ __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
     const int row = tile * NRX_TILE_M + r;
     const int srow = row / g.Tp, t = row - srow * g.Tp;
     if (row >= g.rows_data || t >= g.T) return;
+    uint32_t bad = 0;
 #pragma unroll
-    for (int c = 0; c < 32; ++c) o[c] = X3 ? __fadd_rn(__fmul_rn(o[c], dsc), s.sb1[c]) : o[c] + s.sb1[c];
+    for (int c = 0; c < 32; ++c) {
+      o[c] = X3 ? __fadd_rn(__fmul_rn(o[c], dsc), s.sb1[c]) : o[c] + s.sb1[c];
+      bad |= (__float_as_uint(o[c]) & 0x7f800000u) == 0x7f800000u;
+    }
+    if (bad && g.flag) atomicOr(g.flag, 1u);  // range guard (nrx_forward)
     const int mio = io_index(p.mod_order, slab, g);
     const int width = mio < 0 ? 0 : g.io_width[mio];
     const size_t re = ((size_t)slab * g.S + srow) * g.T + t;

@@ -91,6 +91,10 @@ extern "C" int nrx_forward(const nrx_model_desc* model, const nrx_slot_desc* slo
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   const uint8_t* wb = static_cast<const uint8_t*>(packed_weights);
+  // range guard of the half-precision operand modes: the readouts set this
+  // word when an output is not finite (fp16 planes overflow above 65504)
+  g.flag = precision == NRX_FP32 ? nullptr : reinterpret_cast<uint32_t*>(ws + W.flag);
+  if (g.flag && cudaMemsetAsync(g.flag, 0, 4, st) != cudaSuccess) return NRX_ERR_CUDA;
 
   {
     ProfScope p(KID_LSFEAT, st);

@@ -177,6 +177,19 @@ __device__ __forceinline__ void split_chunk(const float* v, uint4& hi, uint4& lo
   hi = make_uint4(h[0], h[1], h[2], h[3]);
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
+// split_chunk that also records a range violation: |v| > 65504 (the fp16
+// maximum), inf or NaN.  A NaN from an overflowed plane would otherwise be
+// swallowed by the next ReLU (fmaxf), so every split checks.
+__device__ __forceinline__ void split_chunk(const float* v, uint4& hi, uint4& lo, uint32_t& bad) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) bad |= (__float_as_uint(v[i]) & 0x7fffffffu) > 0x477fe000u;
+  split_chunk(v, hi, lo);
+}
+// the range-guard word (Geom::flag, NRX_WS_FLAG_OFFSET): one atomic per offending thread
+__device__ __forceinline__ void report_range(uint32_t bad, uint32_t* flag) {
+  if (bad && flag) atomicOr(flag, 1u);
+}
+
 // hi + lo 2^-11 in fp32 (exact: both terms fit the 24-bit significand)
 __device__ __forceinline__ void unsplit_chunk(uint4 hi, uint4 lo, float* v) {
   const uint32_t h[4] = {hi.x, hi.y, hi.z, hi.w}, l[4] = {lo.x, lo.y, lo.z, lo.w};

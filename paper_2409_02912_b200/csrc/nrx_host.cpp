@@ -599,6 +599,7 @@ void ws_layout(const Geom& g, WsLayout* w) {
   const size_t plane = (size_t)g.NU * g.rows_slab * esz * (g.prec == NRX_FP32X3 ? 2 : 1);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+  w->flag = take(4);  // offset 0 (NRX_WS_FLAG_OFFSET)
   w->feats = take(plane * g.Cf);
   w->h = take(plane * g.Ch);
   w->state = take(plane * g.Cs);

@@ -56,6 +56,7 @@ struct Geom {
   int prec;
   float dt[32];               // positional encoding, symbol axis (float32, nrx.py:164)
   int nearest[32];            // nearest pilot-symbol index per t (classical.py:71)
+  uint32_t* flag;             // workspace word set when a tensor-core readout wrote a non-finite output
 };
 
 // Byte offsets of each weight sub-buffer inside the packed blob.
@@ -75,7 +76,7 @@ struct PackLayout {
 };
 
 struct WsLayout {
-  size_t feats, h, state, agg, state32, total;
+  size_t flag, feats, h, state, agg, state32, total;  // flag: uint32 at workspace offset 0
 };
 
 }  // namespace nrx

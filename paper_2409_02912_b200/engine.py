@@ -285,7 +285,7 @@ class NrxEngine:
         into pinned staging (one pass); the results are pinned-memory arrays
         (see _pinned_outputs)."""
         return self.finish(self.enqueue_arrays(cfg, y, pilot_vals, noise_feat, mod_order, num_iterations,
-                                               llr_width, exact_inputs))
+                                               llr_width, exact_inputs))[:2]
 
     def enqueue_arrays(self, cfg, y, pilot_vals, noise_feat, mod_order, num_iterations, llr_width,
                        exact_inputs=False):
@@ -313,14 +313,26 @@ class NrxEngine:
                 d.copy_(h, non_blocking=True)
             d_llr = self._staging("llr", (n, U, S, T, llr_width), torch.float32, False)
             d_chest = self._staging("chest", (n, U, S, T, B), torch.complex64, False)
-            self.forward_device(cfg, d_y, d_p, d_n, d_m, num_iterations, d_llr, d_chest, stream=tls.stream)
+            ws = self.workspace(cfg, n)
+            self.forward_device(cfg, d_y, d_p, d_n, d_m, num_iterations, d_llr, d_chest, workspace=ws,
+                                stream=tls.stream)
             h_llr, h_chest, llr_np, chest_np = self._pinned_outputs(d_llr.shape, d_chest.shape)
             h_llr.copy_(d_llr, non_blocking=True)
             h_chest.copy_(d_chest, non_blocking=True)
-        return tls.stream, llr_np, chest_np
+            h_flag = self._staging("flag", (4,), torch.uint8, True)
+            h_flag.copy_(ws[:4], non_blocking=True)  # NRX_WS_FLAG_OFFSET: non-finite readout output
+        return tls.stream, llr_np, chest_np, h_flag
 
     @staticmethod
     def finish(handle):
-        stream, llr_np, chest_np = handle
+        """Wait for enqueue_arrays' work; returns (llr, chest, nonfinite) where
+        nonfinite is the range-guard word of a tensor-core mode."""
+        stream, llr_np, chest_np, h_flag = handle
         stream.synchronize()
-        return llr_np, chest_np
+        return llr_np, chest_np, bool(h_flag.numpy().any())
+
+    def nonfinite_flag(self, workspace):
+        """Device view of the range-guard word (NRX_WS_FLAG_OFFSET) of a
+        workspace after forward_device: nonzero when a tensor-core readout
+        wrote a non-finite output (fp16 operand overflow)."""
+        return workspace[:4].view(_require_cuda().int32)

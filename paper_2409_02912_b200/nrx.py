@@ -16,6 +16,7 @@ evaluation.py:24,144-154,343-347).
 from __future__ import annotations
 
 import threading
+import warnings
 import zlib
 
 import numpy as np
@@ -171,12 +172,19 @@ def nrx_forward(y, books, cfg, mcs_per_ue, w, config, n0, num_iterations=None, a
         # step, autodiff.py:525) repack and run again
         handle = eng.enqueue_arrays(*args)
         fp = _fingerprint(w)
-        llr_full, chest = eng.finish(handle)
+        llr_full, chest, nonfinite = eng.finish(handle)
         if fp != fp_packed:
             eng = get_engine(w, config, precision, device, check_weights, fingerprint=fp)
-            llr_full, chest = eng.run_arrays(*args)
+            llr_full, chest, nonfinite = eng.finish(eng.enqueue_arrays(*args))
     else:
         eng = get_engine(w, config, precision, device, check_weights)
+        llr_full, chest, nonfinite = eng.finish(eng.enqueue_arrays(*args))
+    if nonfinite and precision != "fp32_simt" and np.isfinite(y).all():
+        # range guard: an fp16 operand plane overflowed (|activation| > 65504);
+        # the fp32 SIMT kernels compute this call with the reference's range
+        warnings.warn(f"nrx_forward: {precision} tensor-core path overflowed its fp16 operand range; "
+                      "recomputing this call with precision='fp32_simt'", RuntimeWarning, stacklevel=2)
+        eng = get_engine(w, config, "fp32_simt", device, check_weights)
         llr_full, chest = eng.run_arrays(*args)
     llrs = []
     for u in range(U):

@@ -278,3 +278,27 @@ def test_pdl_launch_bit_identical_to_stream_order(tmp_path):
             res[pdl] = {k: z[k] for k in z.files}
     for k in res["1"]:
         np.testing.assert_array_equal(res["1"][k], res["0"][k], err_msg=k)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
+def test_range_guard_reruns_on_fp32_simt(precision):
+    """Inputs far outside the fp16 operand range (received grid scaled by 1e5:
+    features ~1e5 > 65504): the tensor-core readout flags the non-finite
+    outputs (NRX_WS_FLAG_OFFSET) and the drop-in recomputes the call on the
+    fp32 SIMT kernels with a RuntimeWarning -- results stay within the fp32
+    gate of the float64 oracle instead of turning into NaN."""
+    _, gnrx = _gpu()
+    from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights
+    from paper_2409_02912_b200.synth import synth_slots
+    t = default_mcs_table()
+    cfg = SlotConfig(num_subcarriers=96, num_ues=2, comb_size=2)
+    config = NrxConfig.from_table(t, (14,), d_s=56, num_iterations=2)
+    w = orc.perturb_biases(init_weights(config, 2))
+    mcs = (t[14], t[14])
+    y, books, _ = synth_slots(cfg, [4, 4], 1, 0.1, seed=8)
+    y = y * 1e5
+    ref, _ = orc.nrx_forward(y, books, cfg, mcs, w, config, 0.1, dtype=np.float64)
+    with pytest.warns(RuntimeWarning, match="fp32_simt"):
+        got, chest = gnrx.nrx_forward(y, books, cfg, mcs, w, config, 0.1, precision=precision)
+    assert np.isfinite(chest).all()
+    check_llrs(got, ref, "fp32_simt", "range guard")
