@@ -607,6 +607,13 @@ static X3Fn select_conv_x3(const Geom& g, int mode, int c0, int c1, int prec) {
   }
   static const X3Fn generic[3] = {k_conv_x3<NP, 0>, k_conv_x3<NP, 1>, k_conv_x3<NP, 2>};
   X3Fn fn = generic[mode];
+  if (NP == 16 && g.ks == 3) {  // the desk models (d_s = 16): features 32, state 32, h / messages 16 channels
+    const int nk0 = c0 / 16, nk1 = c1 / 16;
+    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_x3<16, EPI_RELU, 3, 2, 0>;
+    if (mode == EPI_RELU && nk0 == 2 && nk1 == 1) fn = k_conv_x3<16, EPI_RELU, 3, 2, 1>;
+    if (mode == EPI_STATE_INIT && nk0 == 1 && nk1 == 0) fn = k_conv_x3<16, EPI_STATE_INIT, 3, 1, 0>;
+    if (mode == EPI_RESIDUAL && nk0 == 1 && nk1 == 0) fn = k_conv_x3<16, EPI_RESIDUAL, 3, 1, 0>;
+  }
   if (NP == 56 && g.ks == 3) {  // fully unrolled issue for the RT / large models' 3x3 layers
     const int nk0 = c0 / 16, nk1 = c1 / 16;
     if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_x3<56, EPI_RELU, 3, 2, 0>;
