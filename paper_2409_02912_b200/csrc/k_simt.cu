@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(256, 2) k_conv_simt(Geom g, ConvArgs a) {
         if (valid) {
           if (c < g.d) {
             float x = acc[i][4 * half + e] + bias[c];
-            if (a.mode == EPI_RELU) x = fmaxf(x, 0.f);
+            if (a.mode == EPI_RELU) x = relu_f(x);
             else if (a.mode == EPI_RESIDUAL) x = old[e] + x;
             val = x;
           } else if (a.mode != EPI_RELU) {
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(128) k_msg_agg_simt(Geom g, const uint8_t* __r
         float acc = 0.f;
 #pragma unroll
         for (int i = 0; i < DM; ++i) acc = fmaf(x[i], W0[i * g.h + j], acc);
-        const float hj = fmaxf(acc + b0[j], 0.f);
+        const float hj = relu_f(acc + b0[j]);
 #pragma unroll
         for (int c = 0; c < DM; ++c) msg[c] = fmaf(hj, W1[j * DM + c], msg[c]);
       }
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(128) k_readout_simt(Geom g, const uint8_t* __r
       al = fmaf(x[i], lW0[i * h + j], al);
       ac = fmaf(x[i], cW0[i * h + j], ac);
     }
-    const float hl = fmaxf(al + lb0[j], 0.f), hc = fmaxf(ac + cb0[j], 0.f);
+    const float hl = relu_f(al + lb0[j]), hc = relu_f(ac + cb0[j]);
 #pragma unroll
     for (int c = 0; c < 8; ++c) ol[c] = fmaf(hl, lW1[j * 8 + c], ol[c]);
 #pragma unroll

@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           float y = x[e] + bb[e];  // conv + bias first, as the reference adds them
-          if (MODE == EPI_RELU) y = fmaxf(y, 0.f);
+          if (MODE == EPI_RELU) y = relu_f(y);
           if (MODE == EPI_RESIDUAL) y = (MASTER ? old[8 * c8 + e] : o8[e]) + y;
           x[e] = (valid && (full || 8 * cc + e < g.d)) ? y : 0.f;
         }

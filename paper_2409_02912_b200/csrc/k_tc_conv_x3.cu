@@ -179,6 +179,8 @@ struct ConvX3Params {
   int np;            // pair MMA N = rup(d, 32); each CTA holds np/2 B rows
   int nacc;          // partial accumulators per tile (hi*Whi MMAs by tap row)
   int cdst, stages, n_io, src1_xor, hup;
+  int posf, kc;      // positional channels folded out (upd0_posf): both sources' kc chunks share one stage
+  int ptab;          // posf: per-(comb residue, symbol) table of the positional contribution in shared memory
   uint32_t wbytes;   // one rank's weight block: [hi | lo][taps*ktap/8][np/2][8] fp16
   uint32_t abytes, tmem_cols, rbox;
   const uint8_t* wbase;
@@ -188,7 +190,7 @@ struct ConvX3Params {
 };
 
 struct ConvX3Smem {
-  uint32_t w, a, bars, tmem_ptr, sbias, dt, total;
+  uint32_t w, a, bars, tmem_ptr, sbias, dt, posw, ptab, total;
 };
 __host__ __device__ inline ConvX3Smem conv_x3_smem(const ConvX3Params& p) {
   ConvX3Smem s;
@@ -205,6 +207,10 @@ __host__ __device__ inline ConvX3Smem conv_x3_smem(const ConvX3Params& p) {
   off += 80 * 4;
   s.dt = off;
   off += 32 * 4;
+  s.posw = off;
+  off += p.posf ? 18 * p.np * 4 : 0;
+  s.ptab = off;
+  off += p.posf && p.ptab ? p.g.comb * p.g.T * (p.np + 4) * 4 : 0;  // rows padded: conflict-free by symbol
   s.total = off;
   return s;
 }
@@ -221,7 +227,19 @@ __host__ __device__ constexpr int x3_epi_cols(int mode) { return mode == EPI_RES
 // and iteration.update.conv0): each CTA holds the weights of np/2 output
 // channels, an N = np pair MMA reads 4 KB of A and 1 KB of B per SM (5 KB
 // instead of 6 KB single-CTA: 40 instead of 48 cycles per K=16 step).
-template <int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0, int PREC = NRX_FP32X3>
+//
+// POSF (iteration.update.conv0, upd0_posf): the A operand is [state (d) |
+// agg (d)] without the two positional channels -- both sources land in one
+// stage (kc chunks each, contiguous, so a K=16 step may straddle them) and
+// the K loop runs NK0 = d/8 steps; the epilogue adds the positional
+// contribution sum_{tap, ch} W_pos[ch][tap][c] pos_ch(s + a - 1, t + b - 1)
+// (zero outside the grid, as the reference's zero padding) in fp32.  pos_dt
+// depends on t only and pos_df on the distance to the UE's comb, so away from
+// the band edges (o < s < S - comb - 1, o the UE's comb offset) the sum is a
+// function of ((s - o) mod comb, t): each CTA tabulates it once (comb x T x np
+// fp32, before griddepcontrol.wait) and the epilogue adds one table row; edge
+// rows evaluate the 18 terms.
+template <int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0, int PREC = NRX_FP32X3, bool POSF = false>
 __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_epi_cols(MODE)), 1)
     k_conv_x3(const __grid_constant__ ConvX3Params p, const __grid_constant__ CUtensorMap map0,
               const __grid_constant__ CUtensorMap map1) {
@@ -232,6 +250,7 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_
   constexpr int BROWS = SPLIT ? NP : NP / 2;  // B rows held by each CTA
   constexpr int DST = SPLIT ? (NB + 31) / 32 * 32 : NB;  // TMEM columns per partial accumulator
   static_assert(SPLIT || MODE == EPI_RELU, "half-precision pair kernels: ReLU layers only");
+  static_assert(!POSF || (KS == 3 && NK1 == 0 && MODE == EPI_RELU), "positional fold: 3x3 update.conv0 only");
   // 32 accumulator columns per epilogue thread: 2 + 4 * NP/32 warps (10 for
   // NP = 64) leave each SM sub-partition <= 3 warps, i.e. up to 168 registers
   // for the fully unrolled MMA issue (18 warps would cap it at 96 and spill)
@@ -255,6 +274,8 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L.tmem_ptr);
   float* sbias = reinterpret_cast<float*>(smem + L.sbias);
   float* sdt = reinterpret_cast<float*>(smem + L.dt);
+  float* sposw = reinterpret_cast<float*>(smem + L.posw);
+  float* sptab = reinterpret_cast<float*>(smem + L.ptab);
   const uint32_t B_full = smem_u32(full), B_empty = smem_u32(empty), B_tfull = smem_u32(tfull),
                  B_tempty = smem_u32(tempty), B_wbar = smem_u32(wbar), B_wpeer = smem_u32(wpeer);
 
@@ -279,6 +300,32 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_
   if (threadIdx.x >= 64 && threadIdx.x <= 64 + NP)  // bias[0..NP) and the descale 2^-E at [NP]
     sbias[threadIdx.x - 64] = reinterpret_cast<const float*>(p.wbase + p.b_off[io])[threadIdx.x - 64];
   if (threadIdx.x < 32) sdt[threadIdx.x] = g.dt[threadIdx.x];
+  if constexpr (POSF) {
+    const float* pw = reinterpret_cast<const float*>(p.wbase + p.b_off[0]) + (NP + 4);  // posw_off(NP)
+    for (int i = threadIdx.x; i < 18 * NP; i += blockDim.x) sposw[i] = pw[i];
+  }
+  if constexpr (POSF) {
+    if (p.ptab) {  // interior positional contribution per (comb residue, symbol): weights and geometry only
+      __syncthreads();
+      const int cb = g.comb, n = cb * g.T * NP;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int c = i % NP, t = (i / NP) % g.T, r = i / (NP * g.T);
+        float acc = 0.f;
+        for (int a = 0; a < 3; ++a) {
+          int q = (r + a - 1 + cb) % cb;
+          q = q < cb - q ? q : cb - q;  // comb distance of the neighbour row
+          const float f = g.freq_enc ? (cb <= 16 ? g.df_tab[q] : __fdiv_rn((float)q, (float)g.S)) : 0.f;
+          for (int b = 0; b < 3; ++b) {
+            const int t2 = t + b - 1;
+            if (t2 < 0 || t2 >= g.T) continue;
+            acc = fmaf(sdt[t2], sposw[(3 * a + b) * NP + c], acc);
+            acc = fmaf(f, sposw[(9 + 3 * a + b) * NP + c], acc);
+          }
+        }
+        sptab[(r * g.T + t) * (NP + 4) + c] = acc;
+      }
+    }
+  }
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / TMA
@@ -306,6 +353,18 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_
       uint32_t ph = 0;
       while (w.next(slab, tile, real)) {
         const int grp0 = (tile * NRX_TILE_M - p.hup) / 16;
+        if constexpr (POSF) {  // one stage per plane: [src0 kc chunks | src1 kc chunks]
+          for (int pl = 0; pl < NPL; ++pl) {
+            mbar_wait_backoff(B_empty + 8u * st, ph ^ 1, 64);
+            if (rank == 0) mbar_expect_tx(B_full + 8u * st, 2u * 2u * (uint32_t)p.kc * R * 16);
+            const uint32_t dst = As_s + st * p.abytes;
+            tma_load_4d_pair(dst, &map0, full_leader + 8u * st, 0, grp0, SPLIT && pl == 0 ? p.c0 / 8 : 0, slab);
+            tma_load_4d_pair(dst + (uint32_t)p.kc * R * 16, &map1, full_leader + 8u * st, 0, grp0,
+                             SPLIT && pl == 0 ? p.c1 / 8 : 0, slab ^ p.src1_xor);
+            if (++st == p.stages) { st = 0; ph ^= 1; }
+          }
+          continue;
+        }
         for (int pl = 0; pl < NPL; ++pl) {  // lo planes first (their MMAs run first), then hi
           for (int src = 0; src < nsrc; ++src) {
             const int cs = src ? p.c1 : p.c0;
@@ -521,6 +580,34 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_
       if (!cur_real) continue;
 
       uint32_t bad = 0;  // range guard (fp16 planes)
+      float pc[POSF ? 18 : 1];  // coefficients of W_pos[ch][tap]: pos_ch(s + a - 1, t + b - 1), 0 outside
+      int prow = -1;            // row of the interior table, or -1: evaluate the 18 terms
+      if constexpr (POSF) {
+        const int u = cslab % g.U;
+        const int o = u < g.comb ? u : u % g.comb;
+        if (p.ptab && !valid) {
+          prow = 0;  // pad row: stored as zero whatever the sum (keeps the warp on the table path)
+        } else if (p.ptab && s > o && s < g.S - g.comb - 1) {
+          const unsigned x = (unsigned)(s - o);
+          const int q = g.comb == 1 ? 0 : (int)(x - (unsigned)g.comb * __umulhi(x, g.comb_magic));
+          prow = q * g.T + t;
+        }
+        if (prow < 0) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const int s2 = s + a - 1;
+            const bool ins = valid && s2 >= 0 && s2 < g.S;
+            const float f = ins ? pos_df(s2, u, g) : 0.f;
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              const int t2 = t + b - 1;
+              const bool in = ins && t2 >= 0 && t2 < g.T;
+              pc[3 * a + b] = in ? sdt[t2] : 0.f;
+              pc[9 + 3 * a + b] = in ? f : 0.f;
+            }
+          }
+        }
+      }
       const float pdt = (MODE != EPI_RELU && valid) ? sdt[t] : 0.f;
       const float pdf = (MODE != EPI_RELU && valid) ? pos_df(s, cslab % g.U, g) : 0.f;
 #pragma unroll
@@ -528,13 +615,30 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_
         const int cc = cbase / 8 + c8;
         if (MODE == EPI_RESIDUAL && cc >= dch) continue;  // constant positional / zero chunk
         if (cc >= nd || 8 * cc >= NP) continue;         // past the buffer / the accumulator
-        float bb[8], x[8];
+        float bb[8], x[8], pz[8];
         ld_shared_f8(sbias_s + 32u * cc, bb);
         const bool full = 8 * cc + 8 <= g.d;
 #pragma unroll
+        for (int e = 0; e < 8; ++e) pz[e] = 0.f;
+        if constexpr (POSF) {
+          if (prow >= 0) {
+            ld_shared_f8(smem_u32(sptab) + 4u * (uint32_t)(prow * (NP + 4) + 8 * cc), pz);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 18; ++k) {
+              float wp[8];
+              ld_shared_f8(smem_u32(sposw) + 4u * (uint32_t)(k * NP + 8 * cc), wp);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) pz[e] = fmaf(pc[k], wp[e], pz[e]);
+            }
+          }
+        }
+#pragma unroll
         for (int e = 0; e < 8; ++e) {
-          float y = __fadd_rn(__fmul_rn(v[8 * c8 + e], descale), bb[e]);  // conv (exact 2^-E) + bias, as the reference
-          if (MODE == EPI_RELU) y = fmaxf(y, 0.f);
+          // conv (exact 2^-E; + the folded positional terms) + bias, as the reference
+          float y = __fadd_rn(POSF ? __fadd_rn(__fmul_rn(v[8 * c8 + e], descale), pz[e]) : __fmul_rn(v[8 * c8 + e], descale),
+                              bb[e]);
+          if (MODE == EPI_RELU) y = relu_f(y);
           if (MODE == EPI_RESIDUAL) y = old[8 * c8 + e] + y;
           x[e] = (valid && (full || 8 * cc + e < g.d)) ? y : 0.f;
         }
@@ -592,7 +696,12 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_
 using X3Fn = void (*)(const ConvX3Params, const CUtensorMap, const CUtensorMap);
 
 template <int NP>
-static X3Fn select_conv_x3(const Geom& g, int mode, int c0, int c1, int prec) {
+static X3Fn select_conv_x3(const Geom& g, int mode, int c0, int c1, int prec, bool posf) {
+  if (posf) {  // update.conv0 without the positional channels in K (upd0_posf)
+    if constexpr (NP == 56) return g.d == 56 ? k_conv_x3<56, EPI_RELU, 3, 7, 0, NRX_FP32X3, true> : nullptr;
+    if constexpr (NP == 16) return g.d == 16 ? k_conv_x3<16, EPI_RELU, 3, 2, 0, NRX_FP32X3, true> : nullptr;
+    return nullptr;
+  }
   if (prec != NRX_FP32X3) {  // half-precision pair kernels: ReLU layers only, np 32 / 64
     if constexpr (NP == 32 || NP == 64) {
       const bool f16 = prec == NRX_FP16;
@@ -626,13 +735,13 @@ static X3Fn select_conv_x3(const Geom& g, int mode, int c0, int c1, int prec) {
 
 // 4-D map over a split buffer [NU][2C/8][rows][8] fp16 whose box covers the
 // C/8 chunks of one plane (the plane is picked by the chunk coordinate).
-static int make_map_plane(CUtensorMap* m, const void* base, const Geom& g, int C, int rbox) {
+static int make_map_plane(CUtensorMap* m, const void* base, const Geom& g, int C, int rbox, int box_chunks) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return NRX_ERR_NO_DEVICE;
   if (rbox % 16 || g.rows_slab % 16) return NRX_ERR_UNSUPPORTED;
   const cuuint64_t dims[4] = {128, (cuuint64_t)(g.rows_slab / 16), (cuuint64_t)(2 * C / 8), (cuuint64_t)g.NU};
   const cuuint64_t strides[3] = {256, (cuuint64_t)g.rows_slab * 16, (cuuint64_t)(2 * C / 8) * g.rows_slab * 16};
-  const cuuint32_t box[4] = {128, (cuuint32_t)(rbox / 16), (cuuint32_t)(C / 8), 1};
+  const cuuint32_t box[4] = {128, (cuuint32_t)(rbox / 16), (cuuint32_t)box_chunks, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -657,10 +766,13 @@ int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, cons
   p.n_io = c.n_off;
   p.hup = rup(g.H, 16);
   p.rbox = NRX_TILE_M + 2 * p.hup;
-  const int ktap = c.c0 + c.c1;
+  p.posf = c.posf ? 1 : 0;
+  p.kc = g.d / 8;
+  if (c.posf && (g.d % 8 || !c.c1)) return NRX_ERR_UNSUPPORTED;
+  const int ktap = c.posf ? 2 * g.d : c.c0 + c.c1;
   // split: W_hi (rank 0) or W_lo (rank 1) for every output channel; else np/2 output channels
   p.wbytes = (uint32_t)(g.ks * g.ks * ktap * (split ? p.np : p.np / 2) * 2);
-  p.abytes = (uint32_t)((c.c0 > c.c1 ? c.c0 : c.c1) * p.rbox * 2);
+  p.abytes = c.posf ? (uint32_t)(2 * p.kc * p.rbox * 16) : (uint32_t)((c.c0 > c.c1 ? c.c0 : c.c1) * p.rbox * 2);
   p.wbase = wb;
   for (int i = 0; i < p.n_io; ++i) {
     p.w_off[i] = c.offs[i].w;
@@ -672,25 +784,32 @@ int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, cons
   p.nacc = split && g.ks > 1 ? 2 : 1;
   const uint32_t cols = split ? 2 * p.nacc * ((2 * p.np + 31) / 32 * 32) : 2 * p.np;
   p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+  p.ptab = p.posf;
   p.stages = 8;
   while (p.stages > 2 && conv_x3_smem(p).total > SMEM_LIMIT) --p.stages;
+  if (p.ptab && conv_x3_smem(p).total > SMEM_LIMIT) {  // no room for the table: edge path for every row
+    p.ptab = 0;
+    p.stages = 8;
+    while (p.stages > 2 && conv_x3_smem(p).total > SMEM_LIMIT) --p.stages;
+  }
   if (conv_x3_smem(p).total > SMEM_LIMIT || p.rbox > 256 || p.np > 64 || c.mode < 0 || c.mode > 2)
     return NRX_ERR_UNSUPPORTED;
   const size_t smem = conv_x3_smem(p).total;
   CUtensorMap m0, m1;
-  int rc = split ? make_map_plane(&m0, c.src0, g, c.c0, p.rbox) : make_map(&m0, c.src0, g, c.c0, p.rbox);
-  if (rc) return rc;
   const void* s1 = c.src1 ? c.src1 : c.src0;
   const int cc1 = c.c1 ? c.c1 : c.c0;
-  rc = split ? make_map_plane(&m1, s1, g, cc1, p.rbox) : make_map(&m1, s1, g, cc1, p.rbox);
+  const int box0 = c.posf ? p.kc : c.c0 / 8, box1 = c.posf ? p.kc : cc1 / 8;
+  int rc = split ? make_map_plane(&m0, c.src0, g, c.c0, p.rbox, box0) : make_map(&m0, c.src0, g, c.c0, p.rbox, box0);
+  if (rc) return rc;
+  rc = split ? make_map_plane(&m1, s1, g, cc1, p.rbox, box1) : make_map(&m1, s1, g, cc1, p.rbox, box1);
   if (rc) return rc;
   X3Fn fn = nullptr;
   switch (p.np) {
-    case 16: fn = select_conv_x3<16>(g, c.mode, c.c0, c.c1, c.prec); break;
-    case 32: fn = select_conv_x3<32>(g, c.mode, c.c0, c.c1, c.prec); break;
-    case 48: fn = select_conv_x3<48>(g, c.mode, c.c0, c.c1, c.prec); break;
-    case 56: fn = select_conv_x3<56>(g, c.mode, c.c0, c.c1, c.prec); break;
-    case 64: fn = select_conv_x3<64>(g, c.mode, c.c0, c.c1, c.prec); break;
+    case 16: fn = select_conv_x3<16>(g, c.mode, c.c0, c.c1, c.prec, c.posf); break;
+    case 32: fn = select_conv_x3<32>(g, c.mode, c.c0, c.c1, c.prec, c.posf); break;
+    case 48: fn = select_conv_x3<48>(g, c.mode, c.c0, c.c1, c.prec, c.posf); break;
+    case 56: fn = select_conv_x3<56>(g, c.mode, c.c0, c.c1, c.prec, c.posf); break;
+    case 64: fn = select_conv_x3<64>(g, c.mode, c.c0, c.c1, c.prec, c.posf); break;
     default: return NRX_ERR_UNSUPPORTED;
   }
   if (!fn) return NRX_ERR_UNSUPPORTED;
@@ -775,6 +894,7 @@ int launch_forward_x3(const Geom& g, const PackLayout& L, const WsLayout& W, int
     c.dst = h;
     c.cdst = g.Ch;
     c.mode = EPI_RELU;
+    c.posf = upd0_posf(g.d, g.ks, NRX_FP32X3);
     {
       ProfScope ps(KID_UPD0, st);
       NRX_TRY_X3(launch_conv_x3(g, c, wb, mod_order, st));

@@ -250,7 +250,7 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
             const int ch = c32 / 8 + c8;
             if constexpr (X3) {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) o[e] = fmaxf(__fadd_rn(__fmul_rn(v[8 * c8 + e], dsc), s.sb0[8 * ch + e]), 0.f);
+              for (int e = 0; e < 8; ++e) o[e] = relu_f(__fadd_rn(__fmul_rn(v[8 * c8 + e], dsc), s.sb0[8 * ch + e]));
               uint4 hi, lo;
               uint32_t bad = 0;
               split_chunk(o, hi, lo, bad);
@@ -259,7 +259,7 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
               *reinterpret_cast<uint4*>(H + ((size_t)(p.hp / 8 + ch) * NRX_TILE_M + r) * 16) = lo;
             } else {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) o[e] = fmaxf(v[8 * c8 + e] + s.sb0[c32 + 8 * c8 + e], 0.f);
+              for (int e = 0; e < 8; ++e) o[e] = relu_f(v[8 * c8 + e] + s.sb0[c32 + 8 * c8 + e]);
               store_chunk(reinterpret_cast<ET*>(H + ((size_t)ch * NRX_TILE_M + r) * 16), o);
             }
           }

@@ -74,6 +74,7 @@ extern "C" int nrx_forward(const nrx_model_desc* model, const nrx_slot_desc* slo
                            int n_pilot_sets, const float* noise_feat, const int32_t* mod_order,
                            const void* packed_weights, float* llr_out, int llr_width, void* chest_out,
                            void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxScope range("nrx_forward");
   Geom g;
   NRX_TRY(make_geom(model, slot, n_slots, precision, &g));
   if (num_iterations < 1 || num_iterations > model->num_iterations) return NRX_ERR_DEPTH;

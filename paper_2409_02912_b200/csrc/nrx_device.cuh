@@ -110,12 +110,15 @@ __device__ __forceinline__ uint4 pack_chunk(const float* v, const __half*) {
   return make_uint4(*reinterpret_cast<uint32_t*>(&h[0]), *reinterpret_cast<uint32_t*>(&h[1]),
                     *reinterpret_cast<uint32_t*>(&h[2]), *reinterpret_cast<uint32_t*>(&h[3]));
 }
-// max(x, 0) on a packed chunk (exact: rounding commutes with the clamp)
+// The reference's ReLU, np.maximum(x, 0) (autodiff.py:203-205): NaN propagates
+// (fmaxf would return 0 and hide a non-finite input from CHECK_FINITE).
+__device__ __forceinline__ float relu_f(float x) { return x < 0.f ? 0.f : x; }
+// max(x, 0) on a packed chunk (exact: rounding commutes with the clamp; NaN propagates)
 __device__ __forceinline__ uint4 relu_chunk(uint4 q, const __half*) {
   uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    __half2 h = __hmax2(*reinterpret_cast<__half2*>(&w[i]), __float2half2_rn(0.f));
+    __half2 h = __hmax2_nan(*reinterpret_cast<__half2*>(&w[i]), __float2half2_rn(0.f));
     w[i] = *reinterpret_cast<uint32_t*>(&h);
   }
   return make_uint4(w[0], w[1], w[2], w[3]);
@@ -124,7 +127,7 @@ __device__ __forceinline__ uint4 relu_chunk(uint4 q, const __nv_bfloat16*) {
   uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    __nv_bfloat162 h = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&w[i]), __float2bfloat162_rn(0.f));
+    __nv_bfloat162 h = __hmax2_nan(*reinterpret_cast<__nv_bfloat162*>(&w[i]), __float2bfloat162_rn(0.f));
     w[i] = *reinterpret_cast<uint32_t*>(&h);
   }
   return make_uint4(w[0], w[1], w[2], w[3]);
@@ -178,8 +181,8 @@ __device__ __forceinline__ void split_chunk(const float* v, uint4& hi, uint4& lo
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 // split_chunk that also records a range violation: |v| > 65504 (the fp16
-// maximum), inf or NaN.  A NaN from an overflowed plane would otherwise be
-// swallowed by the next ReLU (fmaxf), so every split checks.
+// maximum), inf or NaN, at every split (the earliest point an overflowed
+// plane can be seen).
 __device__ __forceinline__ void split_chunk(const float* v, uint4& hi, uint4& lo, uint32_t& bad) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) bad |= (__float_as_uint(v[i]) & 0x7fffffffu) > 0x477fe000u;

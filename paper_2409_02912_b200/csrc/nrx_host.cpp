@@ -181,10 +181,10 @@ void pack_layout(const nrx_model_desc* m, int prec, PackLayout* L) {
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
   if (prec == NRX_FP32X3) {  // fp16 hi/lo operand pairs, CTA-pair convolutions
     const int npx = x3_np(m->d_s), np = rup(m->d_s, 16), hp = rup(m->hidden, 16);
-    auto conv = [&](ConvOff& c, int ktap) {
+    auto conv = [&](ConvOff& c, int ktap, bool posf = false) {
       c.ktap = ktap;
       c.w = take((size_t)taps * ktap * npx * 2 * 2);  // [rank 0: W_hi | rank 1: W_lo][K/8][npx][8]
-      c.b = take((size_t)(npx + 4) * 4);              // bias, then the descale 2^-E
+      c.b = take((size_t)(posw_off(npx) + (posf ? 2 * taps * npx : 0)) * 4);  // bias, descale 2^-E, pos weights
     };
     auto mlp = [&](MlpOff& o, int k0, int n0, int n1) {
       o.out = n1;
@@ -199,7 +199,8 @@ void pack_layout(const nrx_model_desc* m, int prec, PackLayout* L) {
       mlp(L->llr[i], g.Cs, 2 * hp, 32);
     }
     mlp(L->msg, g.Cs, hp, np);
-    conv(L->upd0, g.Cs + g.Ca);
+    const bool posf = upd0_posf(m->d_s, m->kernel_size, NRX_FP32X3);
+    conv(L->upd0, posf ? 2 * m->d_s : g.Cs + g.Ca, posf);
     conv(L->upd1, g.Ch);
     L->total = off;
     return;
@@ -273,6 +274,19 @@ int map_update(int j, const Geom& g) {
   if (j < g.Cs) return -1;
   int a = j - g.Cs;
   return a < g.d ? g.d + a : -1;
+}
+// update conv0 with the positional channels folded out (upd0_posf): [state (d) | agg (d)]
+int map_update_posf(int j, const Geom& g) { return j < 2 * g.d ? j : -1; }
+
+// fp32 weights of the two positional input channels (reference Cin 2d, 2d+1)
+// as [channel][tap][np] after the bias block (posw_off)
+void pack_posw(const Geom& g, int k, const ConvOff& c, int np, const float* w, uint8_t* base) {
+  const int taps = k * k, cout = g.d, cin_ref = 2 * g.d + 2;
+  float* pw = (float*)(base + c.b) + posw_off(np);
+  for (int p = 0; p < 2; ++p)
+    for (int tap = 0; tap < taps; ++tap)
+      for (int o = 0; o < np; ++o)
+        pw[((size_t)p * taps + tap) * np + o] = o < cout ? w[((size_t)tap * cin_ref + 2 * g.d + p) * cout + o] : 0.f;
 }
 
 void pack_conv_f32(const Geom& g, int k, const ConvOff& c, int cdst, int cin_ref, const float* w,
@@ -493,7 +507,12 @@ int pack_weights_x3(const nrx_model_desc* m, const float* const* t, uint8_t* bas
     }
     pb1[np] = std::ldexp(1.f, -E1);
   }
-  pack_conv_x3(g, k, L.upd0, 2 * d + 2, t[i_upd], t[i_upd + 1], map_update, base);
+  if (upd0_posf(d, k, NRX_FP32X3)) {
+    pack_conv_x3(g, k, L.upd0, 2 * d + 2, t[i_upd], t[i_upd + 1], map_update_posf, base);
+    pack_posw(g, k, L.upd0, x3_np(d), t[i_upd], base);
+  } else {
+    pack_conv_x3(g, k, L.upd0, 2 * d + 2, t[i_upd], t[i_upd + 1], map_update, base);
+  }
   pack_conv_x3(g, k, L.upd1, d, t[i_upd + 2], t[i_upd + 3], map_identity_hidden, base);
   return NRX_OK;
 }

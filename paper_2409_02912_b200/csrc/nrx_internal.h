@@ -19,6 +19,7 @@
 #pragma once
 #include <stddef.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/nrx_b200.h"
 
@@ -34,6 +35,27 @@ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // 56 for d in (48, 56] (the RT model: N = 112 instead of 128 skips 12.5 % of
 // the tensor work).
 inline int x3_np(int d) { return (d + 7) / 8 * 8 == 56 ? 56 : rup(d, 16); }
+// iteration.update.conv0 with the two positional channels taken out of the
+// GEMM (K = 2 d instead of rup(d + 2, 16) + rup(d, 16): 112 instead of 128
+// for d = 56, 32 instead of 48 for d = 16); the epilogue adds their
+// contribution from 18 x np fp32 weights stored after the bias (POSW_OFF).
+// On for the fp32x3 layer where an unrolled instance exists (d = 16, 56):
+// update.conv0 0.975 -> 0.887 ms per 32 C2 slots.  The bf16 / fp16 pair copy
+// keeps K = 128: there the shared 2-source stage and the table lookups cost
+// more than the 12.5 % of MMAs they save (0.341 -> 0.357 ms).
+inline bool posf_enabled() {  // NRX_POSF=0: keep the positional channels in K (A/B experiments)
+  static const bool on = [] {
+    const char* e = std::getenv("NRX_POSF");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+inline bool upd0_posf(int d, int ks, int prec) {
+  if (ks != 3 || d % 8 || !posf_enabled()) return false;
+  return prec == NRX_FP32X3 && (d == 56 || d == 16);
+}
+// float offset of the positional weights [channel dt, df][tap][np] in a conv bias block
+inline int posw_off(int np) { return np + 4; }
 
 // Geometry + channel bookkeeping, passed by value to kernels.
 struct Geom {

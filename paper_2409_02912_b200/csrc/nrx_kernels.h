@@ -35,6 +35,7 @@ struct ConvX3Launch {
   int cdst;
   int mode;
   int prec = NRX_FP32X3;
+  bool posf = false;  // update.conv0 with the positional channels folded out of K (upd0_posf)
 };
 int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, const int32_t* mod_order,
                    cudaStream_t st);

@@ -1,4 +1,8 @@
-// Optional per-launch CUDA-event timing (nrx_profile_* in include/nrx_b200.h).
+// Optional per-launch CUDA-event timing (nrx_profile_* in include/nrx_b200.h),
+// and NVTX ranges (domain "nrx", one per layer launch) that Nsight tools show
+// on the host timeline; without an attached tool an NVTX push is a no-op call.
+#include <nvtx3/nvToolsExt.h>
+
 #include <mutex>
 #include <vector>
 
@@ -17,9 +21,30 @@ uint32_t g_mask = 0;
 std::vector<cudaEvent_t> g_pool;
 std::vector<Record> g_recs;
 size_t g_next = 0;
+
+const char* const kNames[] = {"ls_feat", "state_init.conv0", "state_init.conv1", "msg", "update.conv0",
+                              "update.conv1", "readout"};
+
+nvtxDomainHandle_t domain() {
+  static nvtxDomainHandle_t d = nvtxDomainCreateA("nrx");
+  return d;
+}
+
+void range_push(const char* name) {
+  nvtxEventAttributes_t a = {};
+  a.version = NVTX_VERSION;
+  a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+  a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+  a.message.ascii = name;
+  nvtxDomainRangePushEx(domain(), &a);
+}
 }  // namespace
 
+NvtxScope::NvtxScope(const char* name) { range_push(name); }
+NvtxScope::~NvtxScope() { nvtxDomainRangePop(domain()); }
+
 ProfScope::ProfScope(int kid, cudaStream_t st) : kid_(kid), st_(st), rec_(-1) {
+  range_push(kid >= 0 && kid < 7 ? kNames[kid] : "kernel");
   if (!g_on) return;  // racy read is fine: enable/disable are not concurrent with forwards
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_on || !(g_mask >> kid & 1u) || g_next + 2 > g_pool.size()) return;
@@ -31,6 +56,7 @@ ProfScope::ProfScope(int kid, cudaStream_t st) : kid_(kid), st_(st), rec_(-1) {
 }
 
 ProfScope::~ProfScope() {
+  nvtxDomainRangePop(domain());
   if (rec_ < 0) return;
   std::lock_guard<std::mutex> lk(g_mu);
   cudaEventRecord(g_recs[rec_].b, st_);

@@ -22,4 +22,13 @@ class ProfScope {
   int rec_;
 };
 
+// NVTX range (domain "nrx") around a host-side scope, e.g. one nrx_forward call.
+class NvtxScope {
+ public:
+  explicit NvtxScope(const char* name);
+  ~NvtxScope();
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
+
 }  // namespace nrx

@@ -350,13 +350,13 @@ inline EncodeTiledFn encode_fn() {
 // requests instead of 16-byte ones.  Box {128, rbox/16, C/8, 1} lands as the
 // K-major no-swizzle [C/8][rbox][8] tile; the row coordinate is in units of
 // 16 rows (tiles start on 16-row boundaries, zero fill outside the slab).
-inline int make_map(CUtensorMap* m, const void* base, const Geom& g, int C, int rbox) {
+inline int make_map(CUtensorMap* m, const void* base, const Geom& g, int C, int rbox, int box_chunks = 0) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return NRX_ERR_NO_DEVICE;
   if (rbox % 16 || g.rows_slab % 16) return NRX_ERR_UNSUPPORTED;
   const cuuint64_t dims[4] = {128, (cuuint64_t)(g.rows_slab / 16), (cuuint64_t)(C / 8), (cuuint64_t)g.NU};
   const cuuint64_t strides[3] = {256, (cuuint64_t)g.rows_slab * 16, (cuuint64_t)(C / 8) * g.rows_slab * 16};
-  const cuuint32_t box[4] = {128, (cuuint32_t)(rbox / 16), (cuuint32_t)(C / 8), 1};
+  const cuuint32_t box[4] = {128, (cuuint32_t)(rbox / 16), (cuuint32_t)(box_chunks ? box_chunks : C / 8), 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,

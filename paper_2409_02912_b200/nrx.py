@@ -15,6 +15,8 @@ evaluation.py:24,144-154,343-347).
 
 from __future__ import annotations
 
+import os
+import sys
 import threading
 import warnings
 import zlib
@@ -23,6 +25,13 @@ import numpy as np
 
 from .config import weight_array
 from .engine import NrxEngine, pilot_comb_values
+
+# Mirror of the reference's debug switch autodiff.CHECK_FINITE
+# (autodiff.py:27-29,130-131): when set, a forward whose outputs are not all
+# finite raises FloatingPointError instead of returning them.  Settable here,
+# by NRX_CHECK_FINITE=1, per call (check_finite=True), or through install(),
+# which follows the reference package's own autodiff.CHECK_FINITE.
+CHECK_FINITE = os.environ.get("NRX_CHECK_FINITE", "0") == "1"
 
 _CACHE_LOCK = threading.Lock()
 _ENGINES: dict = {}
@@ -142,16 +151,17 @@ def noise_features(n0, n: int) -> np.ndarray:
 
 def nrx_forward(y, books, cfg, mcs_per_ue, w, config, n0, num_iterations=None, apply_mask=True, *,
                 precision: str = "fp32", device=None, exact_inputs: bool = False,
-                check_weights: bool = True):
+                check_weights: bool = True, check_finite: bool | None = None):
     """Full receiver pass on received grids, computed on the GPU.
 
     Same contract as the reference: y (N,S,T,B) or (S,T,B) complex; books a
     PilotBook or one per sample; mcs_per_ue per-UE McsEntry; returns (llrs,
     chest) with llrs a per-UE list of (N,S,T,m_u) float32 (label-prefix
     masked for single/masking) and chest (N,U,S,T,B) complex64, squeezed for
-    3-D y.  Extra keyword-only knobs: precision "fp32" (parity mode) or
-    "bf16" (tensor cores); exact_inputs ships complex128 inputs instead of
-    complex64.
+    3-D y.  Extra keyword-only knobs: precision "fp32" (reference accuracy on
+    the tensor cores, default), "fp32_simt" (fp32 FFMA), "bf16" or "fp16";
+    exact_inputs ships complex128 inputs instead of complex64; check_finite
+    (default: CHECK_FINITE) raises FloatingPointError on non-finite outputs.
     """
     n_it = validate_call(mcs_per_ue, config, num_iterations)
     y = np.asarray(y)
@@ -186,6 +196,9 @@ def nrx_forward(y, books, cfg, mcs_per_ue, w, config, n0, num_iterations=None, a
                       "recomputing this call with precision='fp32_simt'", RuntimeWarning, stacklevel=2)
         eng = get_engine(w, config, "fp32_simt", device, check_weights)
         llr_full, chest = eng.run_arrays(*args)
+    if (CHECK_FINITE if check_finite is None else check_finite) and not (
+            np.isfinite(llr_full).all() and np.isfinite(chest.view(np.float32)).all()):
+        raise FloatingPointError("non-finite values produced by a forward op")
     llrs = []
     for u in range(U):
         grid = llr_full[:, u, ..., :width[u]]
@@ -201,9 +214,12 @@ def install(module, **kwargs):
     """Point ``module.nrx_forward`` at the GPU implementation (keeping the
     reference signature); returns the previous function for restoring."""
     previous = module.nrx_forward
+    autodiff = sys.modules.get(module.__name__.rpartition(".")[0] + ".autodiff")
 
     def _gpu_nrx_forward(*args, **kw):
         kw = {**kwargs, **kw}
+        if getattr(autodiff, "CHECK_FINITE", False):
+            kw.setdefault("check_finite", True)
         return nrx_forward(*args, **kw)
 
     module.nrx_forward = _gpu_nrx_forward

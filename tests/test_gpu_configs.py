@@ -94,3 +94,26 @@ def test_c4_large_model_and_depth_control(precision):
     for depth in (8, 3):
         got, ref, chest, ref_chest = _run(cfg, config, w, (t[14], t[14]), 1, 9, precision, num_iterations=depth)
         check_llrs(got, ref, precision, f"C4 depth {depth}", depth=depth)
+
+
+@pytest.mark.parametrize("d,comb,S,U,T,pilots,freq", [
+    (56, 4, 24, 3, 14, (2, 11), True),   # comb 4, three UE offsets, few interior rows
+    (16, 2, 10, 2, 14, (2, 11), True),
+    (16, 4, 8, 2, 7, (3,), True),        # no interior row at all, T = 7, one pilot symbol
+    (56, 1, 12, 1, 14, (2, 11), True),   # comb 1
+    (56, 2, 48, 2, 14, (0, 13), False),  # no frequency encoding, pilots on the edge symbols
+])
+def test_fp32x3_positional_fold_edges(d, comb, S, U, T, pilots, freq):
+    """update.conv0 of the fp32 mode takes the positional channels out of the
+    GEMM (upd0_posf): a per-(comb residue, symbol) table for interior rows and
+    the 18-term sum at the band edges and pad rows.  Against the float64
+    oracle at the fp32 gate over comb sizes, UE comb offsets, tiny grids and
+    the frequency-encoding flag."""
+    from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights
+    t = default_mcs_table()
+    cfg = SlotConfig(num_subcarriers=S, num_symbols=T, pilot_symbols=pilots, num_ues=U, comb_size=comb)
+    config = NrxConfig.from_table(t, (14,), d_s=d, num_iterations=2, include_freq_encoding=freq)
+    w = orc.perturb_biases(init_weights(config, 9))
+    got, ref, chest, ref_chest = _run(cfg, config, w, tuple(t[14] for _ in range(U)), 2, 11, "fp32")
+    check_llrs(got, ref, "fp32", f"posf d={d} comb={comb} S={S}")
+    check_chest(chest, ref_chest, "fp32")

@@ -98,7 +98,7 @@ def test_receiver_bank_nrx_on_gpu_matches_cpu(ref):
         assert np.abs(g.astype(np.float64) - c).max() <= 1e-5 * scale
 
 
-def test_latency_bench_returns_report(ref, installed):
+def test_latency_bench_returns_report(ref, installed, tmp_path):
     from nrxsim import evaluation as ev
     from nrxsim.nrx import init_weights
     from nrxsim.nrx import NrxConfig
@@ -109,6 +109,44 @@ def test_latency_bench_returns_report(ref, installed):
     rep = ev.latency_bench((config, init_weights(config, seed=0)), cfg, table, depths=(1, 2, 4), runs=5, warmup=2)
     assert isinstance(rep, ev.LatencyReport)
     assert set(rep.median_s) == {1, 2, 4} and all(0 < v < 0.05 for v in rep.median_s.values())
+    path = tmp_path / "latency.csv"
+    ev.write_latency_csv(rep, path)  # the reference's latency CSV schema (evaluation.py:404-410)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "n_it,median_s,p10_s,p90_s" and [int(x.split(",")[0]) for x in lines[1:4]] == [1, 2, 4]
+    assert lines[4].startswith("# fit a=")
+
+
+def test_check_finite_follows_reference_switch(ref):
+    """autodiff.CHECK_FINITE (autodiff.py:27-29,130-131) makes the reference
+    raise FloatingPointError on a non-finite forward; with install() applied
+    the GPU drop-in follows the same switch, and stays silent without it."""
+    from nrxsim import autodiff, evaluation as ev
+    from nrxsim.nrx import checkpoint_load
+    from nrxsim.slot import SlotConfig
+    from paper_2409_02912_b200 import nrx as gnrx
+    table = _table(ref)
+    cfg = SlotConfig(num_subcarriers=48)
+    config, w = checkpoint_load(CKPT)
+    ecfg = ev.EvalConfig(snr_grid_db=(8.0,), receivers=("nrx",), mcs_indices=(14, 14), seed=3)
+    bank = ev.ReceiverBank(ecfg, cfg, table, nrx_model=(config, w))
+    y, books, h_eff, n0 = _chunk(ref, cfg, bank.entries, 2)
+    y[1, 5, 3, 0] = np.nan
+    prev_flag = autodiff.CHECK_FINITE
+    autodiff.CHECK_FINITE = True
+    try:
+        with pytest.raises(FloatingPointError):
+            bank.run("nrx", y, books, h_eff, n0)       # the reference on the CPU
+        prev = gnrx.install(ev)
+        try:
+            with pytest.raises(FloatingPointError, match="non-finite"):
+                bank.run("nrx", y, books, h_eff, n0)   # the drop-in
+            autodiff.CHECK_FINITE = False
+            out = bank.run("nrx", y, books, h_eff, n0)
+            assert not all(np.isfinite(o).all() for o in out)
+        finally:
+            ev.nrx_forward = prev
+    finally:
+        autodiff.CHECK_FINITE = prev_flag
 
 
 def test_evaluate_tbler_workers_and_cpu(ref):
