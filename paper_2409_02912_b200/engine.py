@@ -29,6 +29,20 @@ from .config import weight_array
 _TORCH = None
 
 
+def _stage(torch, dst, arr):
+    """Write a numpy array into a pinned staging tensor, converting the dtype
+    (complex128 -> complex64, round to nearest as numpy).  torch's copy runs
+    on all host threads (C2 y: 0.02 ms instead of 0.2 ms for np.copyto);
+    arrays torch cannot wrap (read-only, negative strides) go through numpy."""
+    if arr.flags.writeable and all(st >= 0 for st in arr.strides):
+        try:
+            dst.copy_(torch.from_numpy(arr))
+            return
+        except (TypeError, ValueError, RuntimeError):
+            pass
+    np.copyto(dst.numpy(), arr, casting="same_kind")
+
+
 def _require_cuda():
     global _TORCH
     if _TORCH is None:
@@ -298,9 +312,9 @@ class NrxEngine:
         tls = self._local()
         with torch.cuda.stream(tls.stream):
             h_y = self._staging("y", y.shape, cdt, True)
-            np.copyto(h_y.numpy(), y, casting="same_kind")
+            _stage(torch, h_y, y)
             h_p = self._staging("p", pilot_vals.shape, cdt, True)
-            np.copyto(h_p.numpy(), pilot_vals, casting="same_kind")
+            _stage(torch, h_p, pilot_vals)
             h_n = self._staging("n", (n,), torch.float32, True)
             h_n.numpy()[...] = noise_feat
             h_m = self._staging("m", (n * U,), torch.int32, True)
