@@ -219,7 +219,13 @@ __host__ __device__ inline ConvX3Smem conv_x3_smem(const ConvX3Params& p) {
 // holds <= 3 warps and the fully unrolled MMA issue gets up to 168 registers);
 // the residual update, whose epilogue also reads the previous state and is
 // the bottleneck of that layer, runs twice the warps (16 columns each).
-__host__ __device__ constexpr int x3_epi_cols(int mode) { return mode == EPI_RESIDUAL ? 16 : 32; }
+// Layers with at most two K=16 steps per tap (state_init.conv0: 19 -> 32
+// feature channels) issue few MMAs per tile, so their epilogue is the long
+// pole: 16 columns per thread (twice the warps) there too.
+__host__ __device__ constexpr int x3_epi_cols(int mode, bool small_k = false) {
+  return mode == EPI_RESIDUAL || small_k ? 16 : 32;
+}
+__host__ __device__ constexpr bool x3_small_k(int ks, int nk0, int nk1) { return ks > 0 && nk0 + nk1 <= 2; }
 
 // PREC = NRX_FP32X3: the split-operand kernel described above.  PREC =
 // NRX_FP16 / NRX_BF16: the same CTA-pair pipeline for one half-precision plane
@@ -240,7 +246,9 @@ __host__ __device__ constexpr int x3_epi_cols(int mode) { return mode == EPI_RES
 // fp32, before griddepcontrol.wait) and the epilogue adds one table row; edge
 // rows evaluate the 18 terms.
 template <int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0, int PREC = NRX_FP32X3, bool POSF = false>
-__global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_epi_cols(MODE)), 1)
+__global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k(KS, NK0, NK1)) - 1) /
+                                              x3_epi_cols(MODE, x3_small_k(KS, NK0, NK1))),
+                                  1)
     k_conv_x3(const __grid_constant__ ConvX3Params p, const __grid_constant__ CUtensorMap map0,
               const __grid_constant__ CUtensorMap map1) {
   constexpr bool SPLIT = PREC == NRX_FP32X3;
@@ -254,7 +262,7 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_
   // 32 accumulator columns per epilogue thread: 2 + 4 * NP/32 warps (10 for
   // NP = 64) leave each SM sub-partition <= 3 warps, i.e. up to 168 registers
   // for the fully unrolled MMA issue (18 warps would cap it at 96 and spill)
-  constexpr int NC = x3_epi_cols(MODE);  // accumulator columns per epilogue thread
+  constexpr int NC = x3_epi_cols(MODE, x3_small_k(KS, NK0, NK1));  // accumulator columns per epilogue thread
   constexpr int PARTS = (NP + NC - 1) / NC;  // NP = 56: the last part's columns past NP are ignored
   constexpr int EPI_WARPS = 4 * PARTS;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -696,18 +704,24 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE) - 1) / x3_
 using X3Fn = void (*)(const ConvX3Params, const CUtensorMap, const CUtensorMap);
 
 template <int NP>
-static X3Fn select_conv_x3(const Geom& g, int mode, int c0, int c1, int prec, bool posf) {
+static X3Fn select_conv_x3(const Geom& g, int mode, int c0, int c1, int prec, bool posf, bool* small) {
+  *small = false;
   if (posf) {  // update.conv0 without the positional channels in K (upd0_posf)
     if constexpr (NP == 56) return g.d == 56 ? k_conv_x3<56, EPI_RELU, 3, 7, 0, NRX_FP32X3, true> : nullptr;
-    if constexpr (NP == 16) return g.d == 16 ? k_conv_x3<16, EPI_RELU, 3, 2, 0, NRX_FP32X3, true> : nullptr;
+    if constexpr (NP == 16) {
+      *small = true;
+      return g.d == 16 ? k_conv_x3<16, EPI_RELU, 3, 2, 0, NRX_FP32X3, true> : nullptr;
+    }
     return nullptr;
   }
   if (prec != NRX_FP32X3) {  // half-precision pair kernels: ReLU layers only, np 32 / 64
     if constexpr (NP == 32 || NP == 64) {
       const bool f16 = prec == NRX_FP16;
       if (mode != EPI_RELU) return nullptr;
-      if (NP == 64 && g.ks == 3 && c0 == 32 && c1 == 0)
+      if (NP == 64 && g.ks == 3 && c0 == 32 && c1 == 0) {
+        *small = true;
         return f16 ? k_conv_x3<64, EPI_RELU, 3, 2, 0, NRX_FP16> : k_conv_x3<64, EPI_RELU, 3, 2, 0, NRX_BF16>;
+      }
       if (NP == 64 && g.ks == 3 && c0 == 64 && c1 == 64)
         return f16 ? k_conv_x3<64, EPI_RELU, 3, 4, 4, NRX_FP16> : k_conv_x3<64, EPI_RELU, 3, 4, 4, NRX_BF16>;
       return f16 ? k_conv_x3<NP, EPI_RELU, 0, 0, 0, NRX_FP16> : k_conv_x3<NP, EPI_RELU, 0, 0, 0, NRX_BF16>;
@@ -718,14 +732,14 @@ static X3Fn select_conv_x3(const Geom& g, int mode, int c0, int c1, int prec, bo
   X3Fn fn = generic[mode];
   if (NP == 16 && g.ks == 3) {  // the desk models (d_s = 16): features 32, state 32, h / messages 16 channels
     const int nk0 = c0 / 16, nk1 = c1 / 16;
-    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_x3<16, EPI_RELU, 3, 2, 0>;
+    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_x3<16, EPI_RELU, 3, 2, 0>, *small = true;
     if (mode == EPI_RELU && nk0 == 2 && nk1 == 1) fn = k_conv_x3<16, EPI_RELU, 3, 2, 1>;
-    if (mode == EPI_STATE_INIT && nk0 == 1 && nk1 == 0) fn = k_conv_x3<16, EPI_STATE_INIT, 3, 1, 0>;
-    if (mode == EPI_RESIDUAL && nk0 == 1 && nk1 == 0) fn = k_conv_x3<16, EPI_RESIDUAL, 3, 1, 0>;
+    if (mode == EPI_STATE_INIT && nk0 == 1 && nk1 == 0) fn = k_conv_x3<16, EPI_STATE_INIT, 3, 1, 0>, *small = true;
+    if (mode == EPI_RESIDUAL && nk0 == 1 && nk1 == 0) fn = k_conv_x3<16, EPI_RESIDUAL, 3, 1, 0>, *small = true;
   }
   if (NP == 56 && g.ks == 3) {  // fully unrolled issue for the RT / large models' 3x3 layers
     const int nk0 = c0 / 16, nk1 = c1 / 16;
-    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_x3<56, EPI_RELU, 3, 2, 0>;
+    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_x3<56, EPI_RELU, 3, 2, 0>, *small = true;
     if (mode == EPI_RELU && nk0 == 4 && nk1 == 4) fn = k_conv_x3<56, EPI_RELU, 3, 4, 4>;
     if (mode == EPI_STATE_INIT && nk0 == 4 && nk1 == 0) fn = k_conv_x3<56, EPI_STATE_INIT, 3, 4, 0>;
     if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0) fn = k_conv_x3<56, EPI_RESIDUAL, 3, 4, 0>;
@@ -804,12 +818,13 @@ int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, cons
   rc = split ? make_map_plane(&m1, s1, g, cc1, p.rbox, box1) : make_map(&m1, s1, g, cc1, p.rbox, box1);
   if (rc) return rc;
   X3Fn fn = nullptr;
+  bool small = false;  // the selected instance drains 16 columns per epilogue thread (x3_small_k)
   switch (p.np) {
-    case 16: fn = select_conv_x3<16>(g, c.mode, c.c0, c.c1, c.prec, c.posf); break;
-    case 32: fn = select_conv_x3<32>(g, c.mode, c.c0, c.c1, c.prec, c.posf); break;
-    case 48: fn = select_conv_x3<48>(g, c.mode, c.c0, c.c1, c.prec, c.posf); break;
-    case 56: fn = select_conv_x3<56>(g, c.mode, c.c0, c.c1, c.prec, c.posf); break;
-    case 64: fn = select_conv_x3<64>(g, c.mode, c.c0, c.c1, c.prec, c.posf); break;
+    case 16: fn = select_conv_x3<16>(g, c.mode, c.c0, c.c1, c.prec, c.posf, &small); break;
+    case 32: fn = select_conv_x3<32>(g, c.mode, c.c0, c.c1, c.prec, c.posf, &small); break;
+    case 48: fn = select_conv_x3<48>(g, c.mode, c.c0, c.c1, c.prec, c.posf, &small); break;
+    case 56: fn = select_conv_x3<56>(g, c.mode, c.c0, c.c1, c.prec, c.posf, &small); break;
+    case 64: fn = select_conv_x3<64>(g, c.mode, c.c0, c.c1, c.prec, c.posf, &small); break;
     default: return NRX_ERR_UNSUPPORTED;
   }
   if (!fn) return NRX_ERR_UNSUPPORTED;
@@ -819,7 +834,8 @@ int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, cons
   const int pairs = (total + 1) / 2 < pairs_max ? (total + 1) / 2 : pairs_max;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs, p.n_io);
-  cfg.blockDim = dim3(64 + 128 * ((p.np + x3_epi_cols(c.mode) - 1) / x3_epi_cols(c.mode)));
+  const int nc = x3_epi_cols(c.mode, small);
+  cfg.blockDim = dim3(64 + 128 * ((p.np + nc - 1) / nc));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];

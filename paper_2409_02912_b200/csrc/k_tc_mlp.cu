@@ -27,7 +27,7 @@ namespace tc {
 // warps: 0 producer, 1 MMA, HW hidden-epilogue warps, OW output-epilogue warps
 // (OW / 4 groups per TMEM lane quarter, each draining a share of the columns)
 constexpr int mlp_threads(int hw, int ow = 4) { return 64 + 32 * hw + 32 * ow; }
-constexpr int MSG_HW = 4, READOUT_HW = 8;
+constexpr int MSG_HW = 4, READOUT_HW = 8;  // (fp32x3 message kernel with 8 hidden warps: 0.36 -> 0.42 ms, spills)
 constexpr int MSG_OW = 8;  // the message epilogue (2 UEs x 64 columns, split planes) is the long pole
 constexpr int MSG_MAXU = 4;  // UEs per slot on the tensor-core path
 constexpr int A_STAGES = 4;  // maximum; fp32x3 uses fewer (p.astages)
@@ -78,6 +78,7 @@ struct MlpSmem {
 __device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int io, int hidden_threads,
                                           int output_threads = 128) {
   const int warp = threadIdx.x >> 5;
+  pdl_launch_dependents();  // launched with programmatic serialization: the next layer's prologue may start
   if (warp == 0) tmem_alloc(s.tmem_ptr, p.tmem_cols);
   if (threadIdx.x == 32) {
     for (int i = 0; i < p.astages; ++i) {
@@ -124,6 +125,7 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
       mbar_expect_tx(s.wbar, p.w0bytes + p.w1bytes);
       bulk_load(s.W0, p.wbase + p.w0[io], p.w0bytes, s.wbar);
       bulk_load(s.W1, p.wbase + p.w1[io], p.w1bytes, s.wbar);
+      pdl_wait();  // the state tiles: written by the previous layer
       WorkIter w(g, p.units, g.tiles, p.n_io, p.mod_order);
       int unit, tile, st = 0;
       uint32_t ph = 0;
@@ -498,7 +500,9 @@ int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const void
   const int total = g.N * g.tiles;
   const int per_sm = (512 / p.tmem_cols) < 2 || 2 * smem > SMEM_LIMIT ? 1 : 2;
   const int cap = num_sms() * per_sm;
-  fn<<<total < cap ? total : cap, mlp_threads(MSG_HW, MSG_OW), smem, st>>>(p, m);
+  if (launch_pdl(fn, dim3(total < cap ? total : cap), dim3(mlp_threads(MSG_HW, MSG_OW)), smem, st, p, m) !=
+      cudaSuccess)
+    return NRX_ERR_CUDA;
   return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
 }
 
@@ -530,7 +534,7 @@ int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const 
   const int per_sm = (512 / p.tmem_cols) < 2 || 2 * smem > SMEM_LIMIT ? 1 : 2;
   const int cap = num_sms() * per_sm;
   dim3 grid(total < cap ? total : cap, g.n_io);
-  fn<<<grid, mlp_threads(READOUT_HW), smem, st>>>(p, m);
+  if (launch_pdl(fn, grid, dim3(mlp_threads(READOUT_HW)), smem, st, p, m) != cudaSuccess) return NRX_ERR_CUDA;
   return cudaPeekAtLastError() == cudaSuccess ? NRX_OK : NRX_ERR_CUDA;
 }
 

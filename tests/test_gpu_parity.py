@@ -243,7 +243,8 @@ def test_concurrent_threads_deterministic():
 
 
 def test_pdl_launch_bit_identical_to_stream_order(tmp_path):
-    """The tensor-core layers are launched with programmatic dependent launch
+    """The tensor-core layers (convolutions and the message / readout MLP
+    kernels) are launched with programmatic dependent launch
     (each layer's prologue overlaps its predecessor; every activation access
     waits for the predecessor grid).  The results must be bit-identical to
     plain stream order (NRX_PDL=0, read once per process: run in a child)."""
@@ -265,9 +266,14 @@ def test_pdl_launch_bit_identical_to_stream_order(tmp_path):
         "w = {k: v + (0.05 * rng.standard_normal(v.shape).astype(np.float32) if v.ndim == 1 else 0) for k, v in w.items()}\n"
         "y, books, _ = synth_slots(cfg, [4, 4], 3, 0.1, seed=4)\n"
         "out = {}\n"
-        "for p in ('fp16', 'bf16'):\n"
+        "for p in ('fp32', 'fp16', 'bf16'):\n"
         "    llrs, chest = nrx_forward(y, books, cfg, (t[14], t[14]), w, config, 0.1, precision=p)\n"
         "    out[p + '_l0'], out[p + '_l1'], out[p + '_c'] = llrs[0], llrs[1], chest\n"
+        "cfg1 = SlotConfig(num_subcarriers=288, num_ues=1, comb_size=2)\n"  # standalone message / readout kernels
+        "y1, books1, _ = synth_slots(cfg1, [4], 3, 0.1, seed=6)\n"
+        "for p in ('fp32', 'fp16'):\n"
+        "    llrs, chest = nrx_forward(y1, books1, cfg1, (t[14],), w, config, 0.1, precision=p)\n"
+        "    out[p + '_u1_l0'], out[p + '_u1_c'] = llrs[0], chest\n"
         "np.savez(sys.argv[1], **out)\n")
     res = {}
     for pdl in ("1", "0"):
