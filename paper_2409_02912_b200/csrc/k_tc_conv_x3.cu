@@ -646,8 +646,8 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           // conv (exact 2^-E; + the folded positional terms) + bias, as the reference
-          float y = __fadd_rn(POSF ? __fadd_rn(__fmul_rn(v[8 * c8 + e], descale), pz[e]) : __fmul_rn(v[8 * c8 + e], descale),
-                              bb[e]);
+          // (v 2^-E is exact, so the fma rounds once exactly like the separate multiply and add)
+          float y = POSF ? __fadd_rn(fmaf(v[8 * c8 + e], descale, pz[e]), bb[e]) : fmaf(v[8 * c8 + e], descale, bb[e]);
           if (MODE == EPI_RELU) y = relu_f(y);
           if (MODE == EPI_RESIDUAL) y = old[8 * c8 + e] + y;
           x[e] = (valid && (full || 8 * cc + e < g.d)) ? y : 0.f;

@@ -18,7 +18,8 @@
 // "use" j enumerates the (work item, UE) pairs a CTA processes.
 // X3 (NRX_FP32X3): state tiles, hidden layers and weights carry fp16 hi + lo
 // planes; every GEMM is mma_x3_gemm (lo*Whi, then hi*Whi folded by
-// scale-input-d, hi*Wlo) and the epilogues apply the packer's 2^-E descale.
+// scale-input-d, hi*Wlo) and the epilogues apply the packer's 2^-E descale
+// (fmaf(acc, 2^-E, bias): the product is exact, so one rounding as acc 2^-E + bias).
 #include "tc_common.cuh"
 
 namespace nrx {
@@ -252,7 +253,7 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
             const int ch = c32 / 8 + c8;
             if constexpr (X3) {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) o[e] = relu_f(__fadd_rn(__fmul_rn(v[8 * c8 + e], dsc), s.sb0[8 * ch + e]));
+              for (int e = 0; e < 8; ++e) o[e] = relu_f(fmaf(v[8 * c8 + e], dsc, s.sb0[8 * ch + e]));
               uint4 hi, lo;
               uint32_t bad = 0;
               split_chunk(o, hi, lo, bad);
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
       for (int u = 0; u < MSG_MAXU; ++u)
         if (u < U)
 #pragma unroll
-          for (int e = 0; e < 16; ++e) m[u][e] = X3 ? __fadd_rn(__fmul_rn(m[u][e], dsc), s.sb1[c16 + e]) : m[u][e] + s.sb1[c16 + e];
+          for (int e = 0; e < 16; ++e) m[u][e] = X3 ? fmaf(m[u][e], dsc, s.sb1[c16 + e]) : m[u][e] + s.sb1[c16 + e];
 #pragma unroll
       for (int u = 0; u < MSG_MAXU; ++u) {
         if (u >= U) break;
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
     uint32_t bad = 0;
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
-      o[c] = X3 ? __fadd_rn(__fmul_rn(o[c], dsc), s.sb1[c]) : o[c] + s.sb1[c];
+      o[c] = X3 ? fmaf(o[c], dsc, s.sb1[c]) : o[c] + s.sb1[c];
       bad |= (__float_as_uint(o[c]) & 0x7f800000u) == 0x7f800000u;
     }
     if (bad && g.flag) atomicOr(g.flag, 1u);  // range guard (nrx_forward)

@@ -180,13 +180,16 @@ __device__ __forceinline__ void split_chunk(const float* v, uint4& hi, uint4& lo
   hi = make_uint4(h[0], h[1], h[2], h[3]);
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
-// split_chunk that also records a range violation: |v| > 65504 (the fp16
-// maximum), inf or NaN, at every split (the earliest point an overflowed
-// plane can be seen).
+// split_chunk that also records a range violation at every split (the
+// earliest point an overflowed plane can be seen): a hi half that is inf or
+// NaN (|v| >= 65520 rounds to inf; below that hi + lo 2^-11 still represents v).
+// Exponent field all ones, two halves per word: (e & 0x7c00) + 0x0400 carries
+// into the half's sign bit only for 0x7c00.
 __device__ __forceinline__ void split_chunk(const float* v, uint4& hi, uint4& lo, uint32_t& bad) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) bad |= (__float_as_uint(v[i]) & 0x7fffffffu) > 0x477fe000u;
   split_chunk(v, hi, lo);
+  const uint32_t h[4] = {hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) bad |= ((h[i] & 0x7c007c00u) + 0x04000400u) & 0x80008000u;
 }
 // the range-guard word (Geom::flag, NRX_WS_FLAG_OFFSET): one atomic per offending thread
 __device__ __forceinline__ void report_range(uint32_t bad, uint32_t* flag) {
