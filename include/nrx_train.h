@@ -16,10 +16,18 @@
  *
  * All pointers are device pointers; each call enqueues on `stream` (a
  * cudaStream_t) and returns 0, 1 (bad argument / shape beyond the limits:
- * cin, cout <= 128 with ceil(cin/8) * ceil(cout/4) <= 256, odd k) or 4 (CUDA error).
+ * cin, cout <= 128, odd k) or 4 (CUDA error).
+ *
+ * Tensor-core versions (csrc/k_train_tc.cu): the same three operators as
+ * fp32x3 GEMMs on tcgen05 (fp16 hi / lo operand planes with per-tensor
+ * power-of-two scales, fp32 accumulation) over a caller-owned
+ * device workspace of nrx_train_tc_workspace(...) bytes (0: unsupported
+ * shape; cin, cout <= 128, odd k).  No bias: the graph adds it.
  */
 #ifndef NRX_TRAIN_H_
 #define NRX_TRAIN_H_
+
+#include <stddef.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -33,6 +41,14 @@ int nrx_train_conv_wgrad(int n, int S, int T, int cin, int cout, int k, const fl
                          float* db, void* stream);
 int nrx_train_adam(int n, float* p, const float* grad, float* m, float* v, float lr, float beta1, float beta2,
                    float eps, int step, void* stream);
+
+size_t nrx_train_tc_workspace(int n, int S, int T, int cin, int cout, int k);
+int nrx_train_conv_tc_fwd(int n, int S, int T, int cin, int cout, int k, const float* x, const float* w, float* y,
+                          void* workspace, size_t workspace_bytes, void* stream);
+int nrx_train_conv_tc_dgrad(int n, int S, int T, int cin, int cout, int k, const float* dy, const float* w,
+                            float* dx, void* workspace, size_t workspace_bytes, void* stream);
+int nrx_train_conv_tc_wgrad(int n, int S, int T, int cin, int cout, int k, const float* x, const float* dy,
+                            float* dw, void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -37,7 +37,8 @@ EXPORTED = ("nrx_abi_version", "nrx_status_string", "nrx_validate", "nrx_weight_
             # include/nrx_classical.h
             "nrx_ls_lmmse", "nrx_kbest",
             # include/nrx_train.h
-            "nrx_train_conv_fwd", "nrx_train_conv_dgrad", "nrx_train_conv_wgrad", "nrx_train_adam")
+            "nrx_train_conv_fwd", "nrx_train_conv_dgrad", "nrx_train_conv_wgrad", "nrx_train_adam",
+            "nrx_train_tc_workspace", "nrx_train_conv_tc_fwd", "nrx_train_conv_tc_dgrad", "nrx_train_conv_tc_wgrad")
 KERNEL_IDS = {"ls_feat": 0, "conv_state_init0": 1, "conv_state_init1": 2, "msg_agg": 3,
               "conv_update0": 4, "conv_update1": 5, "readout": 6}
 
@@ -153,6 +154,11 @@ def load() -> ctypes.CDLL:
     lib.nrx_train_conv_dgrad.argtypes = [I, I, I, I, I, I, V, V, V, V]
     lib.nrx_train_conv_wgrad.argtypes = [I, I, I, I, I, I, V, V, V, V, V]
     lib.nrx_train_adam.argtypes = [I, V, V, V, V, F32, F32, F32, F32, I, V]
+    lib.nrx_train_tc_workspace.argtypes = [I, I, I, I, I, I]
+    lib.nrx_train_tc_workspace.restype = ctypes.c_size_t
+    for fn in (lib.nrx_train_conv_tc_fwd, lib.nrx_train_conv_tc_dgrad):
+        fn.argtypes = [I, I, I, I, I, I, V, V, V, V, ctypes.c_size_t, V]
+    lib.nrx_train_conv_tc_wgrad.argtypes = [I, I, I, I, I, I, V, V, V, V, ctypes.c_size_t, V]
     if lib.nrx_abi_version() != 1:
         raise NrxLibraryError("libnrx_b200.so ABI version mismatch")
     _LIB = lib

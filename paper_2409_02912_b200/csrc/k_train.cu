@@ -128,7 +128,8 @@ constexpr int WCHUNK = 1024;  // max pixels per wgrad block (fewer when there ar
 constexpr int WTP = 32;       // pixels staged per step
 
 // dw[tap] (+)= sum over a pixel chunk of x[p + shift(tap)] (outer) dy[p]; thread
-// (ti, to) owns i in [8 ti, 8 ti + 8), o in [4 to, 4 to + 4).  Tap-0 blocks
+// (ti, to) owns i in [8 ti, 8 ti + 8), o in [ob + 4 to, ob + 4 to + 4) with
+// ob = 64 blockIdx.z (outputs beyond 64 in a second grid plane).  Tap-0 blocks
 // also accumulate db.  Partials are added with fp32 atomics.
 __global__ void __launch_bounds__(THREADS) k_conv_wgrad(Shape g, int chunk, const float* __restrict__ x,
                                                         const float* __restrict__ dy, float* __restrict__ dw,
@@ -143,7 +144,8 @@ __global__ void __launch_bounds__(THREADS) k_conv_wgrad(Shape g, int chunk, cons
   const int ti = threadIdx.x >> 4, to = threadIdx.x & 15;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ds = a - g.r, dt = bb - g.r;
-  const bool active = 8 * ti < g.cin && 4 * to < g.cout;
+  const int ob = 64 * blockIdx.z + 4 * to;  // first output channel of this thread
+  const bool active = 8 * ti < g.cin && ob < g.cout;
   float acc[8][4], bacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < 8; ++i)
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(THREADS) k_conv_wgrad(Shape g, int chunk, cons
     for (int px = 0; px < WTP; ++px) {
       const float4 x0 = *reinterpret_cast<const float4*>(Xs + px * cip + 8 * ti);
       const float4 x1 = *reinterpret_cast<const float4*>(Xs + px * cip + 8 * ti + 4);
-      const float4 d4 = *reinterpret_cast<const float4*>(Ds + px * cop + 4 * to);
+      const float4 d4 = *reinterpret_cast<const float4*>(Ds + px * cop + ob);
       const float xi[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
       const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
@@ -183,13 +185,13 @@ __global__ void __launch_bounds__(THREADS) k_conv_wgrad(Shape g, int chunk, cons
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int o = 0; o < 4; ++o) {
-      const int ii = 8 * ti + i, oo = 4 * to + o;
+      const int ii = 8 * ti + i, oo = ob + o;
       if (ii < g.cin && oo < g.cout) atomicAdd(dw + (size_t)tap * nio + (size_t)ii * g.cout + oo, acc[i][o]);
     }
   if (db && tap == 0 && ti == 0)
 #pragma unroll
     for (int o = 0; o < 4; ++o)
-      if (4 * to + o < g.cout) atomicAdd(db + 4 * to + o, bacc[o]);
+      if (ob + o < g.cout) atomicAdd(db + ob + o, bacc[o]);
 }
 
 // Adam with the reference's bias-corrected update (autodiff.py:485-525)
@@ -262,7 +264,7 @@ int nrx_train_conv_wgrad(int n, int S, int T, int cin, int cout, int k, const fl
   if (chunks < want) chunks = want;
   const int per = ((g.pixels() + chunks - 1) / chunks + WTP - 1) / WTP * WTP;
   chunks = (g.pixels() + per - 1) / per;
-  dim3 grid(chunks, k * k);
+  dim3 grid(chunks, k * k, (cout + 63) / 64);
   k_conv_wgrad<<<grid, THREADS, smem, st>>>(g, per, x, dy, dw, db);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 4;
 }

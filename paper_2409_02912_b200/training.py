@@ -4,10 +4,12 @@ The reference trains with its own numpy autodiff on the CPU (multi-loss
 BCE over the readouts of every iteration + gamma * MSE on the channel
 readout, Adam; training.py:180-234, autodiff.py:358-525).  Here one training
 step is the same graph in PyTorch autograd on the device: convolutions and
-dense layers run as cuDNN / cuBLAS library kernels (the training path is
-not the inference hot path; inference stays on the hand-written tcgen05
-kernels), the inputs come from the GPU slot generator and the LS/feature
-kernel, and the Adam update follows the reference's formula exactly.
+dense layers, forward and backward, run on hand-written kernels (by default
+the tcgen05 fp32x3 GEMMs of csrc/k_train_tc.cu; the fp32 SIMT kernels of
+csrc/k_train.cu or cuDNN / cuBLAS on request), torch autograd sequences them
+and does the elementwise glue, the inputs come from the GPU slot generator
+and the LS/feature kernel, and the Adam update (csrc/k_train.cu) follows the
+reference's formula exactly.
 
 Parity (tests/test_training_cpu.py, against tests/golden/train_*.npz made by
 the reference's own train_step): loss, every gradient and the weights after
@@ -60,6 +62,81 @@ def _nrx_lib():
 
 
 _CONV_FN = None
+_CONV_TC_FN = None
+_TC_WS = {}
+
+
+def _tc_workspace(torch, device, nbytes):
+    """One growing device workspace per device for the tensor-core training
+    GEMMs (every op of a step runs on the same stream, so they can share it)."""
+    ws = _TC_WS.get(device)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _TC_WS[device] = ws
+    return ws
+
+
+def _nrx_conv_tc_fn():
+    """torch.autograd.Function over the tcgen05 fp32x3 GEMMs of
+    csrc/k_train_tc.cu (include/nrx_train.h nrx_train_conv_tc_*): the same
+    three operators as _nrx_conv_fn at fp32 accuracy on the tensor cores."""
+    global _CONV_TC_FN
+    if _CONV_TC_FN is not None:
+        return _CONV_TC_FN
+    torch = _torch()
+
+    def _stream(t):
+        return torch.cuda.current_stream(t.device).cuda_stream
+
+    def _ws(lib, x_shape, cin, cout, k, device):
+        n, S, T = x_shape[0], x_shape[1], x_shape[2]
+        need = lib.nrx_train_tc_workspace(n, S, T, cin, cout, k)
+        if need == 0:
+            raise RuntimeError(f"nrx_train_tc: unsupported shape {tuple(x_shape)} x ({k},{k},{cin},{cout})")
+        return _tc_workspace(torch, device, need), need
+
+    class NrxConvTc(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, x, w):
+            x = x.contiguous()
+            w = w.contiguous()
+            n, S, T, cin = x.shape
+            k, cout = w.shape[0], w.shape[3]
+            lib = _nrx_lib()
+            ws, nb = _ws(lib, x.shape, cin, cout, k, x.device)
+            y = torch.empty((n, S, T, cout), dtype=torch.float32, device=x.device)
+            code = lib.nrx_train_conv_tc_fwd(n, S, T, cin, cout, k, x.data_ptr(), w.data_ptr(), y.data_ptr(),
+                                             ws.data_ptr(), nb, _stream(x))
+            if code:
+                raise RuntimeError(f"nrx_train_conv_tc_fwd failed ({code})")
+            ctx.save_for_backward(x, w)
+            return y
+
+        @staticmethod
+        def backward(ctx, dy):
+            x, w = ctx.saved_tensors
+            dy = dy.contiguous()
+            n, S, T, cin = x.shape
+            k, cout = w.shape[0], w.shape[3]
+            lib = _nrx_lib()
+            ws, nb = _ws(lib, x.shape, cin, cout, k, x.device)
+            dx = dw = None
+            if ctx.needs_input_grad[0]:
+                dx = torch.empty_like(x)
+                code = lib.nrx_train_conv_tc_dgrad(n, S, T, cin, cout, k, dy.data_ptr(), w.data_ptr(),
+                                                   dx.data_ptr(), ws.data_ptr(), nb, _stream(dy))
+                if code:
+                    raise RuntimeError(f"nrx_train_conv_tc_dgrad failed ({code})")
+            if ctx.needs_input_grad[1]:
+                dw = torch.empty_like(w)
+                code = lib.nrx_train_conv_tc_wgrad(n, S, T, cin, cout, k, x.data_ptr(), dy.data_ptr(),
+                                                   dw.data_ptr(), ws.data_ptr(), nb, _stream(dy))
+                if code:
+                    raise RuntimeError(f"nrx_train_conv_tc_wgrad failed ({code})")
+            return dx, dw
+
+    _CONV_TC_FN = NrxConvTc
+    return NrxConvTc
 
 
 def _nrx_conv_fn():
@@ -121,8 +198,9 @@ class TorchNrxGraph:
     """The NRX graph on torch tensors.  ``params`` maps the reference's weight
     names to leaf tensors (float32, requires_grad).
 
-    kernels="nrx" (default on CUDA devices) runs every convolution and dense
-    layer, forward and backward, on the hand-written fp32 kernels of
+    kernels="nrx_tc" (default on CUDA devices) runs every convolution and
+    dense layer, forward and backward, on the tcgen05 fp32x3 GEMMs of
+    csrc/k_train_tc.cu; kernels="nrx" on the hand-written fp32 SIMT kernels of
     csrc/k_train.cu; torch autograd only sequences them and does the
     elementwise glue (bias, ReLU, residual, concat, sum of others, losses).
     kernels="torch" uses cuDNN / cuBLAS (with TF32 off, see fp32_math)."""
@@ -131,11 +209,16 @@ class TorchNrxGraph:
         torch = _torch()
         self.config = config
         self.device = torch.device(device)
-        self.kernels = kernels or ("nrx" if self.device.type == "cuda" else "torch")
-        if self.kernels == "nrx" and self.device.type != "cuda":
-            raise ValueError("kernels='nrx' needs a CUDA device")
+        self.kernels = kernels or ("nrx_tc" if self.device.type == "cuda" else "torch")
+        if self.kernels not in ("nrx", "nrx_tc", "torch"):
+            raise ValueError(f"unknown kernels {self.kernels!r}")
+        if self.kernels != "torch" and self.device.type != "cuda":
+            raise ValueError(f"kernels={self.kernels!r} needs a CUDA device")
         self.params = {k: torch.tensor(np.asarray(getattr(v, "data", v), dtype=np.float32), device=self.device,
                                        requires_grad=True) for k, v in weights.items()}
+
+    def _conv_fn(self):
+        return _nrx_conv_tc_fn() if self.kernels == "nrx_tc" else _nrx_conv_fn()
 
     def numpy_weights(self) -> dict:
         return {k: v.detach().cpu().numpy().copy() for k, v in self.params.items()}
@@ -145,8 +228,8 @@ class TorchNrxGraph:
         """'same' k x k convolution of NHWC x (H = subcarrier, W = symbol)
         with a (k, k, Cin, Cout) kernel (autodiff.py:324-350)."""
         w = self.params[name]
-        if self.kernels == "nrx":
-            return _nrx_conv_fn().apply(x, w)
+        if self.kernels != "torch":
+            return self._conv_fn().apply(x, w)
         F = _torch().nn.functional
         k = w.shape[0]
         y = F.conv2d(x.permute(0, 3, 1, 2), w.permute(3, 2, 0, 1), padding=k // 2)
@@ -155,11 +238,11 @@ class TorchNrxGraph:
     def _dense(self, x, name):
         """x (..., cin) @ W (cin, cout): a 1x1 convolution of the flattened rows."""
         w = self.params[name]
-        if self.kernels != "nrx":
+        if self.kernels == "torch":
             return x @ w
         lead = x.shape[:-1]
         rows = x.reshape(-1, 1, 1, x.shape[-1])
-        y = _nrx_conv_fn().apply(rows, w.reshape(1, 1, w.shape[0], w.shape[1]))
+        y = self._conv_fn().apply(rows, w.reshape(1, 1, w.shape[0], w.shape[1]))
         return y.reshape(lead + (w.shape[1],))
 
     def _conv_block(self, x, prefix):

@@ -9,6 +9,6 @@ cfg = SlotConfig(num_subcarriers=96, num_ues=2)
 config = NrxConfig.from_table(table, (14,), d_s=56, num_iterations=2)
 w = init_weights(config, 0)
 src = GpuSlotSource(cfg)
-g = TorchNrxGraph(config, w, src.device, kernels="nrx")
+g = TorchNrxGraph(config, w, src.device, kernels=sys.argv[1] if len(sys.argv) > 1 else "nrx")
 train_gpu(config, w, src, table, GpuTrainConfig(batch_size=32, steps=3, seed=1), graph=g, adam=Adam(lr=1e-3))
 torch.cuda.synchronize()

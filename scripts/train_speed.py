@@ -29,7 +29,7 @@ def main():
         config = NrxConfig.from_table(table, (14,), d_s=d, num_iterations=2)
         w = init_weights(config, 0)
         src = GpuSlotSource(cfg)
-        for kernels in ("nrx", "torch"):
+        for kernels in ("nrx", "nrx_tc", "torch"):
             tcfg = GpuTrainConfig(batch_size=batch, steps=args.steps, snr_lo_db=4.0, snr_hi_db=24.0,
                                   learning_rate=1e-3, seed=1)
             g = TorchNrxGraph(config, w, src.device, kernels=kernels)

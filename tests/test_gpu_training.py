@@ -36,11 +36,12 @@ def test_gpu_training_reduces_loss_and_ber():
     assert b1 < 0.75 * b0, (b0, b1)
 
 
-@pytest.mark.parametrize("kernels", ["nrx", "torch"])
+@pytest.mark.parametrize("kernels", ["nrx", "nrx_tc", "torch"])
 @pytest.mark.parametrize("name", ["train_masking", "train_var_io"])
 def test_gpu_train_step_matches_reference(name, kernels):
     """One training step on the GPU (kernels="nrx": the hand-written fp32
-    convolution / dense / Adam kernels; "torch": cuDNN / cuBLAS with TF32 off) against the
+    convolution / dense / Adam kernels; "nrx_tc": the tcgen05 fp32x3 GEMMs;
+    "torch": cuDNN / cuBLAS with TF32 off) against the
     reference's own train_step on the same batch (tests/golden/train_*.npz):
     the loss breakdown to 1e-5, the Adam step to 1e-3 relative (same gates
     as the CPU test)."""
@@ -63,14 +64,17 @@ def test_gpu_train_step_matches_reference(name, kernels):
         np.testing.assert_allclose(got[k] - w0[k], ref - w0[k], rtol=1e-3, atol=1e-6, err_msg=k)
 
 
+@pytest.mark.parametrize("tc", [False, True])
 @pytest.mark.parametrize("k,cin,cout,S,T,n", [(3, 19, 16, 24, 14, 3), (3, 114, 56, 20, 14, 2), (5, 8, 8, 11, 7, 2),
-                                              (1, 56, 56, 300, 1, 1), (1, 56, 4, 1000, 1, 1)])
-def test_train_conv_kernels_vs_float64(k, cin, cout, S, T, n):
-    """The hand-written training kernels (csrc/k_train.cu) against float64
-    torch: 'same' convolution forward, input gradient and kernel gradient
-    (k = 1, T = 1 is the dense layer), fp32 accumulation error only."""
+                                              (1, 56, 56, 300, 1, 1), (1, 56, 4, 1000, 1, 1),
+                                              (3, 128, 128, 40, 14, 3), (3, 56, 114, 96, 14, 4)])
+def test_train_conv_kernels_vs_float64(k, cin, cout, S, T, n, tc):
+    """The hand-written training kernels (csrc/k_train.cu SIMT, or with tc the
+    tcgen05 fp32x3 GEMMs of csrc/k_train_tc.cu) against float64 torch: 'same'
+    convolution forward, input gradient and kernel gradient (k = 1, T = 1 is
+    the dense layer), fp32-level error only."""
     import torch
-    from paper_2409_02912_b200.training import _nrx_conv_fn
+    from paper_2409_02912_b200.training import _nrx_conv_fn, _nrx_conv_tc_fn
     g = torch.Generator().manual_seed(k * 1000 + cin)
     x = torch.randn(n, S, T, cin, generator=g, dtype=torch.float64)
     w = torch.randn(k, k, cin, cout, generator=g, dtype=torch.float64) / np.sqrt(k * k * cin)
@@ -80,7 +84,7 @@ def test_train_conv_kernels_vs_float64(k, cin, cout, S, T, n):
     yr.backward(dy)
     xc = x.float().cuda().requires_grad_()
     wc = w.float().cuda().requires_grad_()
-    yc = _nrx_conv_fn().apply(xc, wc)
+    yc = (_nrx_conv_tc_fn() if tc else _nrx_conv_fn()).apply(xc, wc)
     yc.backward(dy.float().cuda())
     for got, ref in ((yc, yr), (xc.grad, xr.grad), (wc.grad, wr.grad)):
         ref = ref.detach()
