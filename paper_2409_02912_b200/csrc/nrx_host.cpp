@@ -86,11 +86,18 @@ int validate(const nrx_model_desc* m, const nrx_slot_desc* s) {
 
 int quantum(int prec) { return prec == NRX_FP32 ? 4 : 16; }
 
+// Largest padded MLP hidden width per mode: the message / readout MLPs keep two
+// hidden tiles and the readout's N = 2 hidden GEMM in TMEM and shared memory
+// (fp16 / bf16: the fused readout tail next to the convolution accumulators;
+// fp32x3: hi and lo planes of the hidden tile).
+int hidden_limit(int prec) { return prec == NRX_FP32 ? 256 : prec == NRX_FP32X3 ? 96 : 64; }
+
 int make_geom(const nrx_model_desc* m, const nrx_slot_desc* s, int n_slots, int prec, Geom* g) {
   int st = validate(m, s);
   if (st) return st;
   if (n_slots < 1) return NRX_ERR_INVALID;
   if (prec != NRX_FP32 && prec != NRX_BF16 && prec != NRX_FP16 && prec != NRX_FP32X3) return NRX_ERR_INVALID;
+  if (hidden_limit(prec) < rup(m->hidden, 16)) return NRX_ERR_UNSUPPORTED;
   std::memset(g, 0, sizeof(*g));
   g->N = n_slots;
   g->U = s->num_ues;
@@ -684,14 +691,9 @@ int nrx_pack_weights(const nrx_model_desc* m, int prec, const float* const* tens
   for (int i = 0; i < n; ++i)
     if (!tensors[i]) return NRX_ERR_INVALID;
   if (prec == NRX_FP32) return pack_weights_f32(m, tensors, (uint8_t*)out);
-  if (prec == NRX_FP32X3) {
-    if (m->hidden > 128) return NRX_ERR_UNSUPPORTED;
-    return pack_weights_x3(m, tensors, (uint8_t*)out);
-  }
-  if (prec == NRX_BF16 || prec == NRX_FP16) {
-    if (m->hidden > 128) return NRX_ERR_UNSUPPORTED;
-    return pack_weights_tc(m, prec, tensors, (uint8_t*)out);
-  }
+  if (hidden_limit(prec) < rup(m->hidden, 16)) return NRX_ERR_UNSUPPORTED;
+  if (prec == NRX_FP32X3) return pack_weights_x3(m, tensors, (uint8_t*)out);
+  if (prec == NRX_BF16 || prec == NRX_FP16) return pack_weights_tc(m, prec, tensors, (uint8_t*)out);
   return NRX_ERR_INVALID;
 }
 

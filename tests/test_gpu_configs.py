@@ -117,3 +117,34 @@ def test_fp32x3_positional_fold_edges(d, comb, S, U, T, pilots, freq):
     got, ref, chest, ref_chest = _run(cfg, config, w, tuple(t[14] for _ in range(U)), 2, 11, "fp32")
     check_llrs(got, ref, "fp32", f"posf d={d} comb={comb} S={S}")
     check_chest(chest, ref_chest, "fp32")
+
+
+HIDDEN_LIMIT = {"fp32": 96, "fp32_simt": 256, "bf16": 64, "fp16": 64}  # nrx_host.cpp hidden_limit
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("d,h,U,comb,k,T,pilots,S", [
+    (64, 64, 2, 2, 3, 14, (2, 11), 48),       # largest state depth
+    (64, 96, 2, 2, 3, 14, (2, 11), 48),       # largest hidden width of the fp32 mode
+    (56, 128, 2, 2, 3, 14, (2, 11), 48),      # beyond the tensor-core modes' hidden width: fp32_simt only
+    (48, 48, 4, 4, 3, 14, (2, 11), 40),       # four UEs (direct sums over the others), N = 2 x 48 pair MMAs
+    (24, 24, 2, 2, 1, 14, (2, 11), 60),       # 1x1 kernels
+    (32, 32, 2, 2, 3, 32, (0, 9, 18, 27), 24),  # 32 symbols (the longest slot), four pilot symbols
+])
+def test_limit_configs_vs_oracle(precision, d, h, U, comb, k, T, pilots, S):
+    """Model / slot shapes at the limits include/nrx_b200.h documents, run
+    through the generic (not unrolled) kernel instances, against the float64
+    oracle with the per-precision gates."""
+    from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights
+    t = default_mcs_table()
+    cfg = SlotConfig(num_subcarriers=S, num_symbols=T, pilot_symbols=pilots, num_ues=U, comb_size=comb)
+    config = NrxConfig.from_table(t, (14,), d_s=d, hidden_width=h, kernel_size=k, num_iterations=2)
+    w = orc.perturb_biases(init_weights(config, 5))
+    if -(-h // 16) * 16 > HIDDEN_LIMIT[precision]:  # rejected up front, not at a kernel launch
+        from paper_2409_02912_b200._lib import NrxLibraryError
+        with pytest.raises(NrxLibraryError, match="outside the limits"):
+            _run(cfg, config, w, tuple(t[14] for _ in range(U)), 1, 13, precision)
+        return
+    got, ref, chest, ref_chest = _run(cfg, config, w, tuple(t[14] for _ in range(U)), 2, 13, precision)
+    check_llrs(got, ref, precision, f"limits d={d} h={h} U={U} k={k} T={T}")
+    check_chest(chest, ref_chest, precision)
