@@ -91,6 +91,11 @@ int quantum(int prec) { return prec == NRX_FP32 ? 4 : 16; }
 // (fp16 / bf16: the fused readout tail next to the convolution accumulators;
 // fp32x3: hi and lo planes of the hidden tile).
 int hidden_limit(int prec) { return prec == NRX_FP32 ? 256 : prec == NRX_FP32X3 ? 96 : 64; }
+constexpr size_t kResidentLimit = 170 * 1024;
+size_t resident_conv_bytes(int ks, int d, int prec) {
+  const int np = prec == NRX_FP32X3 ? x3_np(d) : rup(d, 16);
+  return (size_t)ks * ks * (rup(d + 2, 16) + rup(d, 16)) * np * 2;
+}
 
 int make_geom(const nrx_model_desc* m, const nrx_slot_desc* s, int n_slots, int prec, Geom* g) {
   int st = validate(m, s);
@@ -133,6 +138,15 @@ int make_geom(const nrx_model_desc* m, const nrx_slot_desc* s, int n_slots, int 
   g->Cs = rup(g->d + 2, q);
   g->Ch = rup(g->d, q);
   g->Ca = rup(g->d, q);
+  // tensor-core modes keep a layer's weights resident in shared memory: update.conv0
+  // (taps x (Cs + Ca) x np fp16, the largest layer) must leave room for two pipeline
+  // stages (e.g. 5x5 kernels fit up to d_s = 32)
+  if (prec != NRX_FP32 && resident_conv_bytes(g->ks, g->d, prec) > kResidentLimit) return NRX_ERR_UNSUPPORTED;
+  // the standalone message kernel (fp32x3: every U; bf16 / fp16: U != 2) holds two
+  // hidden tiles and the U message tiles of a slot in TMEM (512 columns)
+  if (prec != NRX_FP32 && (prec == NRX_FP32X3 || g->U != 2) &&
+      2 * rup(m->hidden, 16) + 2 * g->U * rup(g->d, 16) > 512)
+    return NRX_ERR_UNSUPPORTED;
   g->n_io = m->n_io;
   int w = 0;
   for (int i = 0; i < m->n_io; ++i) {

@@ -130,9 +130,9 @@ class NrxEngine:
         torch = _require_cuda()
         s = _lib.slot_desc(cfg)
         nbytes = self.lib.nrx_workspace_bytes(ctypes.byref(self._m), ctypes.byref(s), n_slots, self.prec_id)
-        if nbytes == 0:
+        if nbytes == 0:  # the model / slot is invalid, or outside this precision mode's limits
             code = self.lib.nrx_validate(ctypes.byref(self._m), ctypes.byref(s))
-            _lib.check(code or 1, "nrx_workspace_bytes")
+            _lib.check(code or 2, f"nrx_workspace_bytes ({self.precision})")
         tls = self._local()
         ws = tls.ws.get("ws")
         if ws is None or ws.numel() < nbytes:

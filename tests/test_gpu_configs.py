@@ -148,3 +148,63 @@ def test_limit_configs_vs_oracle(precision, d, h, U, comb, k, T, pilots, S):
     got, ref, chest, ref_chest = _run(cfg, config, w, tuple(t[14] for _ in range(U)), 2, 13, precision)
     check_llrs(got, ref, precision, f"limits d={d} h={h} U={U} k={k} T={T}")
     check_chest(chest, ref_chest, precision)
+
+
+def tc_supported(precision, d, h, U, k):
+    """Mirror of the tensor-core modes' shape limits (nrx_host.cpp make_geom)."""
+    r16 = lambda v: -(-v // 16) * 16  # noqa: E731
+    if precision == "fp32_simt":
+        return True
+    np_ = (56 if -(-d // 8) * 8 == 56 else r16(d)) if precision == "fp32" else r16(d)
+    if k * k * (r16(d + 2) + r16(d)) * np_ * 2 > 170 * 1024:   # update.conv0 weights resident
+        return False
+    if r16(h) > (96 if precision == "fp32" else 64):            # hidden_limit
+        return False
+    if (precision == "fp32" or U != 2) and 2 * r16(h) + 2 * U * r16(d) > 512:   # message kernel TMEM
+        return False
+    return True
+
+
+def _random_config(seed):
+    rng = np.random.default_rng(seed)
+    d = int(rng.choice([8, 12, 16, 24, 32, 40, 48, 56, 64]))
+    h = int(min(96, rng.choice([d, d, 16, 24, 40, 72])))
+    U = int(rng.integers(1, 4))
+    comb = int(max(U, rng.choice([1, 2, 4])))
+    k = int(rng.choice([1, 3, 3, 5]))
+    T = int(rng.choice([7, 14, 14, 20]))
+    pilots = tuple(sorted(rng.choice(T, size=int(rng.integers(1, 3)), replace=False).tolist()))
+    S = int(rng.integers(4, 30)) * comb
+    variant = str(rng.choice(["single", "masking", "var_io"]))
+    noise, freq = bool(rng.integers(0, 2)), bool(rng.integers(0, 2))
+    return d, h, U, comb, k, T, pilots, S, variant, noise, freq
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
+@pytest.mark.parametrize("seed", range(16))
+def test_random_configs_vs_oracle(seed, precision):
+    """Seeded random model / slot shapes (depth, hidden width, UEs, comb,
+    kernel size, symbols, pilot symbols, variant, flags) through whichever
+    kernel instances they select, against the float64 oracle."""
+    from paper_2409_02912_b200.config import NrxConfig, SlotConfig, default_mcs_table, init_weights
+    d, h, U, comb, k, T, pilots, S, variant, noise, freq = _random_config(seed)
+    if precision == "fp16" and h > 64:
+        h = 64
+    t = default_mcs_table()
+    cfg = SlotConfig(num_subcarriers=S, num_symbols=T, pilot_symbols=pilots, num_ues=U, comb_size=comb)
+    supported = {"single": (14,), "masking": (9, 14, 19), "var_io": (9, 14, 19)}[variant]
+    config = NrxConfig.from_table(t, supported, variant=variant, d_s=d, hidden_width=h, kernel_size=k,
+                                  num_iterations=2, include_noise_plane=noise, include_freq_encoding=freq)
+    w = orc.perturb_biases(init_weights(config, seed))
+    rng = np.random.default_rng(100 + seed)
+    mcs = tuple(t[int(rng.choice(supported))] for _ in range(U))
+    if not tc_supported(precision, d, h, U, k):
+        # beyond the tensor-core mode's limits (nrx_host.cpp make_geom): rejected up front;
+        # the fp32 SIMT kernels take the shape
+        from paper_2409_02912_b200._lib import NrxLibraryError
+        with pytest.raises(NrxLibraryError, match="outside the limits"):
+            _run(cfg, config, w, mcs, 1, 20 + seed, precision)
+        precision = "fp32_simt"
+    got, ref, chest, ref_chest = _run(cfg, config, w, mcs, 2, 20 + seed, precision)
+    check_llrs(got, ref, precision, f"random config {seed}: {_random_config(seed)}")
+    check_chest(chest, ref_chest, precision)
