@@ -90,7 +90,11 @@ class LdpcDesc(ctypes.Structure):
 
 
 class NrxLibraryError(RuntimeError):
-    pass
+    """A failed library call; ``status`` is the nrx_status code (0 if none)."""
+
+    def __init__(self, msg, status: int = 0):
+        super().__init__(msg)
+        self.status = status
 
 
 _LIB = None
@@ -171,7 +175,7 @@ def status_text(code: int) -> str:
 
 def check(code: int, what: str) -> None:
     if code != 0:
-        raise NrxLibraryError(f"{what} failed: {status_text(code)} (status {code})")
+        raise NrxLibraryError(f"{what} failed: {status_text(code)} (status {code})", code)
 
 
 def model_desc(config) -> ModelDesc:

@@ -23,8 +23,11 @@ import zlib
 
 import numpy as np
 
+from ._lib import NrxLibraryError
 from .config import weight_array
 from .engine import NrxEngine, pilot_comb_values
+
+NRX_ERR_UNSUPPORTED = 2  # include/nrx_b200.h
 
 # Mirror of the reference's debug switch autodiff.CHECK_FINITE
 # (autodiff.py:27-29,130-131): when set, a forward whose outputs are not all
@@ -175,20 +178,31 @@ def nrx_forward(y, books, cfg, mcs_per_ue, w, config, n0, num_iterations=None, a
              (m if config.variant == "var_io" else config.m_max) for m in orders]
     args = (cfg, y, stack_pilots(books, n, cfg), noise_features(n0, n),
             np.tile(np.asarray(orders, dtype=np.int32), (n, 1)), n_it, max(width), exact_inputs)
-    eng, fp_packed = _speculative_engine(w, config, precision, device) if check_weights else (None, None)
-    if eng is not None:
-        # run with the engine this dict used last time and fingerprint the
-        # weights while the GPU works; if they changed in place (e.g. an Adam
-        # step, autodiff.py:525) repack and run again
-        handle = eng.enqueue_arrays(*args)
-        fp = _fingerprint(w)
-        llr_full, chest, nonfinite = eng.finish(handle)
-        if fp != fp_packed:
-            eng = get_engine(w, config, precision, device, check_weights, fingerprint=fp)
+    try:
+        eng, fp_packed = _speculative_engine(w, config, precision, device) if check_weights else (None, None)
+        if eng is not None:
+            # run with the engine this dict used last time and fingerprint the
+            # weights while the GPU works; if they changed in place (e.g. an Adam
+            # step, autodiff.py:525) repack and run again
+            handle = eng.enqueue_arrays(*args)
+            fp = _fingerprint(w)
+            llr_full, chest, nonfinite = eng.finish(handle)
+            if fp != fp_packed:
+                eng = get_engine(w, config, precision, device, check_weights, fingerprint=fp)
+                llr_full, chest, nonfinite = eng.finish(eng.enqueue_arrays(*args))
+        else:
+            eng = get_engine(w, config, precision, device, check_weights)
             llr_full, chest, nonfinite = eng.finish(eng.enqueue_arrays(*args))
-    else:
-        eng = get_engine(w, config, precision, device, check_weights)
-        llr_full, chest, nonfinite = eng.finish(eng.enqueue_arrays(*args))
+    except NrxLibraryError as e:
+        if precision == "fp32_simt" or e.status != NRX_ERR_UNSUPPORTED:
+            raise
+        # a shape beyond the tensor-core modes' limits (resident weights, TMEM):
+        # the reference accepts any shape, so the fp32 SIMT kernels take it
+        warnings.warn(f"nrx_forward: {precision} tensor-core path does not support this model / slot shape "
+                      f"({e}); computing it with precision='fp32_simt'", RuntimeWarning, stacklevel=2)
+        eng = get_engine(w, config, "fp32_simt", device, check_weights)
+        llr_full, chest = eng.run_arrays(*args)
+        nonfinite = False
     if nonfinite and precision != "fp32_simt" and np.isfinite(y).all():
         # range guard: an fp16 operand plane overflowed (|activation| > 65504);
         # the fp32 SIMT kernels compute this call with the reference's range

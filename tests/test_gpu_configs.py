@@ -140,12 +140,14 @@ def test_limit_configs_vs_oracle(precision, d, h, U, comb, k, T, pilots, S):
     cfg = SlotConfig(num_subcarriers=S, num_symbols=T, pilot_symbols=pilots, num_ues=U, comb_size=comb)
     config = NrxConfig.from_table(t, (14,), d_s=d, hidden_width=h, kernel_size=k, num_iterations=2)
     w = orc.perturb_biases(init_weights(config, 5))
-    if -(-h // 16) * 16 > HIDDEN_LIMIT[precision]:  # rejected up front, not at a kernel launch
-        from paper_2409_02912_b200._lib import NrxLibraryError
-        with pytest.raises(NrxLibraryError, match="outside the limits"):
-            _run(cfg, config, w, tuple(t[14] for _ in range(U)), 1, 13, precision)
-        return
-    got, ref, chest, ref_chest = _run(cfg, config, w, tuple(t[14] for _ in range(U)), 2, 13, precision)
+    if -(-h // 16) * 16 > HIDDEN_LIMIT[precision]:
+        # rejected up front (not at a kernel launch); the drop-in computes the call on the
+        # fp32 SIMT kernels with a RuntimeWarning, the reference accepting any shape
+        with pytest.warns(RuntimeWarning, match="does not support"):
+            got, ref, chest, ref_chest = _run(cfg, config, w, tuple(t[14] for _ in range(U)), 2, 13, precision)
+        precision = "fp32_simt"
+    else:
+        got, ref, chest, ref_chest = _run(cfg, config, w, tuple(t[14] for _ in range(U)), 2, 13, precision)
     check_llrs(got, ref, precision, f"limits d={d} h={h} U={U} k={k} T={T}")
     check_chest(chest, ref_chest, precision)
 
@@ -199,12 +201,12 @@ def test_random_configs_vs_oracle(seed, precision):
     rng = np.random.default_rng(100 + seed)
     mcs = tuple(t[int(rng.choice(supported))] for _ in range(U))
     if not tc_supported(precision, d, h, U, k):
-        # beyond the tensor-core mode's limits (nrx_host.cpp make_geom): rejected up front;
-        # the fp32 SIMT kernels take the shape
-        from paper_2409_02912_b200._lib import NrxLibraryError
-        with pytest.raises(NrxLibraryError, match="outside the limits"):
-            _run(cfg, config, w, mcs, 1, 20 + seed, precision)
+        # beyond the tensor-core mode's limits (nrx_host.cpp make_geom): rejected up front,
+        # and the drop-in computes the call on the fp32 SIMT kernels with a RuntimeWarning
+        with pytest.warns(RuntimeWarning, match="does not support"):
+            got, ref, chest, ref_chest = _run(cfg, config, w, mcs, 2, 20 + seed, precision)
         precision = "fp32_simt"
-    got, ref, chest, ref_chest = _run(cfg, config, w, mcs, 2, 20 + seed, precision)
+    else:
+        got, ref, chest, ref_chest = _run(cfg, config, w, mcs, 2, 20 + seed, precision)
     check_llrs(got, ref, precision, f"random config {seed}: {_random_config(seed)}")
     check_chest(chest, ref_chest, precision)
