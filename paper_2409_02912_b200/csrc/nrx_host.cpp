@@ -433,6 +433,29 @@ void pack_conv_x3(const Geom& g, int k, const ConvOff& c, int cin_ref, const flo
   db[npx] = std::ldexp(1.f, -E);
 }
 
+// The same for a 56-channel conv1 in the tap-pair K order (tp2_slot); the
+// block keeps the taps x ktap size, its last 8 slots stay zero.
+void pack_conv_x3_tp2(const Geom& g, const ConvOff& c, const float* w, const float* b, uint8_t* base) {
+  const int npx = x3_np(g.d), taps = 9, cout = g.d, cin_ref = g.d;
+  float mx = 0.f;
+  for (size_t i = 0; i < (size_t)taps * cin_ref * cout; ++i) mx = std::fmax(mx, std::fabs(w[i]));
+  const int E = split_exponent(mx);
+  const size_t half = (size_t)taps * c.ktap * npx;
+  SplitB B{(uint16_t*)(base + c.w), npx, half, std::ldexp(1.f, E)};
+  for (int slot = 0; slot < 2 * TP2_STEPS; ++slot) {
+    int tap, ch;
+    tp2_slot(slot, &tap, &ch);
+    for (int j = 0; j < 8; ++j) {
+      const int src = 8 * ch + j;
+      for (int o = 0; o < npx; ++o)
+        B.set(o, 8 * slot + j, (src < cin_ref && o < cout) ? w[((size_t)tap * cin_ref + src) * cout + o] : 0.f);
+    }
+  }
+  float* db = (float*)(base + c.b);
+  for (int o = 0; o < npx; ++o) db[o] = o < cout ? b[o] : 0.f;
+  db[npx] = std::ldexp(1.f, -E);
+}
+
 // Half-precision convolution for the CTA pair: rank r holds output channels
 // [r np/2, (r+1) np/2) as [K/8][np/2][8] (the pair MMA reads B as rank 0's
 // rows followed by rank 1's).
@@ -480,7 +503,10 @@ int pack_weights_x3(const nrx_model_desc* m, const float* const* t, uint8_t* bas
   for (int io = 0; io < m->n_io; ++io) {
     const int i = 8 * io;
     pack_conv_x3(g, k, L.init0[io], g.Cin, t[i], t[i + 1], map_identity_feats, base);
-    pack_conv_x3(g, k, L.init1[io], d, t[i + 2], t[i + 3], map_identity_hidden, base);
+    if (tp2_layer(d, k, NRX_FP32X3))
+      pack_conv_x3_tp2(g, L.init1[io], t[i + 2], t[i + 3], base);
+    else
+      pack_conv_x3(g, k, L.init1[io], d, t[i + 2], t[i + 3], map_identity_hidden, base);
     const MlpOff& o = L.llr[io];
     const int width = llr_width_of(m, io);
     const float *lw0 = t[i + 4], *lb0 = t[i + 5], *lw1 = t[i + 6], *lb1 = t[i + 7];
@@ -534,7 +560,10 @@ int pack_weights_x3(const nrx_model_desc* m, const float* const* t, uint8_t* bas
   } else {
     pack_conv_x3(g, k, L.upd0, 2 * d + 2, t[i_upd], t[i_upd + 1], map_update, base);
   }
-  pack_conv_x3(g, k, L.upd1, d, t[i_upd + 2], t[i_upd + 3], map_identity_hidden, base);
+  if (tp2_layer(d, k, NRX_FP32X3))
+    pack_conv_x3_tp2(g, L.upd1, t[i_upd + 2], t[i_upd + 3], base);
+  else
+    pack_conv_x3(g, k, L.upd1, d, t[i_upd + 2], t[i_upd + 3], map_identity_hidden, base);
   return NRX_OK;
 }
 

@@ -57,6 +57,32 @@ inline bool upd0_posf(int d, int ks, int prec) {
 // float offset of the positional weights [channel dt, df][tap][np] in a conv bias block
 inline int posw_off(int np) { return np + 4; }
 
+// fp32x3 3x3 convolutions over a 56-channel input (state_init.conv1 and
+// iteration.update.conv1 of d_s = 56): 7 channel chunks per tap, so a K = 16
+// MMA step over one tap wastes the zero 8th chunk.  "Tap pairs" order the K
+// slots (8 channels each) so that one step straddles two taps: taps (t, t+1)
+// take 7 steps instead of 8 -- (t,0)(t,1) (t,2)(t,3) (t,4)(t,5) (t+1,0)(t,6)
+// (t+1,1)(t+1,2) (t+1,3)(t+1,4) (t+1,5)(t+1,6) -- for the pairs (0,1) (2,3) (4,5)
+// (6,7), then tap 8 alone in 4 steps: 32 MMA steps per plane instead of 36.
+// Only chunks 0-6 are loaded (the TMA box skips the zero chunk 7).
+// The straddling step's two 8-channel halves sit at different row offsets,
+// which its A descriptor's leading-byte offset expresses.
+inline bool tp2_layer(int d, int ks, int prec) { return prec == NRX_FP32X3 && ks == 3 && d == 56; }
+constexpr int TP2_STEPS = 32;
+inline void tp2_slot(int slot, int* tap, int* chunk) {  // half-slot (8 K values) -> (tap, channel chunk)
+  const int step = slot / 2, h = slot & 1;
+  if (step >= 28) {  // tap 8 alone; the last step pairs the zero-weight chunk 7 slot (its A half
+    *tap = 8;         // reads chunk 5, which the TMA does load) with chunk 6
+    *chunk = step == 31 ? (h ? 6 : 7) : 2 * (step - 28) + h;
+    return;
+  }
+  const int pr = step / 7, s = step % 7, t = 2 * pr;
+  static const int tap_of[7][2] = {{0, 0}, {0, 0}, {0, 0}, {1, 0}, {1, 1}, {1, 1}, {1, 1}};
+  static const int ch_of[7][2] = {{0, 1}, {2, 3}, {4, 5}, {0, 6}, {1, 2}, {3, 4}, {5, 6}};
+  *tap = t + tap_of[s][h];
+  *chunk = ch_of[s][h];
+}
+
 // Geometry + channel bookkeeping, passed by value to kernels.
 struct Geom {
   int N, U, NU, S, T, B, comb, K;
