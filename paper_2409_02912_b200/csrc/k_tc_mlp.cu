@@ -252,8 +252,10 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
             float o[8];
             const int ch = c32 / 8 + c8;
             if constexpr (X3) {
+              float bb[8];
+              ld_shared_f8(smem_u32(s.sb0) + 32u * ch, bb);  // two LDS.128 (the bias chunk, broadcast)
 #pragma unroll
-              for (int e = 0; e < 8; ++e) o[e] = relu_f(fmaf(v[8 * c8 + e], dsc, s.sb0[8 * ch + e]));
+              for (int e = 0; e < 8; ++e) o[e] = relu_f(fmaf(v[8 * c8 + e], dsc, bb[e]));
               uint4 hi, lo;
               uint32_t bad = 0;
               split_chunk(o, hi, lo, bad);
@@ -342,11 +344,14 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
         tc_fence_before();
         mbar_arrive_relaxed(free_bar);
       }
+      float bb[16];
+      ld_shared_f8(smem_u32(s.sb1) + 4u * c16, bb);
+      ld_shared_f8(smem_u32(s.sb1) + 4u * c16 + 32u, bb + 8);
 #pragma unroll
       for (int u = 0; u < MSG_MAXU; ++u)
         if (u < U)
 #pragma unroll
-          for (int e = 0; e < 16; ++e) m[u][e] = X3 ? fmaf(m[u][e], dsc, s.sb1[c16 + e]) : m[u][e] + s.sb1[c16 + e];
+          for (int e = 0; e < 16; ++e) m[u][e] = X3 ? fmaf(m[u][e], dsc, bb[e]) : m[u][e] + bb[e];
 #pragma unroll
       for (int u = 0; u < MSG_MAXU; ++u) {
         if (u >= U) break;
