@@ -371,13 +371,26 @@ class Adam:
         c1 = 1.0 - self.beta1 ** self.t
         c2 = 1.0 - self.beta2 ** self.t
         with torch.no_grad():
-            for k in names:
+            names = list(names)
+            # the reference checks each gradient just before its update and raises at the
+            # first bad one (earlier parameters already updated, autodiff.py:509-515); the
+            # finiteness of all gradients is read back in one device sync instead of one per tensor
+            bad, why = len(names), None
+            for i, k in enumerate(names):
+                if params[k].grad is None:
+                    bad, why = i, f"missing gradient for parameter '{k}'"
+                    break
+            checked = [params[k].grad for k in names[:bad]]
+            if checked:
+                ok = torch.stack([torch.isfinite(g).all() for g in checked]).cpu().tolist()
+                if not all(ok):
+                    bad = ok.index(False)
+                    why = f"non-finite gradient for parameter '{names[bad]}'"
+            for i, k in enumerate(names):
+                if i == bad:
+                    raise ValueError(why)
                 p = params[k]
                 g = p.grad
-                if g is None:
-                    raise ValueError(f"missing gradient for parameter '{k}'")
-                if not torch.isfinite(g).all():
-                    raise ValueError(f"non-finite gradient for parameter '{k}'")
                 if k not in self.m:
                     self.m[k] = torch.zeros_like(p)
                     self.v[k] = torch.zeros_like(p)

@@ -56,3 +56,21 @@ def test_train_step_matches_reference(name):
         # Adam's first step moves every touched weight by ~lr * sign(g): compare the step itself
         step_ref, step_got = ref - w0[k], got[k] - w0[k]
         np.testing.assert_allclose(step_got, step_ref, rtol=1e-3, atol=1e-6, err_msg=k)
+
+
+def test_adam_gradient_checks_mirror_reference():
+    """adam_step (autodiff.py:497-525): parameters before the first missing /
+    non-finite gradient are updated, then ValueError names the parameter."""
+    import torch
+    from paper_2409_02912_b200.training import Adam
+    p = {k: torch.ones(3) for k in ("a", "b", "c")}
+    p["a"].grad = torch.ones(3)
+    p["b"].grad = torch.tensor([1.0, float("nan"), 1.0])
+    p["c"].grad = torch.ones(3)
+    with pytest.raises(ValueError, match="non-finite gradient for parameter 'b'"):
+        Adam(lr=0.1).step(p, ["a", "b", "c"])
+    assert not torch.equal(p["a"], torch.ones(3)) and torch.equal(p["b"], torch.ones(3))
+    assert torch.equal(p["c"], torch.ones(3))
+    p["b"].grad = None
+    with pytest.raises(ValueError, match="missing gradient for parameter 'b'"):
+        Adam(lr=0.1).step(p, ["a", "b", "c"])
