@@ -663,8 +663,7 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k
           }
         }
       }
-      const float pdt = (MODE != EPI_RELU && valid) ? sdt[t] : 0.f;
-      const float pdf = (MODE != EPI_RELU && valid) ? pos_df(s, cslab % g.U, g) : 0.f;
+      const uint32_t vmask = valid ? 0xffffffffu : 0u;
 #pragma unroll
       for (int c8 = 0; c8 < NC / 8; ++c8) {
         const int cc = cbase / 8 + c8;
@@ -672,7 +671,7 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k
         if (cc >= nd || 8 * cc >= NP) continue;         // past the buffer / the accumulator
         float bb[8], x[8], pz[8];
         ld_shared_f8(sbias_s + 32u * cc, bb);
-        const bool full = 8 * cc + 8 <= g.d;
+        const bool full = 8 * cc + 8 <= g.d;  // warp-uniform
 #pragma unroll
         for (int e = 0; e < 8; ++e) pz[e] = 0.f;
         if constexpr (POSF) {
@@ -695,15 +694,33 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k
           float y = POSF ? __fadd_rn(fmaf(v[8 * c8 + e], descale, pz[e]), bb[e]) : fmaf(v[8 * c8 + e], descale, bb[e]);
           if (MODE == EPI_RELU) y = relu_f(y);
           if (MODE == EPI_RESIDUAL) y = old[8 * c8 + e] + y;
-          x[e] = (valid && (full || 8 * cc + e < g.d)) ? y : 0.f;
+          x[e] = y;
         }
-        if (MODE != EPI_RELU && !full) {
+        if (full) {  // every channel of the chunk is a state channel: pad rows zeroed on the packed words
+          if constexpr (SPLIT) {
+            uint4 hi, lo;
+            split_chunk(x, hi, lo);
+            hi = mask_chunk(hi, vmask);
+            lo = mask_chunk(lo, vmask);
+            const uint32_t h[4] = {hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int c = 8 * cc + e;
-            if (valid && c == g.d) x[e] = pdt;
-            if (valid && c == g.d + 1) x[e] = pdf;
+            for (int i = 0; i < 4; ++i) bad |= ((h[i] & 0x7c007c00u) + 0x04000400u) & 0x80008000u;  // as split_chunk
+            *reinterpret_cast<uint4*>(drow + cc * dcs) = hi;
+            *reinterpret_cast<uint4*>(drow + (nd + cc) * dcs) = lo;
+          } else {
+            *reinterpret_cast<uint4*>(drow + cc * dcs) = mask_chunk(pack_chunk(x, static_cast<const ET*>(nullptr)), vmask);
           }
+          continue;
+        }
+        // the chunk holding channel d (and the positional channels d, d+1 of the state)
+        const float pdt = (MODE != EPI_RELU && valid) ? sdt[t] : 0.f;
+        const float pdf = (MODE != EPI_RELU && valid) ? pos_df(s, cslab % g.U, g) : 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int c = 8 * cc + e;
+          x[e] = (valid && c < g.d) ? x[e] : 0.f;
+          if (MODE != EPI_RELU && valid && c == g.d) x[e] = pdt;
+          if (MODE != EPI_RELU && valid && c == g.d + 1) x[e] = pdf;
         }
         if constexpr (SPLIT) {
           uint4 hi, lo;
