@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
         if (u < U)
 #pragma unroll
           for (int e = 0; e < 16; ++e) m[u][e] = X3 ? fmaf(m[u][e], dsc, bb[e]) : m[u][e] + bb[e];
+      const uint32_t vmask = valid ? 0xffffffffu : 0u;
 #pragma unroll
       for (int u = 0; u < MSG_MAXU; ++u) {
         if (u >= U) break;
@@ -359,6 +360,7 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
         for (int h2 = 0; h2 < 2; ++h2) {
           const int c8 = c16 / 8 + h2;
           if (c8 >= nca) break;
+          const bool full = 8 * c8 + 8 <= g.d;  // warp-uniform: no per-channel select
           float o[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
@@ -366,17 +368,23 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
 #pragma unroll
             for (int v = 0; v < MSG_MAXU; ++v)
               if (v < U && v != u) a += m[v][8 * h2 + e];
-            const int c = 8 * c8 + e;
-            o[e] = (valid && c < g.d) ? a : 0.f;
+            o[e] = full || 8 * c8 + e < g.d ? a : 0.f;
           }
-          if constexpr (X3) {  // [hi | lo] planes of the aggregate
+          if constexpr (X3) {  // [hi | lo] planes of the aggregate, pad rows zeroed on the packed words
             uint4 hi, lo;
+            split_chunk(o, hi, lo);
+            hi = mask_chunk(hi, vmask);
+            lo = mask_chunk(lo, vmask);
             uint32_t bad = 0;
-            split_chunk(o, hi, lo, bad);
+            const uint32_t hw[4] = {hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) bad |= ((hw[i] & 0x7c007c00u) + 0x04000400u) & 0x80008000u;  // as split_chunk
             report_range(bad, g.flag);
             *reinterpret_cast<uint4*>(chunk_ptr(agg, n * U + u, 2 * nca, c8, row, g)) = hi;
             *reinterpret_cast<uint4*>(chunk_ptr(agg, n * U + u, 2 * nca, nca + c8, row, g)) = lo;
           } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = valid ? o[e] : 0.f;
             store_chunk(chunk_ptr(agg, n * U + u, nca, c8, row, g), o);
           }
         }
@@ -396,19 +404,22 @@ __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
   const float dsc = X3 ? s.sb1[p.op] : 1.f;
   mlp_body<ET, READOUT_HW, X3>(p, s, io, &smap, [&](int slab, int tile, int r, uint32_t taddr, uint64_t* free_bar,
                                                     int, int) {
-    float o[32];
+    // columns 0-7 LLRs, 8 .. 8+2B-1 the chest (2B <= 16): the first 24 of the 32-wide block
+    float o[24], bb[24];
     tmem_ld16(taddr, o);
-    tmem_ld16(taddr + 16, o + 16);
+    tmem_ld8(taddr + 16, o + 16);
     tmem_wait_ld();
     tc_fence_before();
     mbar_arrive_relaxed(free_bar);
     const int row = tile * NRX_TILE_M + r;
     const int srow = row / g.Tp, t = row - srow * g.Tp;
     if (row >= g.rows_data || t >= g.T) return;
+#pragma unroll
+    for (int c8 = 0; c8 < 3; ++c8) ld_shared_f8(smem_u32(s.sb1) + 32u * c8, bb + 8 * c8);
     uint32_t bad = 0;
 #pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      o[c] = X3 ? fmaf(o[c], dsc, s.sb1[c]) : o[c] + s.sb1[c];
+    for (int c = 0; c < 24; ++c) {
+      o[c] = X3 ? fmaf(o[c], dsc, bb[c]) : o[c] + bb[c];
       bad |= (__float_as_uint(o[c]) & 0x7f800000u) == 0x7f800000u;
     }
     if (bad && g.flag) atomicOr(g.flag, 1u);  // range guard (nrx_forward)
