@@ -216,14 +216,17 @@ __host__ __device__ inline ConvX3Smem conv_x3_smem(const ConvX3Params& p) {
 }
 
 // Epilogue columns per thread: 32 (2 + 4 np/32 warps, so each SM sub-partition
-// holds <= 3 warps and the fully unrolled MMA issue gets up to 168 registers);
-// the residual update, whose epilogue also reads the previous state and is
-// the bottleneck of that layer, runs twice the warps (16 columns each).
+// holds <= 3 warps and the fully unrolled MMA issue gets up to 168 registers)
+// for update.conv0; the layers whose epilogue is the bottleneck run twice the
+// warps (16 columns each).
 // Layers with at most two K=16 steps per tap (state_init.conv0: 19 -> 32
 // feature channels) issue few MMAs per tile, so their epilogue is the long
 // pole: 16 columns per thread (twice the warps) there too.
 __host__ __device__ constexpr int x3_epi_cols(int mode, bool small_k = false) {
-  return small_k || mode == EPI_RESIDUAL ? 16 : 32;  // (24 for the residual update: 0.60 -> 0.65 ms)
+  // the state-writing layers (state init, residual update) drain with twice the
+  // warps: state_init.conv1 0.50 -> 0.44 ms once the epilogue's full-chunk fast
+  // path made the 18-warp (96-register) configuration cheap enough
+  return small_k || mode != EPI_RELU ? 16 : 32;
 }
 // NC accumulator columns of this thread's lane (x16 loads, x8 for a remainder)
 template <int NC>
