@@ -109,7 +109,10 @@ __device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int 
 
 // Producer / MMA / hidden-epilogue roles are identical for both MLPs; the
 // output epilogue is passed in as a functor.
-template <typename ET, int HW, bool X3, int OW = 4, typename OutEpilogue>
+// NK0 / NK1 > 0: the K=16 step counts of fc0 / fc1 at compile time (fp32x3
+// issue unrolled for exactly that size; the runtime switch over every size
+// otherwise makes the kernel's code outgrow the instruction cache).
+template <typename ET, int HW, bool X3, int OW = 4, int NK0 = 0, int NK1 = 0, typename OutEpilogue>
 __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int io, const CUtensorMap* amap,
                                          OutEpilogue&& out_epi) {
   const Geom& g = p.g;
@@ -162,8 +165,11 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
         const uint32_t d = tmem_base + p.col_h + (jj & 1) * p.hp;
         uint64_t ad = smem_desc(as, NRX_TILE_M * 16, 128), bd = smem_desc(w0s, p.hp * 16, 128);
         if constexpr (X3) {
-          mma_x3_gemm(d, ad, (p.cs / 8) * NRX_TILE_M, 2 * NRX_TILE_M, bd, (p.cs / 8) * p.hp, 2 * p.hp, p.cs / 16,
-                      id0);
+          if constexpr (NK0 > 0)
+            mma_x3_gemm_t<NK0>(d, ad, (p.cs / 8) * NRX_TILE_M, 2 * NRX_TILE_M, bd, (p.cs / 8) * p.hp, 2 * p.hp, id0);
+          else
+            mma_x3_gemm(d, ad, (p.cs / 8) * NRX_TILE_M, 2 * NRX_TILE_M, bd, (p.cs / 8) * p.hp, 2 * p.hp, p.cs / 16,
+                        id0);
         } else {
           for (int kc = 0; kc < p.cs / 8; kc += 2) {
             mma_bf16_warp(d, ad, bd, id0, kc != 0);
@@ -199,8 +205,11 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
           const uint32_t d = tmem_base + p.col_o + (item & 1) * (U * p.op) + u * p.op;
           uint64_t ad = smem_desc(hs, NRX_TILE_M * 16, 128), bd = smem_desc(w1s, p.op * 16, 128);
           if constexpr (X3) {
-            mma_x3_gemm(d, ad, (p.hp / 8) * NRX_TILE_M, 2 * NRX_TILE_M, bd, (p.hp / 8) * p.op, 2 * p.op, p.hp / 16,
-                        id1);
+            if constexpr (NK1 > 0)
+              mma_x3_gemm_t<NK1>(d, ad, (p.hp / 8) * NRX_TILE_M, 2 * NRX_TILE_M, bd, (p.hp / 8) * p.op, 2 * p.op, id1);
+            else
+              mma_x3_gemm(d, ad, (p.hp / 8) * NRX_TILE_M, 2 * NRX_TILE_M, bd, (p.hp / 8) * p.op, 2 * p.op,
+                          p.hp / 16, id1);
           } else {
             for (int kc = 0; kc < p.hp / 8; kc += 2) {
               mma_bf16_warp(d, ad, bd, id1, kc != 0);
@@ -305,18 +314,20 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
   }
 }
 
-template <typename ET, bool X3>
+// UT > 0: the number of UEs at compile time (the 2-UE slots of the benchmark)
+template <typename ET, bool X3, int NK = 0, int UT = 0>
 __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
     k_msg_tc(const __grid_constant__ MlpTcParams p, const __grid_constant__ CUtensorMap smap) {
   extern __shared__ __align__(1024) uint8_t smem[];
   MlpSmem s(smem, p);
   mlp_setup(p, s, 0, 32 * MSG_HW, 32 * MSG_OW);
   const Geom& g = p.g;
-  const int U = p.uses_per_item;
+  const int U = UT > 0 ? UT : p.uses_per_item;
+  constexpr int UMAX = UT > 0 ? UT : MSG_MAXU;
   const int nca = g.Ca / 8;
   ET* const agg = static_cast<ET*>(p.agg);
   const float dsc = X3 ? s.sb1[p.op] : 1.f;
-  mlp_body<ET, MSG_HW, X3, MSG_OW>(p, s, 0, &smap, [&](int n, int tile, int r, uint32_t taddr, uint64_t* free_bar,
+  mlp_body<ET, MSG_HW, X3, MSG_OW, NK, NK>(p, s, 0, &smap, [&](int n, int tile, int r, uint32_t taddr, uint64_t* free_bar,
                                                        int grp, int ngrp) {
     const int row = tile * NRX_TILE_M + r;
     const int srow = row / g.Tp, t = row - srow * g.Tp;
@@ -335,9 +346,9 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
     }
     const int cspan = p.op / ng;
     for (int c16 = grp * cspan; c16 < (grp + 1) * cspan; c16 += 16) {
-      float m[MSG_MAXU][16];
+      float m[UMAX][16];
 #pragma unroll
-      for (int u = 0; u < MSG_MAXU; ++u)
+      for (int u = 0; u < UMAX; ++u)
         if (u < U) tmem_ld16(taddr + u * p.op + c16, m[u]);
       tmem_wait_ld();
       if (c16 + 16 >= (grp + 1) * cspan) {  // this group's messages are in registers: release TMEM
@@ -348,13 +359,13 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
       ld_shared_f8(smem_u32(s.sb1) + 4u * c16, bb);
       ld_shared_f8(smem_u32(s.sb1) + 4u * c16 + 32u, bb + 8);
 #pragma unroll
-      for (int u = 0; u < MSG_MAXU; ++u)
+      for (int u = 0; u < UMAX; ++u)
         if (u < U)
 #pragma unroll
           for (int e = 0; e < 16; ++e) m[u][e] = X3 ? fmaf(m[u][e], dsc, bb[e]) : m[u][e] + bb[e];
       const uint32_t vmask = valid ? 0xffffffffu : 0u;
 #pragma unroll
-      for (int u = 0; u < MSG_MAXU; ++u) {
+      for (int u = 0; u < UMAX; ++u) {
         if (u >= U) break;
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
@@ -366,7 +377,7 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
           for (int e = 0; e < 8; ++e) {
             float a = 0.f;
 #pragma unroll
-            for (int v = 0; v < MSG_MAXU; ++v)
+            for (int v = 0; v < UMAX; ++v)
               if (v < U && v != u) a += m[v][8 * h2 + e];
             o[e] = full || 8 * c8 + e < g.d ? a : 0.f;
           }
@@ -393,7 +404,7 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
   });
 }
 
-template <typename ET, bool X3>
+template <typename ET, bool X3, int NK0 = 0, int NK1 = 0>
 __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
     k_readout_tc(const __grid_constant__ MlpTcParams p, const __grid_constant__ CUtensorMap smap) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -402,7 +413,7 @@ __global__ void __launch_bounds__(mlp_threads(READOUT_HW), 1)
   mlp_setup(p, s, io, 32 * READOUT_HW);
   const Geom& g = p.g;
   const float dsc = X3 ? s.sb1[p.op] : 1.f;
-  mlp_body<ET, READOUT_HW, X3>(p, s, io, &smap, [&](int slab, int tile, int r, uint32_t taddr, uint64_t* free_bar,
+  mlp_body<ET, READOUT_HW, X3, 4, NK0, NK1>(p, s, io, &smap, [&](int slab, int tile, int r, uint32_t taddr, uint64_t* free_bar,
                                                     int, int) {
     // columns 0-7 LLRs, 8 .. 8+2B-1 the chest (2B <= 16): the first 24 of the 32-wide block
     float o[24], bb[24];
@@ -510,7 +521,10 @@ int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const void
   CUtensorMap m;
   rc = make_map(&m, state, g, g.prec == NRX_FP32X3 ? 2 * g.Cs : g.Cs, NRX_TILE_M);
   if (rc) return rc;
-  const auto fn = g.prec == NRX_FP32X3 ? k_msg_tc<__half, true>
+  // fp32x3 RT shapes (64-channel state and hidden, 2 UEs): compile-time sizes keep the code in the icache
+  const bool rt = g.prec == NRX_FP32X3 && g.Cs == 64 && p.hp == 64 && g.U == 2;
+  const auto fn = rt ? k_msg_tc<__half, true, 4, 2>
+                  : g.prec == NRX_FP32X3 ? k_msg_tc<__half, true>
                   : g.prec == NRX_FP16 ? k_msg_tc<__half, false>
                                        : k_msg_tc<__nv_bfloat16, false>;
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
@@ -543,7 +557,9 @@ int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const 
   CUtensorMap m;
   rc = make_map(&m, state, g, g.prec == NRX_FP32X3 ? 2 * g.Cs : g.Cs, NRX_TILE_M);
   if (rc) return rc;
-  const auto fn = g.prec == NRX_FP32X3 ? k_readout_tc<__half, true>
+  const bool rt = g.prec == NRX_FP32X3 && g.Cs == 64 && p.hp == 128;
+  const auto fn = rt ? k_readout_tc<__half, true, 4, 8>
+                  : g.prec == NRX_FP32X3 ? k_readout_tc<__half, true>
                   : g.prec == NRX_FP16 ? k_readout_tc<__half, false>
                                        : k_readout_tc<__nv_bfloat16, false>;
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
