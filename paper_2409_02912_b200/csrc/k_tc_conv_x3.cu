@@ -736,12 +736,16 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k
       }
       report_range(bad, g.flag);
       if (part == PARTS - 1) {  // buffer channels beyond the accumulator: positional / zero only
+        const float qdt = (valid && MODE != EPI_RELU) ? sdt[t] : 0.f;
+        const float qdf = (valid && MODE != EPI_RELU && MODE != EPI_RESIDUAL) ? pos_df(s, cslab % g.U, g) : 0.f;
         for (int cc = NP / 8; cc < nd; ++cc) {
           if (MODE == EPI_RESIDUAL) break;  // written once by the state init
           float o[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            o[e] = (valid && MODE != EPI_RELU) ? state_extra(8 * cc + e, s, t, cslab % g.U, g) : 0.f;
+          for (int e = 0; e < 8; ++e) {
+            const int c = 8 * cc + e;
+            o[e] = c == g.d ? qdt : c == g.d + 1 ? qdf : 0.f;
+          }
           if constexpr (SPLIT) {
             uint4 hi, lo;
             split_chunk(o, hi, lo);

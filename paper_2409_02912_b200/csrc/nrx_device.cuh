@@ -20,7 +20,7 @@ __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepc
 // Distance from subcarrier s to the nearest comb subcarrier of UE u
 // (positional_encoding, nrx.py:165-167).
 __device__ __forceinline__ int comb_dist(int s, int u, const Geom& g) {
-  const int o = u < g.comb ? u : u % g.comb;
+  const int o = u;  // the UE's comb offset: u < U <= comb (validate(), slot.py:60)
   if (s <= o) return o - s;
   const int q = g.comb == 1 ? s - o : (int)__umulhi((unsigned)(s - o), g.comb_magic);  // exact (make_geom)
   const int lo = o + q * g.comb;
@@ -35,10 +35,13 @@ __device__ __forceinline__ int comb_dist(int s, int u, const Geom& g) {
 // identical: the float64 quotient can never fall on (or across) a float32
 // rounding midpoint, since any midpoint differs from a/b by >= 1/(b 2^k)
 // while the float64 error is < 2^-28 / 2^k.
+// combs wider than 16 (not in any reference configuration): an out-of-line
+// IEEE division instead of the table, kept out of the unrolled epilogues
+static __device__ __noinline__ float df_div(int k, int S) { return __fdiv_rn((float)k, (float)S); }
 __device__ __forceinline__ float pos_df(int s, int u, const Geom& g) {
   if (!g.freq_enc) return 0.f;
   const int k = comb_dist(s, u, g);  // < comb
-  return g.comb <= 16 ? g.df_tab[k] : __fdiv_rn((float)k, (float)g.S);
+  return g.comb <= 16 ? g.df_tab[k] : df_div(k, g.S);
 }
 
 // Value a producer writes into state channel c >= d (pos encoding / zero).
