@@ -478,6 +478,13 @@ def run_ours(args):
                      "executed_vs_bf16_sustained": round(executed_flops(args.precision, B) / kavg / 1e12
                                                          / peaks.get("bf16_tflops_sustained", 1375.3), 4)
                      if kernel_ms and args.precision != "fp32_simt" else None,
+                     "executed_vs_clock_peak": (
+                         round(executed_flops(args.precision, B) / kavg
+                               / (148 * 8192 * sampler.summary()["sm_mhz"] * 1e6), 4)
+                         if kernel_ms and args.precision != "fp32_simt" and sampler.summary()["sm_mhz"] else None),
+                     "clock_peak_note": "dense fp16 tensor rate at the timed region's median SM clock: 148 SMs x "
+                                        "8192 FLOP/cycle (one 128x112x16 MMA per 56 cycles per SM, the floor "
+                                        "update.conv0 reaches)",
                      "share_of_step": round(kavg * 1e3 * N_IT / ms_per_step, 4) if kernel_ms else None},
         "whole_path": {"algorithmic_tflops": round(algorithmic_flops_per_slab_re() * U * S * T * value / world / 1e12, 2),
                        "flop_per_slot": algorithmic_flops_per_slab_re() * U * S * T},
