@@ -181,6 +181,7 @@ struct ConvX3Params {
   int cdst, stages, n_io, src1_xor, hup;
   int posf, kc;      // positional channels folded out (upd0_posf): both sources' kc chunks share one stage
   int ptab;          // posf: per-(comb residue, symbol) table of the positional contribution in shared memory
+  int hskip;         // RELU layer writing h for a tap-pair conv1: its zero chunks beyond d are never read
   uint32_t wbytes;   // one rank's weight block: [hi | lo][taps*ktap/8][np/2][8] fp16
   uint32_t abytes, tmem_cols, rbox;
   const uint8_t* wbase;
@@ -740,6 +741,7 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k
         const float qdf = (valid && MODE != EPI_RELU && MODE != EPI_RESIDUAL) ? pos_df(s, cslab % g.U, g) : 0.f;
         for (int cc = NP / 8; cc < nd; ++cc) {
           if (MODE == EPI_RESIDUAL) break;  // written once by the state init
+          if (MODE == EPI_RELU && p.hskip) break;  // h for a tap-pair conv1, which reads 7 chunks only
           float o[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
@@ -855,6 +857,7 @@ int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, cons
   p.hup = rup(g.H, 16);
   p.rbox = NRX_TILE_M + 2 * p.hup;
   p.posf = c.posf ? 1 : 0;
+  p.hskip = split && c.mode == EPI_RELU && tp2_layer(g.d, g.ks, c.prec) && c.cdst == g.Ch ? 1 : 0;
   p.kc = g.d / 8;
   if (c.posf && (g.d % 8 || !c.c1)) return NRX_ERR_UNSUPPORTED;
   const int ktap = c.posf ? 2 * g.d : c.c0 + c.c1;

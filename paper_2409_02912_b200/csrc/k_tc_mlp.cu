@@ -46,6 +46,8 @@ struct MlpTcParams {
   uint64_t w0[NRX_MAX_IO], b0[NRX_MAX_IO], w1[NRX_MAX_IO], b1[NRX_MAX_IO];
   const int32_t* mod_order;
   void* agg;               // message MLP output (bf16 / fp16 = kernel's ET)
+  int agg_skip;            // fp32x3 with the positional fold (upd0_posf): update.conv0 loads the d/8
+                           // chunks of the aggregate only, so its zero chunks beyond d are not written
   float* llr;              // readout outputs
   float2* chest;
 };
@@ -325,6 +327,7 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
   const int U = UT > 0 ? UT : p.uses_per_item;
   constexpr int UMAX = UT > 0 ? UT : MSG_MAXU;
   const int nca = g.Ca / 8;
+  const bool agg_skip = X3 && p.agg_skip;
   ET* const agg = static_cast<ET*>(p.agg);
   const float dsc = X3 ? s.sb1[p.op] : 1.f;
   mlp_body<ET, MSG_HW, X3, MSG_OW, NK, NK>(p, s, 0, &smap, [&](int n, int tile, int r, uint32_t taddr, uint64_t* free_bar,
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
           const int c8 = c16 / 8 + h2;
-          if (c8 >= nca) break;
+          if (c8 >= nca || (X3 && agg_skip && 8 * c8 >= g.d)) break;  // posf update.conv0 reads d channels
           const bool full = 8 * c8 + 8 <= g.d;  // warp-uniform: no per-channel select
           float o[8];
 #pragma unroll
@@ -518,6 +521,7 @@ int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const void
   p.w1[0] = L.msg.w1;
   p.b1[0] = L.msg.b1;
   p.agg = agg;
+  p.agg_skip = g.prec == NRX_FP32X3 && upd0_posf(g.d, g.ks, NRX_FP32X3) && g.d % 8 == 0;
   CUtensorMap m;
   rc = make_map(&m, state, g, g.prec == NRX_FP32X3 ? 2 * g.Cs : g.Cs, NRX_TILE_M);
   if (rc) return rc;
