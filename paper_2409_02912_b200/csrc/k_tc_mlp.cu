@@ -41,6 +41,8 @@ struct MlpTcParams {
   int n_io;
   uint32_t w0bytes, w1bytes, abytes, hbytes, tmem_cols;
   int astages, nhb;        // A ring stages, hidden shared-memory buffers (1 or 2)
+  int akc;                 // fp32x3: state chunks loaded per plane (d/8 < cs/8: the positional chunk,
+                           // whose weights are zero, stays a zeroed shared-memory chunk), else 0
   uint32_t col_h, col_o;   // TMEM column of hidden buffer 0 / output region 0
   const uint8_t* wbase;
   uint64_t w0[NRX_MAX_IO], b0[NRX_MAX_IO], w1[NRX_MAX_IO], b1[NRX_MAX_IO];
@@ -103,6 +105,15 @@ __device__ __forceinline__ void mlp_setup(const MlpTcParams& p, MlpSmem& s, int 
   // fp32x3 blobs store the descale 2^-E right after each bias vector
   const bool x3 = p.g.prec == NRX_FP32X3;
   for (int i = threadIdx.x; i <= p.hp; i += blockDim.x) s.sb0[i] = i < p.hp || x3 ? b0[i] : 1.f;
+  if (x3 && p.akc) {  // the A chunks no TMA writes (beyond akc in each plane): zero once, read by the K steps
+    const int skip = p.cs / 8 - p.akc, per = skip * NRX_TILE_M * 4;  // uint4 per plane and stage
+    for (int i = threadIdx.x; i < p.astages * 2 * per; i += blockDim.x) {
+      const int st = i / (2 * per), pl = (i / per) & 1, j = i % per;
+      const size_t off = (size_t)st * p.abytes + ((size_t)(pl * (p.cs / 8) + p.akc) * NRX_TILE_M) * 16 + 16 * (size_t)j;
+      *reinterpret_cast<uint4*>(s.As + off) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    fence_proxy_async();  // generic-proxy zeros -> tensor-core reads
+  }
   for (int i = threadIdx.x; i <= p.op; i += blockDim.x) s.sb1[i] = i < p.op || x3 ? b1[i] : 1.f;
   tc_fence_before();
   __syncthreads();
@@ -140,9 +151,16 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
           NRX_T(t0);
           mbar_wait(&s.aempty[st], ph ^ 1);
           NRX_TADD(t_a, t0);
-          mbar_expect_tx(&s.afull[st], p.abytes);
-          tma_load_4d(s.As + (size_t)st * p.abytes, amap, &s.afull[st], 0, tile * (NRX_TILE_M / 16), 0,
-                      unit * U + u);
+          uint8_t* dst = s.As + (size_t)st * p.abytes;
+          if (X3 && p.akc) {  // hi chunks [0, akc) and lo chunks [cs/8, cs/8 + akc)
+            mbar_expect_tx(&s.afull[st], 2u * p.akc * NRX_TILE_M * 16);
+            tma_load_4d(dst, amap, &s.afull[st], 0, tile * (NRX_TILE_M / 16), 0, unit * U + u);
+            tma_load_4d(dst + (size_t)(p.cs / 8) * NRX_TILE_M * 16, amap, &s.afull[st], 0, tile * (NRX_TILE_M / 16),
+                        p.cs / 8, unit * U + u);
+          } else {
+            mbar_expect_tx(&s.afull[st], p.abytes);
+            tma_load_4d(dst, amap, &s.afull[st], 0, tile * (NRX_TILE_M / 16), 0, unit * U + u);
+          }
           if (++st == p.astages) { st = 0; ph ^= 1; }
         }
       }
@@ -523,7 +541,8 @@ int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const void
   p.agg = agg;
   p.agg_skip = g.prec == NRX_FP32X3 && upd0_posf(g.d, g.ks, NRX_FP32X3) && g.d % 8 == 0;
   CUtensorMap m;
-  rc = make_map(&m, state, g, g.prec == NRX_FP32X3 ? 2 * g.Cs : g.Cs, NRX_TILE_M);
+  p.akc = g.prec == NRX_FP32X3 && g.d % 8 == 0 && g.d / 8 < g.Cs / 8 ? g.d / 8 : 0;
+  rc = make_map(&m, state, g, g.prec == NRX_FP32X3 ? 2 * g.Cs : g.Cs, NRX_TILE_M, p.akc);
   if (rc) return rc;
   // fp32x3 RT shapes (64-channel state and hidden, 2 UEs): compile-time sizes keep the code in the icache
   const bool rt = g.prec == NRX_FP32X3 && g.Cs == 64 && p.hp == 64 && g.U == 2;
@@ -559,7 +578,8 @@ int launch_readout(const Geom& g, const PackLayout& L, const uint8_t* wb, const 
   p.llr = llr;
   p.chest = chest;
   CUtensorMap m;
-  rc = make_map(&m, state, g, g.prec == NRX_FP32X3 ? 2 * g.Cs : g.Cs, NRX_TILE_M);
+  p.akc = g.prec == NRX_FP32X3 && g.d % 8 == 0 && g.d / 8 < g.Cs / 8 ? g.d / 8 : 0;
+  rc = make_map(&m, state, g, g.prec == NRX_FP32X3 ? 2 * g.Cs : g.Cs, NRX_TILE_M, p.akc);
   if (rc) return rc;
   const bool rt = g.prec == NRX_FP32X3 && g.Cs == 64 && p.hp == 128;
   const auto fn = rt ? k_readout_tc<__half, true, 4, 8>
