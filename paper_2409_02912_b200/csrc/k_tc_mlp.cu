@@ -270,6 +270,30 @@ __device__ __forceinline__ void mlp_body(const MlpTcParams& p, MlpSmem& s, int i
         NRX_T(t2);
         uint8_t* H = s.Hs + (size_t)hb * p.hbytes;
         const float dsc = X3 ? s.sb0[p.hp] : 1.f;
+        if constexpr (X3 && NK1 > 0 && 16 * NK1 / (HW / 4) <= 64) {
+          // compile-time hidden width (hp = 16 NK1): this thread's columns in one TMEM
+          // round trip (every 16-column load issued before the single wait), fully unrolled
+          constexpr int CSPAN = 16 * NK1 / (HW / 4);
+          float v[CSPAN];
+#pragma unroll
+          for (int b16 = 0; b16 < CSPAN / 16; ++b16)
+            tmem_ld16(tmem_base + lane_off + p.col_h + ab * p.hp + cbeg + 16 * b16, v + 16 * b16);
+          tmem_wait_ld();
+          uint32_t bad = 0;
+#pragma unroll
+          for (int c8 = 0; c8 < CSPAN / 8; ++c8) {
+            const int ch = cbeg / 8 + c8;
+            float o[8], bb[8];
+            ld_shared_f8(smem_u32(s.sb0) + 32u * ch, bb);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = relu_f(fmaf(v[8 * c8 + e], dsc, bb[e]));
+            uint4 hi, lo;
+            split_chunk(o, hi, lo, bad);
+            *reinterpret_cast<uint4*>(H + ((size_t)ch * NRX_TILE_M + r) * 16) = hi;
+            *reinterpret_cast<uint4*>(H + ((size_t)(16 * NK1 / 8 + ch) * NRX_TILE_M + r) * 16) = lo;
+          }
+          report_range(bad, g.flag);
+        } else
         for (int c32 = cbeg; c32 < cbeg + cspan; c32 += 32) {
           float v[32];
           tmem_ld16(tmem_base + lane_off + p.col_h + ab * p.hp + c32, v);
