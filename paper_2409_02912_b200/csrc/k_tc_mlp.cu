@@ -390,6 +390,59 @@ __global__ void __launch_bounds__(mlp_threads(MSG_HW, MSG_OW), 1)
       return;
     }
     const int cspan = p.op / ng;
+    if constexpr (X3 && UT > 0 && NK > 0) {
+      // the RT shape (op = 64, launch_msg): this group's UT x 32 message columns in one TMEM
+      // round trip, then the sums of the others, split, stored as the aggregate planes
+      constexpr int CS = 64 / (MSG_OW / 4);
+      static_assert(CS % 16 == 0, "column span");
+      const int c0 = grp * CS;
+      float m[UT][CS];
+#pragma unroll
+      for (int u = 0; u < UT; ++u)
+#pragma unroll
+        for (int b16 = 0; b16 < CS / 16; ++b16) tmem_ld16(taddr + u * 64 + c0 + 16 * b16, m[u] + 16 * b16);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive_relaxed(free_bar);
+      const uint32_t vmask = valid ? 0xffffffffu : 0u;
+      uint32_t bad = 0;
+#pragma unroll
+      for (int c8 = 0; c8 < CS / 8; ++c8) {
+        const int cc = c0 / 8 + c8;
+        if (cc >= nca || (agg_skip && 8 * cc >= g.d)) break;
+        const bool full = 8 * cc + 8 <= g.d;
+        float bb[8];
+        ld_shared_f8(smem_u32(s.sb1) + 32u * cc, bb);
+        float mb[UT][8];
+#pragma unroll
+        for (int u = 0; u < UT; ++u)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) mb[u][e] = fmaf(m[u][8 * c8 + e], dsc, bb[e]);
+#pragma unroll
+        for (int u = 0; u < UT; ++u) {
+          float o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            float a = 0.f;
+#pragma unroll
+            for (int v = 0; v < UT; ++v)
+              if (v != u) a += mb[v][e];
+            o[e] = full || 8 * cc + e < g.d ? a : 0.f;
+          }
+          uint4 hi, lo;
+          split_chunk(o, hi, lo);
+          hi = mask_chunk(hi, vmask);
+          lo = mask_chunk(lo, vmask);
+          const uint32_t hw[4] = {hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) bad |= ((hw[i] & 0x7c007c00u) + 0x04000400u) & 0x80008000u;  // as split_chunk
+          *reinterpret_cast<uint4*>(chunk_ptr(agg, n * UT + u, 2 * nca, cc, row, g)) = hi;
+          *reinterpret_cast<uint4*>(chunk_ptr(agg, n * UT + u, 2 * nca, nca + cc, row, g)) = lo;
+        }
+      }
+      report_range(bad, g.flag);
+      return;
+    }
     for (int c16 = grp * cspan; c16 < (grp + 1) * cspan; c16 += 16) {
       float m[UMAX][16];
 #pragma unroll
@@ -569,7 +622,7 @@ int launch_msg(const Geom& g, const PackLayout& L, const uint8_t* wb, const void
   rc = make_map(&m, state, g, g.prec == NRX_FP32X3 ? 2 * g.Cs : g.Cs, NRX_TILE_M, p.akc);
   if (rc) return rc;
   // fp32x3 RT shapes (64-channel state and hidden, 2 UEs): compile-time sizes keep the code in the icache
-  const bool rt = g.prec == NRX_FP32X3 && g.Cs == 64 && p.hp == 64 && g.U == 2;
+  const bool rt = g.prec == NRX_FP32X3 && g.Cs == 64 && p.hp == 64 && p.op == 64 && g.U == 2;
   const auto fn = rt ? k_msg_tc<__half, true, 4, 2>
                   : g.prec == NRX_FP32X3 ? k_msg_tc<__half, true>
                   : g.prec == NRX_FP16 ? k_msg_tc<__half, false>
