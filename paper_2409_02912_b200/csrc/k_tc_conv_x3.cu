@@ -612,14 +612,22 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k
       // two blocks per TMEM round trip
       tmem_ld_cols<NC>(taddr, v);
       if (!SPLIT) tmem_wait_ld();
-      if (SPLIT) {
+      if (SPLIT && NC <= 16 && KS > 1) {  // narrow threads: all four blocks in one TMEM round trip
+        float w2[NC], w3[NC], w4[NC];
+        tmem_ld_cols<NC>(taddr + NP, w2);
+        tmem_ld_cols<NC>(taddr + DST, w3);
+        tmem_ld_cols<NC>(taddr + DST + NP, w4);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v[c] = __fadd_rn(__fadd_rn(v[c], w2[c]), __fadd_rn(w3[c], w4[c]));
+      } else if (SPLIT) {
         float w2[NC];
         tmem_ld_cols<NC>(taddr + NP, w2);
         tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < NC; ++c) v[c] = __fadd_rn(v[c], w2[c]);
       }
-      if (SPLIT && P > 1) {
+      if (SPLIT && P > 1 && !(NC <= 16 && KS > 1)) {
         float w3[NC], w4[NC];
         tmem_ld_cols<NC>(taddr + DST, w3);
         tmem_ld_cols<NC>(taddr + DST + NP, w4);
