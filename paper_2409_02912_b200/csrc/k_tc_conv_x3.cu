@@ -257,10 +257,11 @@ __host__ __device__ constexpr bool x3_small_k(int ks, int nk0, int nk1) { return
 // fp32, before griddepcontrol.wait) and the epilogue adds one table row; edge
 // rows evaluate the 18 terms.
 //
-// TP2 (fp32x3 conv1 layers of d_s = 56, tp2_layer): the tap-pair K order of
-// nrx_internal.h (32 instead of 36 MMA steps per plane, 7 loaded chunks).
+// TPC (fp32x3 3x3 layers over C = TPC data chunks, tp2_chunks): the tap-pair
+// K order of nrx_internal.h -- 4 C + (C+1)/2 instead of 9 (C+1)/2 MMA steps per
+// plane (C = 7: 32 instead of 36; C = 3: 14 instead of 18), C loaded chunks.
 template <int NP, int MODE, int KS = 0, int NK0 = 0, int NK1 = 0, int PREC = NRX_FP32X3, bool POSF = false,
-          bool TP2 = false>
+          int TPC = 0>
 __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k(KS, NK0, NK1)) - 1) /
                                               x3_epi_cols(MODE, x3_small_k(KS, NK0, NK1))),
                                   1)
@@ -274,7 +275,8 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k
   constexpr int DST = SPLIT ? (NB + 31) / 32 * 32 : NB;  // TMEM columns per partial accumulator
   static_assert(SPLIT || MODE == EPI_RELU, "half-precision pair kernels: ReLU layers only");
   static_assert(!POSF || (KS == 3 && NK1 == 0 && MODE == EPI_RELU), "positional fold: 3x3 update.conv0 only");
-  static_assert(!TP2 || (KS == 3 && NK0 == 4 && NK1 == 0 && PREC == NRX_FP32X3 && !POSF), "tap pairs: 3x3 conv1");
+  static_assert(TPC == 0 || (KS == 3 && 2 * NK0 == TPC + 1 && NK1 == 0 && PREC == NRX_FP32X3 && !POSF),
+                "tap pairs: 3x3 layers over TPC data chunks of 2 NK0");
   // 32 accumulator columns per epilogue thread: 2 + 4 * NP/32 warps (10 for
   // NP = 64) leave each SM sub-partition <= 3 warps, i.e. up to 168 registers
   // for the fully unrolled MMA issue (18 warps would cap it at 96 and spill)
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k
             NRX_T(t0);
             mbar_wait_backoff(B_empty + 8u * st, ph ^ 1, 64);
             NRX_TADD(t_a, t0);
-            if (rank == 0) mbar_expect_tx(B_full + 8u * st, 2u * (uint32_t)(TP2 ? 56 : cs) * R * 2);
+            if (rank == 0) mbar_expect_tx(B_full + 8u * st, 2u * (uint32_t)(TPC ? 8 * TPC : cs) * R * 2);
             tma_load_4d_pair(As_s + st * p.abytes, src ? &map1 : &map0, full_leader + 8u * st, 0, grp0,
                              SPLIT && pl == 0 ? cs / 8 : 0, src ? (slab ^ p.src1_xor) : slab);
             if (++st == p.stages) { st = 0; ph ^= 1; }
@@ -440,7 +442,7 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k
         // Plane lo: D_ra = lo' [W_hi | W_lo] (scale 2^11, first MMA of each partial
         // overwrites); plane hi: the first MMA of each partial folds (D 2^-11 +),
         // the rest accumulate hi [W_hi | W_lo].
-        if constexpr (TP2) {
+        if constexpr (TPC > 0) {
           // tap-pair K order (tp2_slot): per plane pairs (0,1) (2,3) (4,5) (6,7) into
           // partials 0 1 0 1, then tap 8 into partial 0; step q reads B slots 2q, 2q+1
 #pragma unroll
@@ -458,25 +460,23 @@ __global__ void __launch_bounds__(64 + 128 * ((NP + x3_epi_cols(MODE, x3_small_k
                 mma2_warp(d, a, b, idesc, !(pl == 0 && first));
               ++q;
             };
+            constexpr int HALF = (TPC - 1) / 2;
 #pragma unroll
             for (int pr = 0; pr < 4; ++pr) {
               const int t = 2 * pr, u = t + 1, part = pr & 1;
               const uint64_t at = a_stage + shifts[t], au = a_stage + shifts[u];
-              // the straddling step: half 0 = (u, chunk 0), half 1 = (t, chunk 6)
-              const uint64_t lbo = (uint64_t)(uint32_t)(shifts[t] + 6 * R - shifts[u] - R) << 16;
-              step(at, part, pr < 2);
-              step(at + (uint32_t)(2 * R), part, false);
-              step(at + (uint32_t)(4 * R), part, false);
+              // the straddling step: half 0 = (u, chunk 0), half 1 = (t, chunk C-1)
+              const uint64_t lbo = (uint64_t)(uint32_t)(shifts[t] + (TPC - 1) * R - shifts[u] - R) << 16;
+#pragma unroll
+              for (int k = 0; k < HALF; ++k) step(at + (uint32_t)(2 * k * R), part, pr < 2 && k == 0);
               step(au + lbo, part, false);
-              step(au + (uint32_t)R, part, false);
-              step(au + (uint32_t)(3 * R), part, false);
-              step(au + (uint32_t)(5 * R), part, false);
+#pragma unroll
+              for (int k = 1; k <= HALF; ++k) step(au + (uint32_t)((2 * k - 1) * R), part, false);
             }
             const uint64_t a8 = a_stage + shifts[8];
-            step(a8, 0, false);
-            step(a8 + (uint32_t)(2 * R), 0, false);
-            step(a8 + (uint32_t)(4 * R), 0, false);
-            step(a8 + (uint32_t)(5 * R), 0, false);  // zero-weight slot over chunk 5, then chunk 6
+#pragma unroll
+            for (int k = 0; k < HALF; ++k) step(a8 + (uint32_t)(2 * k * R), 0, false);
+            step(a8 + (uint32_t)((TPC - 2) * R), 0, false);  // zero-weight slot over chunk C-2, then chunk C-1
             commit2_warp(B_empty + 8u * st);
             if (++st == p.stages) { st = 0; ph ^= 1; }
           }
@@ -824,9 +824,11 @@ static X3Fn select_conv_x3(const Geom& g, int mode, int c0, int c1, int prec, bo
     if (mode == EPI_RELU && nk0 == 4 && nk1 == 4) fn = k_conv_x3<56, EPI_RELU, 3, 4, 4>;
     const bool tp2 = tp2_layer(g.d, g.ks, prec);
     if (mode == EPI_STATE_INIT && nk0 == 4 && nk1 == 0)
-      fn = tp2 ? k_conv_x3<56, EPI_STATE_INIT, 3, 4, 0, NRX_FP32X3, false, true> : k_conv_x3<56, EPI_STATE_INIT, 3, 4, 0>;
+      fn = tp2 ? k_conv_x3<56, EPI_STATE_INIT, 3, 4, 0, NRX_FP32X3, false, 7> : k_conv_x3<56, EPI_STATE_INIT, 3, 4, 0>;
     if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0)
-      fn = tp2 ? k_conv_x3<56, EPI_RESIDUAL, 3, 4, 0, NRX_FP32X3, false, true> : k_conv_x3<56, EPI_RESIDUAL, 3, 4, 0>;
+      fn = tp2 ? k_conv_x3<56, EPI_RESIDUAL, 3, 4, 0, NRX_FP32X3, false, 7> : k_conv_x3<56, EPI_RESIDUAL, 3, 4, 0>;
+    if (mode == EPI_RELU && nk0 == 2 && nk1 == 0 && tp2_chunks(g.d, g.ks, prec, c0, g.Cin) == 3)
+      fn = k_conv_x3<56, EPI_RELU, 3, 2, 0, NRX_FP32X3, false, 3>, *small = true;
   }
   return fn;
 }
@@ -897,10 +899,14 @@ int launch_conv_x3(const Geom& g, const ConvX3Launch& c, const uint8_t* wb, cons
   CUtensorMap m0, m1;
   const void* s1 = c.src1 ? c.src1 : c.src0;
   const int cc1 = c.c1 ? c.c1 : c.c0;
-  // tap-pair conv1 layers load only the 7 chunks holding the 56 channels (the kernel's TP2 instance)
-  const bool tp2 = split && tp2_layer(g.d, g.ks, c.prec) && (c.mode == EPI_STATE_INIT || c.mode == EPI_RESIDUAL) &&
-                   c.c0 == 64 && c.c1 == 0 && !c.posf;
-  const int box0 = c.posf ? p.kc : tp2 ? 7 : c.c0 / 8, box1 = c.posf ? p.kc : cc1 / 8;
+  // tap-pair layers load only their C data chunks (the kernel's TPC instance): the conv1 layers of
+  // d_s = 56 (C = 7) and state_init.conv0 over the 19 feature channels (C = 3)
+  int tpc = 0;
+  if (split && !c.posf && c.c1 == 0) {
+    if ((c.mode == EPI_STATE_INIT || c.mode == EPI_RESIDUAL) && c.c0 == 64 && tp2_layer(g.d, g.ks, c.prec)) tpc = 7;
+    if (c.mode == EPI_RELU && tp2_chunks(g.d, g.ks, c.prec, c.c0, g.Cin) == 3 && c.c0 == g.Cf) tpc = 3;
+  }
+  const int box0 = c.posf ? p.kc : tpc ? tpc : c.c0 / 8, box1 = c.posf ? p.kc : cc1 / 8;
   int rc = split ? make_map_plane(&m0, c.src0, g, c.c0, p.rbox, box0) : make_map(&m0, c.src0, g, c.c0, p.rbox, box0);
   if (rc) return rc;
   rc = split ? make_map_plane(&m1, s1, g, cc1, p.rbox, box1) : make_map(&m1, s1, g, cc1, p.rbox, box1);

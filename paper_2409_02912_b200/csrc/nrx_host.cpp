@@ -433,18 +433,20 @@ void pack_conv_x3(const Geom& g, int k, const ConvOff& c, int cin_ref, const flo
   db[npx] = std::ldexp(1.f, -E);
 }
 
-// The same for a 56-channel conv1 in the tap-pair K order (tp2_slot); the
-// block keeps the taps x ktap size, its last 8 slots stay zero.
-void pack_conv_x3_tp2(const Geom& g, const ConvOff& c, const float* w, const float* b, uint8_t* base) {
-  const int npx = x3_np(g.d), taps = 9, cout = g.d, cin_ref = g.d;
+// The same in the tap-pair K order (tp2_slot) for an input of C data chunks
+// (cin_ref reference channels); the block keeps the taps x ktap size, the
+// unused slots at its end stay zero.
+void pack_conv_x3_tp2(const Geom& g, int C, const ConvOff& c, int cin_ref, const float* w, const float* b,
+                      uint8_t* base) {
+  const int npx = x3_np(g.d), taps = 9, cout = g.d;
   float mx = 0.f;
   for (size_t i = 0; i < (size_t)taps * cin_ref * cout; ++i) mx = std::fmax(mx, std::fabs(w[i]));
   const int E = split_exponent(mx);
   const size_t half = (size_t)taps * c.ktap * npx;
   SplitB B{(uint16_t*)(base + c.w), npx, half, std::ldexp(1.f, E)};
-  for (int slot = 0; slot < 2 * TP2_STEPS; ++slot) {
+  for (int slot = 0; slot < 2 * tp2_steps(C); ++slot) {
     int tap, ch;
-    tp2_slot(slot, &tap, &ch);
+    tp2_slot(C, slot, &tap, &ch);
     for (int j = 0; j < 8; ++j) {
       const int src = 8 * ch + j;
       for (int o = 0; o < npx; ++o)
@@ -502,9 +504,12 @@ int pack_weights_x3(const nrx_model_desc* m, const float* const* t, uint8_t* bas
   };
   for (int io = 0; io < m->n_io; ++io) {
     const int i = 8 * io;
-    pack_conv_x3(g, k, L.init0[io], g.Cin, t[i], t[i + 1], map_identity_feats, base);
+    if (tp2_chunks(d, k, NRX_FP32X3, g.Cf, g.Cin) == 3)  // the 19 feature channels: 3 data chunks of 4
+      pack_conv_x3_tp2(g, 3, L.init0[io], g.Cin, t[i], t[i + 1], base);
+    else
+      pack_conv_x3(g, k, L.init0[io], g.Cin, t[i], t[i + 1], map_identity_feats, base);
     if (tp2_layer(d, k, NRX_FP32X3))
-      pack_conv_x3_tp2(g, L.init1[io], t[i + 2], t[i + 3], base);
+      pack_conv_x3_tp2(g, 7, L.init1[io], d, t[i + 2], t[i + 3], base);
     else
       pack_conv_x3(g, k, L.init1[io], d, t[i + 2], t[i + 3], map_identity_hidden, base);
     const MlpOff& o = L.llr[io];
@@ -561,7 +566,7 @@ int pack_weights_x3(const nrx_model_desc* m, const float* const* t, uint8_t* bas
     pack_conv_x3(g, k, L.upd0, 2 * d + 2, t[i_upd], t[i_upd + 1], map_update, base);
   }
   if (tp2_layer(d, k, NRX_FP32X3))
-    pack_conv_x3_tp2(g, L.upd1, t[i_upd + 2], t[i_upd + 3], base);
+    pack_conv_x3_tp2(g, 7, L.upd1, d, t[i_upd + 2], t[i_upd + 3], base);
   else
     pack_conv_x3(g, k, L.upd1, d, t[i_upd + 2], t[i_upd + 3], map_identity_hidden, base);
   return NRX_OK;

@@ -57,32 +57,43 @@ inline bool upd0_posf(int d, int ks, int prec) {
 // float offset of the positional weights [channel dt, df][tap][np] in a conv bias block
 inline int posw_off(int np) { return np + 4; }
 
-// fp32x3 3x3 convolutions over a 56-channel input (state_init.conv1 and
-// iteration.update.conv1 of d_s = 56): 7 channel chunks per tap, so a K = 16
-// MMA step over one tap wastes the zero 8th chunk.  "Tap pairs" order the K
-// slots (8 channels each) so that one step straddles two taps: taps (t, t+1)
-// take 7 steps instead of 8 -- (t,0)(t,1) (t,2)(t,3) (t,4)(t,5) (t+1,0)(t,6)
-// (t+1,1)(t+1,2) (t+1,3)(t+1,4) (t+1,5)(t+1,6) -- for the pairs (0,1) (2,3) (4,5)
-// (6,7), then tap 8 alone in 4 steps: 32 MMA steps per plane instead of 36.
-// Only chunks 0-6 are loaded (the TMA box skips the zero chunk 7).
-// The straddling step's two 8-channel halves sit at different row offsets,
-// which its A descriptor's leading-byte offset expresses.
-inline bool tp2_layer(int d, int ks, int prec) { return prec == NRX_FP32X3 && ks == 3 && d == 56; }
-constexpr int TP2_STEPS = 32;
-inline void tp2_slot(int slot, int* tap, int* chunk) {  // half-slot (8 K values) -> (tap, channel chunk)
+// fp32x3 3x3 convolutions whose input has an odd number C of 8-channel chunks
+// holding data (C = 7: state_init.conv1 / update.conv1 of d_s = 56; C = 3: the
+// 19 feature channels of state_init.conv0): a per-tap K = 16 loop reads a zero
+// chunk per tap.  "Tap pairs" order the K slots (8 channels each) so that one
+// MMA step straddles two taps: taps (t, u = t+1) take C steps instead of C+1 --
+// (t,0)(t,1) .. (t,C-3)(t,C-2), then (u,0)(t,C-1), then (u,1)(u,2) .. (u,C-2)(u,C-1)
+// -- for the pairs (0,1) (2,3) (4,5) (6,7), then tap 8 alone in (C+1)/2 steps
+// whose last pairs a zero-weight slot (A: chunk C-2, which the TMA loads) with
+// chunk C-1.  The straddling step's second half sits at another row offset,
+// which its A descriptor's leading-byte offset expresses; only C chunks are loaded.
+inline int tp2_chunks(int d, int ks, int prec, int cin_buf, int cin) {  // C, or 0: not a tap-pair layer
+  if (prec != NRX_FP32X3 || ks != 3 || cin_buf % 16) return 0;
+  const int c = (cin + 7) / 8;
+  return (c % 2 == 1 && c + 1 == cin_buf / 8 && (c == 7 || c == 3) && d == 56) ? c : 0;
+}
+inline bool tp2_layer(int d, int ks, int prec) { return tp2_chunks(d, ks, prec, rup(d, 16), d) == 7; }
+inline int tp2_steps(int C) { return 4 * C + (C + 1) / 2; }
+inline void tp2_slot(int C, int slot, int* tap, int* chunk) {  // half-slot (8 K values) -> (tap, chunk)
   const int step = slot / 2, h = slot & 1;
-  if (step >= 28) {  // tap 8 alone; the last step pairs the zero-weight chunk 7 slot (its A half
-    *tap = 8;         // reads chunk 5, which the TMA does load) with chunk 6
-    *chunk = step == 31 ? (h ? 6 : 7) : 2 * (step - 28) + h;
+  if (step >= 4 * C) {  // tap 8 alone; the last step: zero-weight slot (chunk C, none) then chunk C-1
+    const int s = step - 4 * C;
+    *tap = 8;
+    *chunk = s == (C - 1) / 2 ? (h ? C - 1 : C) : 2 * s + h;
     return;
   }
-  const int pr = step / 7, s = step % 7, t = 2 * pr;
-  static const int tap_of[7][2] = {{0, 0}, {0, 0}, {0, 0}, {1, 0}, {1, 1}, {1, 1}, {1, 1}};
-  static const int ch_of[7][2] = {{0, 1}, {2, 3}, {4, 5}, {0, 6}, {1, 2}, {3, 4}, {5, 6}};
-  *tap = t + tap_of[s][h];
-  *chunk = ch_of[s][h];
+  const int pr = step / C, s = step % C, t = 2 * pr, half = (C - 1) / 2;
+  if (s < half) {
+    *tap = t;
+    *chunk = 2 * s + h;
+  } else if (s == half) {
+    *tap = h ? t : t + 1;
+    *chunk = h ? C - 1 : 0;
+  } else {
+    *tap = t + 1;
+    *chunk = 2 * (s - half) - 1 + h;
+  }
 }
-
 // Geometry + channel bookkeeping, passed by value to kernels.
 struct Geom {
   int N, U, NU, S, T, B, comb, K;
