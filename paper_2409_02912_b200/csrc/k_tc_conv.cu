@@ -106,7 +106,8 @@ __host__ __device__ inline ConvSmem conv_smem_layout(const ConvTcParams& p, int 
 // NK1 K=16 steps per tap from source 0 / 1 (host picks it when the layer
 // matches); KS = 0 is the generic runtime-loop version.
 // ET = __nv_bfloat16 or __half: operand/activation element type.
-template <typename ET, int NP, int MODE, int TAIL, int KS = 0, int NK0 = 0, int NK1 = 0>
+// TPC > 0: the tap-pair K order over TPC data chunks (tp2_chunks, nrx_internal.h).
+template <typename ET, int NP, int MODE, int TAIL, int KS = 0, int NK0 = 0, int NK1 = 0, int TPC = 0>
 __global__ void __launch_bounds__(conv_threads(NP), 1)
     k_conv_tc(const __grid_constant__ ConvTcParams p, const __grid_constant__ CUtensorMap map0,
               const __grid_constant__ CUtensorMap map1) {
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
           NRX_T(t0);
           mbar_wait(B_empty + 8u * (st), ph ^ 1);
           NRX_TADD(t_a, t0);
-          mbar_expect_tx(B_full + 8u * (st), (uint32_t)(src ? p.c1 : p.c0) * R * 2);
+          mbar_expect_tx(B_full + 8u * (st), (uint32_t)(TPC ? 8 * TPC : src ? p.c1 : p.c0) * R * 2);
           tma_load_4d(As_s + st * p.abytes, src ? &map1 : &map0, B_full + 8u * (st), 0, grp0, 0,
                       src ? (slab ^ p.src1_xor) : slab);
           if (++st == p.stages) { st = 0; ph ^= 1; }
@@ -280,7 +281,39 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       NRX_TADD(t_a, t0);
       tc_fence_after();
       const uint32_t d = tmem_base + acc * NP;
-      if constexpr (KS > 0) {
+      if constexpr (TPC > 0) {
+        // tap-pair K order: pairs (0,1) (2,3) (4,5) (6,7), then tap 8; the straddling
+        // step's second half through its descriptor's leading-byte offset
+        static_assert(KS == 3 && NK1 == 0 && 2 * NK0 == TPC + 1, "tap pairs: one source of TPC data chunks");
+        NRX_T(t1);
+        mbar_wait(B_full + 8u * (st), ph);
+        NRX_TADD(t_b, t1);
+        tc_fence_after();
+        const uint64_t a_stage = a_desc0 + (((As_s + st * p.abytes) >> 4) + p.hup);
+        int q = 0;
+        auto step = [&](uint64_t a) {
+          mma_bf16_warp(d, a, b_desc0 + (uint32_t)(2 * q * NP), idesc, q != 0);
+          ++q;
+        };
+        constexpr int HALF = (TPC - 1) / 2;
+#pragma unroll
+        for (int pr = 0; pr < 4; ++pr) {
+          const int t = 2 * pr, u = t + 1;
+          const uint64_t at = a_stage + shifts[t], au = a_stage + shifts[u];
+          const uint64_t lbo = (uint64_t)(uint32_t)(shifts[t] + (TPC - 1) * R - shifts[u] - R) << 16;
+#pragma unroll
+          for (int k = 0; k < HALF; ++k) step(at + (uint32_t)(2 * k * R));
+          step(au + lbo);
+#pragma unroll
+          for (int k = 1; k <= HALF; ++k) step(au + (uint32_t)((2 * k - 1) * R));
+        }
+        const uint64_t a8 = a_stage + shifts[8];
+#pragma unroll
+        for (int k = 0; k < HALF; ++k) step(a8 + (uint32_t)(2 * k * R));
+        step(a8 + (uint32_t)((TPC - 2) * R));  // zero-weight slot over chunk C-2, then chunk C-1
+        mma_commit_warp(B_empty + 8u * (st));
+        if (++st == p.stages) { st = 0; ph ^= 1; }
+      } else if constexpr (KS > 0) {
         // Specialised issue: taps and K steps fully unrolled with constant
         // descriptor offsets (48 cycles per N=64 MMA, the shared-memory
         // operand floor, vs 74 for the runtime loop; scripts/mma_bench_conv_loop.cu).
@@ -618,7 +651,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
 using KFn = void (*)(const ConvTcParams, const CUtensorMap, const CUtensorMap);
 
 template <typename ET, int TAIL>
-static KFn select_conv_tail(const Geom& g, int np, int mode, int c0, int c1) {
+static KFn select_conv_tail(const Geom& g, int np, int mode, int c0, int c1, int tpc) {
   static const KFn table[4][3] = {
       {k_conv_tc<ET, 16, 0, TAIL>, k_conv_tc<ET, 16, 1, TAIL>, k_conv_tc<ET, 16, 2, TAIL>},
       {k_conv_tc<ET, 32, 0, TAIL>, k_conv_tc<ET, 32, 1, TAIL>, k_conv_tc<ET, 32, 2, TAIL>},
@@ -628,20 +661,22 @@ static KFn select_conv_tail(const Geom& g, int np, int mode, int c0, int c1) {
   // fully unrolled issue for the 3x3 layers of d_s in (48, 64] (the RT / large models)
   if (g.ks == 3 && np == 64) {
     const int nk0 = c0 / 16, nk1 = c1 / 16;
-    if (TAIL == TAIL_NONE && mode == EPI_RELU && nk0 == 2 && nk1 == 0) fn = k_conv_tc<ET, 64, EPI_RELU, TAIL, 3, 2, 0>;
+    if (TAIL == TAIL_NONE && mode == EPI_RELU && nk0 == 2 && nk1 == 0)
+      fn = tpc == 3 ? k_conv_tc<ET, 64, EPI_RELU, TAIL, 3, 2, 0, 3> : k_conv_tc<ET, 64, EPI_RELU, TAIL, 3, 2, 0>;
     if (TAIL == TAIL_NONE && mode == EPI_RELU && nk0 == 4 && nk1 == 4) fn = k_conv_tc<ET, 64, EPI_RELU, TAIL, 3, 4, 4>;
     if (TAIL != TAIL_READOUT && mode == EPI_STATE_INIT && nk0 == 4 && nk1 == 0)
-      fn = k_conv_tc<ET, 64, EPI_STATE_INIT, TAIL, 3, 4, 0>;
-    if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0) fn = k_conv_tc<ET, 64, EPI_RESIDUAL, TAIL, 3, 4, 0>;
+      fn = tpc == 7 ? k_conv_tc<ET, 64, EPI_STATE_INIT, TAIL, 3, 4, 0, 7> : k_conv_tc<ET, 64, EPI_STATE_INIT, TAIL, 3, 4, 0>;
+    if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0)
+      fn = tpc == 7 ? k_conv_tc<ET, 64, EPI_RESIDUAL, TAIL, 3, 4, 0, 7> : k_conv_tc<ET, 64, EPI_RESIDUAL, TAIL, 3, 4, 0>;
   }
   return fn;
 }
 
 template <typename ET>
-static KFn select_conv(const Geom& g, int np, int mode, int tail, int c0, int c1) {
-  if (tail == TAIL_MSG) return select_conv_tail<ET, TAIL_MSG>(g, np, mode, c0, c1);
-  if (tail == TAIL_READOUT) return select_conv_tail<ET, TAIL_READOUT>(g, np, mode, c0, c1);
-  return select_conv_tail<ET, TAIL_NONE>(g, np, mode, c0, c1);
+static KFn select_conv(const Geom& g, int np, int mode, int tail, int c0, int c1, int tpc) {
+  if (tail == TAIL_MSG) return select_conv_tail<ET, TAIL_MSG>(g, np, mode, c0, c1, tpc);
+  if (tail == TAIL_READOUT) return select_conv_tail<ET, TAIL_READOUT>(g, np, mode, c0, c1, tpc);
+  return select_conv_tail<ET, TAIL_NONE>(g, np, mode, c0, c1, tpc);
 }
 
 struct ConvLaunch {
@@ -718,14 +753,21 @@ static int launch_conv(const Geom& g, const ConvLaunch& c, const uint8_t* wb, co
   while (stages > 2 && conv_smem_layout(p, c.tail).total > SMEM_LIMIT) p.stages = --stages;
   if (conv_smem_layout(p, c.tail).total > SMEM_LIMIT || p.rbox > 256) return NRX_ERR_UNSUPPORTED;
   const size_t smem = conv_smem_layout(p, c.tail).total;
+  // tap-pair layers (tp2_chunks; the packer wrote their weights in that K order): state_init.conv0
+  // over the feature chunks, the conv1 layers over h; only their data chunks are loaded
+  int tpc = 0;
+  if (c.c1 == 0 && p.np == 64) {
+    if (c.mode == EPI_RELU && c.c0 == g.Cf && tp2_chunks(g.d, g.ks, g.prec, c.c0, g.Cin) == 3) tpc = 3;
+    if (c.mode != EPI_RELU && c.c0 == g.Ch && tp2_layer(g.d, g.ks, g.prec)) tpc = 7;
+  }
   CUtensorMap m0, m1;
-  int rc = make_map(&m0, c.src0, g, c.c0, p.rbox);
+  int rc = make_map(&m0, c.src0, g, c.c0, p.rbox, tpc);
   if (rc) return rc;
   rc = make_map(&m1, c.src1 ? c.src1 : c.src0, g, c.c1 ? c.c1 : c.c0, p.rbox);
   if (rc) return rc;
   if (p.np % 16 || p.np < 16 || p.np > 64 || c.mode < 0 || c.mode > 2) return NRX_ERR_UNSUPPORTED;
-  const KFn fn = g.prec == NRX_FP16 ? select_conv<__half>(g, p.np, c.mode, c.tail, c.c0, c.c1)
-                                    : select_conv<__nv_bfloat16>(g, p.np, c.mode, c.tail, c.c0, c.c1);
+  const KFn fn = g.prec == NRX_FP16 ? select_conv<__half>(g, p.np, c.mode, c.tail, c.c0, c.c1, tpc)
+                                    : select_conv<__nv_bfloat16>(g, p.np, c.mode, c.tail, c.c0, c.c1, tpc);
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.NU * g.tiles;
   dim3 grid(total < num_sms() ? total : num_sms(), p.n_io);

@@ -377,6 +377,24 @@ void pack_conv_bf16(const Geom& g, int k, const ConvOff& c, int cin_ref, const f
   for (int o = 0; o < np; ++o) db[o] = o < cout ? b[o] : 0.f;
 }
 
+// bf16 / fp16 single-CTA convolution in the tap-pair K order (tp2_slot) over C data chunks
+void pack_conv_bf16_tp2(const Geom& g, int C, const ConvOff& c, int cin_ref, const float* w, const float* b,
+                        uint8_t* base) {
+  const int np = rup(g.d, 16), cout = g.d;
+  BOperand B{(uint16_t*)(base + c.w), np, g.prec == NRX_FP16};
+  for (int slot = 0; slot < 2 * tp2_steps(C); ++slot) {
+    int tap, ch;
+    tp2_slot(C, slot, &tap, &ch);
+    for (int j = 0; j < 8; ++j) {
+      const int src = 8 * ch + j;
+      for (int o = 0; o < np; ++o)
+        B.set(o, 8 * slot + j, (src < cin_ref && o < cout) ? w[((size_t)tap * cin_ref + src) * cout + o] : 0.f);
+    }
+  }
+  float* db = (float*)(base + c.b);
+  for (int o = 0; o < np; ++o) db[o] = o < cout ? b[o] : 0.f;
+}
+
 float f16_to_f32(uint16_t b) {
   _Float16 h;
   std::memcpy(&h, &b, 2);
@@ -588,8 +606,14 @@ int pack_weights_tc(const nrx_model_desc* m, int prec, const float* const* t, ui
   const int i_msg = 8 * m->n_io, i_upd = i_msg + 4, i_chest = i_upd + 4;
   for (int io = 0; io < m->n_io; ++io) {
     const int i = 8 * io;
-    pack_conv_bf16(g, k, L.init0[io], g.Cin, t[i], t[i + 1], map_identity_feats, base);
-    pack_conv_bf16(g, k, L.init1[io], d, t[i + 2], t[i + 3], map_identity_hidden, base);
+    if (tp2_chunks(d, k, prec, g.Cf, g.Cin) == 3)
+      pack_conv_bf16_tp2(g, 3, L.init0[io], g.Cin, t[i], t[i + 1], base);
+    else
+      pack_conv_bf16(g, k, L.init0[io], g.Cin, t[i], t[i + 1], map_identity_feats, base);
+    if (tp2_layer(d, k, prec))
+      pack_conv_bf16_tp2(g, 7, L.init1[io], d, t[i + 2], t[i + 3], base);
+    else
+      pack_conv_bf16(g, k, L.init1[io], d, t[i + 2], t[i + 3], map_identity_hidden, base);
     // fused readout: fc0 = [llr fc0 | chest fc0], fc1 block diagonal
     const MlpOff& o = L.llr[io];
     const int width = llr_width_of(m, io);
@@ -632,7 +656,10 @@ int pack_weights_tc(const nrx_model_desc* m, int prec, const float* const* t, ui
     }
   }
   pack_conv_bf16(g, k, L.upd0, 2 * d + 2, t[i_upd], t[i_upd + 1], map_update, base);
-  pack_conv_bf16(g, k, L.upd1, d, t[i_upd + 2], t[i_upd + 3], map_identity_hidden, base);
+  if (tp2_layer(d, k, prec))
+    pack_conv_bf16_tp2(g, 7, L.upd1, d, t[i_upd + 2], t[i_upd + 3], base);
+  else
+    pack_conv_bf16(g, k, L.upd1, d, t[i_upd + 2], t[i_upd + 3], map_identity_hidden, base);
   if (L.upd0p.w) {
     for (int io = 0; io < m->n_io; ++io)
       pack_conv_pair16(g, k, L.init0p[io], g.Cin, t[8 * io], t[8 * io + 1], map_identity_feats, base);

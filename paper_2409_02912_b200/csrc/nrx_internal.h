@@ -68,7 +68,7 @@ inline int posw_off(int np) { return np + 4; }
 // chunk C-1.  The straddling step's second half sits at another row offset,
 // which its A descriptor's leading-byte offset expresses; only C chunks are loaded.
 inline int tp2_chunks(int d, int ks, int prec, int cin_buf, int cin) {  // C, or 0: not a tap-pair layer
-  if (prec != NRX_FP32X3 || ks != 3 || cin_buf % 16) return 0;
+  if ((prec != NRX_FP32X3 && prec != NRX_FP16 && prec != NRX_BF16) || ks != 3 || cin_buf % 16) return 0;
   const int c = (cin + 7) / 8;
   return (c % 2 == 1 && c + 1 == cin_buf / 8 && (c == 7 || c == 3) && d == 56) ? c : 0;
 }
