@@ -107,7 +107,9 @@ __host__ __device__ inline ConvSmem conv_smem_layout(const ConvTcParams& p, int 
 // matches); KS = 0 is the generic runtime-loop version.
 // ET = __nv_bfloat16 or __half: operand/activation element type.
 // TPC > 0: the tap-pair K order over TPC data chunks (tp2_chunks, nrx_internal.h).
-template <typename ET, int NP, int MODE, int TAIL, int KS = 0, int NK0 = 0, int NK1 = 0, int TPC = 0>
+// TH > 0: compile-time tail shape of the RT models (Cs = Ca = 64, hidden TH: 64
+// for the message tail, 128 for the readout), fully unrolled tail stages.
+template <typename ET, int NP, int MODE, int TAIL, int KS = 0, int NK0 = 0, int NK1 = 0, int TPC = 0, int TH = 0>
 __global__ void __launch_bounds__(conv_threads(NP), 1)
     k_conv_tc(const __grid_constant__ ConvTcParams p, const __grid_constant__ CUtensorMap map0,
               const __grid_constant__ CUtensorMap map1) {
@@ -174,9 +176,11 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_ptr, 0);
+  // tail shape: compile-time for TH > 0
+  const int thp = TH ? TH : p.thp, top = TH ? (TAIL == TAIL_MSG ? 64 : 32) : p.top, tcs = TH ? 64 : g.Cs;
   // tail TMEM regions (double buffered): hidden at col_h + b*thp, outputs at col_o + b*top
-  const uint32_t col_h = 2 * NP, col_o = 2 * NP + 2 * p.thp;
-  const uint32_t ta_bytes = (uint32_t)g.Cs * NRX_TILE_M * 2, th_bytes = (uint32_t)p.thp * NRX_TILE_M * 2;
+  const uint32_t col_h = 2 * NP, col_o = 2 * NP + 2 * thp;
+  const uint32_t ta_bytes = (uint32_t)tcs * NRX_TILE_M * 2, th_bytes = (uint32_t)thp * NRX_TILE_M * 2;
   const int R = p.rbox;
   // fc1 of tile j is issued LAG tiles after conv(j).  TAIL_MSG: LAG = 3 with two
   // hidden tiles, so the MMA warp's wait for a hidden layer never holds back the
@@ -238,33 +242,35 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     // fc1(i-LAG) (out = relu-hidden x W1, N = top); buffers alternate by tile parity
     auto issue_fc0 = [&](int j) {
       const int b = j & 1;
-      const uint32_t id0 = idesc_f16kind<ET>(NRX_TILE_M, p.thp);
+      const uint32_t id0 = idesc_f16kind<ET>(NRX_TILE_M, thp);
       NRX_T(tw);
       mbar_wait(B_ta_ready + 8u * (b), (j >> 1) & 1);
       NRX_TADD(t_c, tw);
       tc_fence_after();
       uint64_t ad = smem_desc(smem_u32(smem + L.ta + b * ta_bytes), NRX_TILE_M * 16, 128);
-      uint64_t bd = smem_desc(smem_u32(smem + L.tw0), p.thp * 16, 128);
-      for (int kc = 0; kc < g.Cs / 8; kc += 2) {
-        mma_bf16_warp(tmem_base + col_h + b * p.thp, ad, bd, id0, kc != 0);
+      uint64_t bd = smem_desc(smem_u32(smem + L.tw0), thp * 16, 128);
+#pragma unroll 4
+      for (int kc = 0; kc < tcs / 8; kc += 2) {
+        mma_bf16_warp(tmem_base + col_h + b * thp, ad, bd, id0, kc != 0);
         ad += 2 * NRX_TILE_M;
-        bd += 2 * p.thp;
+        bd += 2 * thp;
       }
       mma_commit_warp(B_hid_full + 8u * (b));
     };
     auto issue_fc1 = [&](int j) {
       const int b = j & 1;
-      const uint32_t id1 = idesc_f16kind<ET>(NRX_TILE_M, p.top);
+      const uint32_t id1 = idesc_f16kind<ET>(NRX_TILE_M, top);
       NRX_T(tw);
       mbar_wait(B_h_ready + 8u * (b), (j >> 1) & 1);
       NRX_TADD(t_d, tw);
       tc_fence_after();
       uint64_t ad = smem_desc(smem_u32(smem + L.th + (NTH == 2 ? b : 0) * th_bytes), NRX_TILE_M * 16, 128);
-      uint64_t bd = smem_desc(smem_u32(smem + L.tw1), p.top * 16, 128);
-      for (int kc = 0; kc < p.thp / 8; kc += 2) {
-        mma_bf16_warp(tmem_base + col_o + b * p.top, ad, bd, id1, kc != 0);
+      uint64_t bd = smem_desc(smem_u32(smem + L.tw1), top * 16, 128);
+#pragma unroll 8
+      for (int kc = 0; kc < thp / 8; kc += 2) {
+        mma_bf16_warp(tmem_base + col_o + b * top, ad, bd, id1, kc != 0);
         ad += 2 * NRX_TILE_M;
-        bd += 2 * p.top;
+        bd += 2 * top;
       }
       mma_commit_warp(B_tout_full + 8u * (b));
     };
@@ -407,18 +413,25 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       mbar_wait(B_hid_full + 8u * (b), (j >> 1) & 1);
       NRX_TADD(t_d, tw);
       tc_fence_after();
-      const int hch = p.thp / 8, hbeg = part * hch / PARTS, hend = (part + 1) * hch / PARTS;
       // TH[j] is free: fc1 of its previous tile (j - NTH) completed (tail_out(j + 1 - LAG) ran first)
       const uint32_t thb = th_s + (NTH == 2 ? b : 0) * th_bytes;
-      for (int c8 = hbeg; c8 < hend; ++c8) {
+      auto hchunk = [&](int c8) {
         float hv[8], bb[8];
-        tmem_ld8(tmem_base + lane_off + col_h + b * p.thp + 8 * c8, hv);
+        tmem_ld8(tmem_base + lane_off + col_h + b * thp + 8 * c8, hv);
         ld_shared_f8(stb0_s + 32u * c8, bb);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) hv[e] += bb[e];
         st_shared_u4(thb + (uint32_t)(c8 * NRX_TILE_M + r) * 16u,
                      relu_chunk(pack_chunk(hv, static_cast<const ET*>(nullptr)), static_cast<const ET*>(nullptr)));
+      };
+      if constexpr (TH > 0) {
+        constexpr int HPP = TH / 8 / PARTS;
+#pragma unroll
+        for (int k = 0; k < HPP; ++k) hchunk(part * HPP + k);
+      } else {
+        const int hch = thp / 8, hbeg = part * hch / PARTS, hend = (part + 1) * hch / PARTS;
+        for (int c8 = hbeg; c8 < hend; ++c8) hchunk(c8);
       }
       fence_proxy_async();
       tc_fence_before();
@@ -435,11 +448,14 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       int s, t;
       row_to_st(row, g, s, t);
       const bool valid = row < g.rows_data && t < g.T;
-      const uint32_t tcol = tmem_base + lane_off + col_o + b * p.top;
+      const uint32_t tcol = tmem_base + lane_off + col_o + b * top;
       const uint32_t vmask = valid ? 0xffffffffu : 0u;
       if (TAIL == TAIL_MSG) {  // messages of this slab, zero on pad rows/channels
-        const int och = g.Ca / 8, obeg = part * och / PARTS, oend = (part + 1) * och / PARTS;
+        constexpr int OPP = 8 / PARTS;  // TH > 0: Ca = 64
+        const int och = TH ? 8 : g.Ca / 8, obeg = TH ? part * OPP : part * och / PARTS,
+                  oend = TH ? obeg + OPP : (part + 1) * och / PARTS;
         ET* const mrow = chunk_ptr(static_cast<ET*>(p.msg), jslab, och, 0, row, g);
+#pragma unroll 2
         for (int cc = obeg; cc < oend; ++cc) {
           float mv[8], bb[8];
           tmem_ld8(tcol + 8 * cc, mv);
@@ -498,6 +514,25 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
 
     WorkIter w(g, g.NU, g.tiles, p.n_io, p.mod_order);
     int slab, tile, it = 0;
+    // fp16 residual: the state chunks of the next tile are loaded while this
+    // tile is processed (each row is read and rewritten only by its own thread)
+    constexpr bool PREF = MODE == EPI_RESIDUAL && !MASTER;
+    WorkIter wp = w;
+    uint4 nraw[PREF ? NC / 8 : 1];
+    auto load_res = [&](int sl, int tl) {
+      const int prow = tl * NRX_TILE_M + r;
+      int ps, pt;
+      row_to_st(prow, g, ps, pt);
+      const bool pv = prow < g.rows_data && pt < g.T;
+      const uint4* src = reinterpret_cast<const uint4*>(chunk_ptr(dst, sl, nd, cbase / 8, prow, g));
+#pragma unroll
+      for (int c8 = 0; c8 < NC / 8; ++c8)
+        nraw[c8] = (pv && cbase / 8 + c8 < dch) ? src[(size_t)c8 * g.rows_slab] : make_uint4(0u, 0u, 0u, 0u);
+    };
+    if (PREF) {
+      int sl, tl;
+      if (wp.next(sl, tl)) load_res(sl, tl);
+    }
     while (w.next(slab, tile)) {
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
@@ -507,26 +542,21 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       const bool valid = row < g.rows_data && t < g.T;
       float old[MASTER ? NC : 1];
       uint4 raw[MASTER ? 1 : NC / 8];
-      if (MODE == EPI_RESIDUAL) {  // residual input: loads issued before the accumulator wait
-        if (MASTER) {             // bf16 path: fp32 residual stream
+      if (PREF) {
 #pragma unroll
-          for (int c4 = 0; c4 < NC / 4; ++c4) {
-            const int cc = cbase / 4 + c4;
-            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid && cc < n32) o = *reinterpret_cast<const float4*>(chunk_ptr(p.dst32, slab, n32, cc, row, g));
-            old[4 * c4 + 0] = o.x;
-            old[4 * c4 + 1] = o.y;
-            old[4 * c4 + 2] = o.z;
-            old[4 * c4 + 3] = o.w;
-          }
-        } else {                   // fp16 path: the state buffer itself
+        for (int c8 = 0; c8 < NC / 8; ++c8) raw[c8] = nraw[c8];
+        int sl, tl;
+        if (wp.next(sl, tl)) load_res(sl, tl);
+      } else if (MODE == EPI_RESIDUAL) {  // bf16: fp32 residual stream, loads issued before the accumulator wait
 #pragma unroll
-          for (int c8 = 0; c8 < NC / 8; ++c8) {
-            const int cc = cbase / 8 + c8;
-            raw[c8] = (valid && cc < dch)
-                          ? *reinterpret_cast<const uint4*>(chunk_ptr(dst, slab, nd, 0, row, g) + (size_t)cc * g.rows_slab * 8)
-                          : make_uint4(0u, 0u, 0u, 0u);
-          }
+        for (int c4 = 0; c4 < NC / 4; ++c4) {
+          const int cc = cbase / 4 + c4;
+          float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (valid && cc < n32) o = *reinterpret_cast<const float4*>(chunk_ptr(p.dst32, slab, n32, cc, row, g));
+          old[4 * c4 + 0] = o.x;
+          old[4 * c4 + 1] = o.y;
+          old[4 * c4 + 2] = o.z;
+          old[4 * c4 + 3] = o.w;
         }
       }
       NRX_T(t0);
@@ -651,7 +681,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
 using KFn = void (*)(const ConvTcParams, const CUtensorMap, const CUtensorMap);
 
 template <typename ET, int TAIL>
-static KFn select_conv_tail(const Geom& g, int np, int mode, int c0, int c1, int tpc) {
+static KFn select_conv_tail(const Geom& g, int np, int mode, int c0, int c1, int tpc, bool rt) {
   static const KFn table[4][3] = {
       {k_conv_tc<ET, 16, 0, TAIL>, k_conv_tc<ET, 16, 1, TAIL>, k_conv_tc<ET, 16, 2, TAIL>},
       {k_conv_tc<ET, 32, 0, TAIL>, k_conv_tc<ET, 32, 1, TAIL>, k_conv_tc<ET, 32, 2, TAIL>},
@@ -664,19 +694,25 @@ static KFn select_conv_tail(const Geom& g, int np, int mode, int c0, int c1, int
     if (TAIL == TAIL_NONE && mode == EPI_RELU && nk0 == 2 && nk1 == 0)
       fn = tpc == 3 ? k_conv_tc<ET, 64, EPI_RELU, TAIL, 3, 2, 0, 3> : k_conv_tc<ET, 64, EPI_RELU, TAIL, 3, 2, 0>;
     if (TAIL == TAIL_NONE && mode == EPI_RELU && nk0 == 4 && nk1 == 4) fn = k_conv_tc<ET, 64, EPI_RELU, TAIL, 3, 4, 4>;
+    // compile-time RT tail shape (rt); TAIL_NONE has no tail (TH = 0 twice)
+    constexpr int TH = TAIL == TAIL_MSG ? 64 : TAIL == TAIL_READOUT ? 128 : 0;
     if (TAIL != TAIL_READOUT && mode == EPI_STATE_INIT && nk0 == 4 && nk1 == 0)
-      fn = tpc == 7 ? k_conv_tc<ET, 64, EPI_STATE_INIT, TAIL, 3, 4, 0, 7> : k_conv_tc<ET, 64, EPI_STATE_INIT, TAIL, 3, 4, 0>;
+      fn = tpc == 7 ? (rt ? k_conv_tc<ET, 64, EPI_STATE_INIT, TAIL, 3, 4, 0, 7, TH>
+                          : k_conv_tc<ET, 64, EPI_STATE_INIT, TAIL, 3, 4, 0, 7>)
+                    : k_conv_tc<ET, 64, EPI_STATE_INIT, TAIL, 3, 4, 0>;
     if (mode == EPI_RESIDUAL && nk0 == 4 && nk1 == 0)
-      fn = tpc == 7 ? k_conv_tc<ET, 64, EPI_RESIDUAL, TAIL, 3, 4, 0, 7> : k_conv_tc<ET, 64, EPI_RESIDUAL, TAIL, 3, 4, 0>;
+      fn = tpc == 7 ? (rt ? k_conv_tc<ET, 64, EPI_RESIDUAL, TAIL, 3, 4, 0, 7, TH>
+                          : k_conv_tc<ET, 64, EPI_RESIDUAL, TAIL, 3, 4, 0, 7>)
+                    : k_conv_tc<ET, 64, EPI_RESIDUAL, TAIL, 3, 4, 0>;
   }
   return fn;
 }
 
 template <typename ET>
-static KFn select_conv(const Geom& g, int np, int mode, int tail, int c0, int c1, int tpc) {
-  if (tail == TAIL_MSG) return select_conv_tail<ET, TAIL_MSG>(g, np, mode, c0, c1, tpc);
-  if (tail == TAIL_READOUT) return select_conv_tail<ET, TAIL_READOUT>(g, np, mode, c0, c1, tpc);
-  return select_conv_tail<ET, TAIL_NONE>(g, np, mode, c0, c1, tpc);
+static KFn select_conv(const Geom& g, int np, int mode, int tail, int c0, int c1, int tpc, bool rt) {
+  if (tail == TAIL_MSG) return select_conv_tail<ET, TAIL_MSG>(g, np, mode, c0, c1, tpc, rt);
+  if (tail == TAIL_READOUT) return select_conv_tail<ET, TAIL_READOUT>(g, np, mode, c0, c1, tpc, rt);
+  return select_conv_tail<ET, TAIL_NONE>(g, np, mode, c0, c1, tpc, false);
 }
 
 struct ConvLaunch {
@@ -766,8 +802,11 @@ static int launch_conv(const Geom& g, const ConvLaunch& c, const uint8_t* wb, co
   rc = make_map(&m1, c.src1 ? c.src1 : c.src0, g, c.c1 ? c.c1 : c.c0, p.rbox);
   if (rc) return rc;
   if (p.np % 16 || p.np < 16 || p.np > 64 || c.mode < 0 || c.mode > 2) return NRX_ERR_UNSUPPORTED;
-  const KFn fn = g.prec == NRX_FP16 ? select_conv<__half>(g, p.np, c.mode, c.tail, c.c0, c.c1, tpc)
-                                    : select_conv<__nv_bfloat16>(g, p.np, c.mode, c.tail, c.c0, c.c1, tpc);
+  // the RT tail shape (message: hidden 64 -> 64; readout: hidden 128 -> 32) as compile-time sizes
+  const bool rt = tpc == 7 && g.Cs == 64 && g.Ca == 64 &&
+                  ((c.tail == TAIL_MSG && p.thp == 64 && p.top == 64) || (c.tail == TAIL_READOUT && p.thp == 128));
+  const KFn fn = g.prec == NRX_FP16 ? select_conv<__half>(g, p.np, c.mode, c.tail, c.c0, c.c1, tpc, rt)
+                                    : select_conv<__nv_bfloat16>(g, p.np, c.mode, c.tail, c.c0, c.c1, tpc, rt);
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
   const int total = g.NU * g.tiles;
   dim3 grid(total < num_sms() ? total : num_sms(), p.n_io);
