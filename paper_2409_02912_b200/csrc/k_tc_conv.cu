@@ -514,20 +514,29 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
 
     WorkIter w(g, g.NU, g.tiles, p.n_io, p.mod_order);
     int slab, tile, it = 0;
-    // fp16 residual: the state chunks of the next tile are loaded while this
-    // tile is processed (each row is read and rewritten only by its own thread)
-    constexpr bool PREF = MODE == EPI_RESIDUAL && !MASTER;
+    // residual: the previous state of the next tile (fp16: the state buffer
+    // itself; bf16: the fp32 master) is loaded while this tile is processed
+    // (each row is read and rewritten only by its own thread)
+    constexpr bool PREF = MODE == EPI_RESIDUAL;
     WorkIter wp = w;
-    uint4 nraw[PREF ? NC / 8 : 1];
+    uint4 nraw[PREF && !MASTER ? NC / 8 : 1];
+    float4 nold[PREF && MASTER ? NC / 4 : 1];
     auto load_res = [&](int sl, int tl) {
       const int prow = tl * NRX_TILE_M + r;
       int ps, pt;
       row_to_st(prow, g, ps, pt);
       const bool pv = prow < g.rows_data && pt < g.T;
-      const uint4* src = reinterpret_cast<const uint4*>(chunk_ptr(dst, sl, nd, cbase / 8, prow, g));
+      if constexpr (MASTER) {
+        const float4* src = reinterpret_cast<const float4*>(chunk_ptr(p.dst32, sl, n32, cbase / 4, prow, g));
 #pragma unroll
-      for (int c8 = 0; c8 < NC / 8; ++c8)
-        nraw[c8] = (pv && cbase / 8 + c8 < dch) ? src[(size_t)c8 * g.rows_slab] : make_uint4(0u, 0u, 0u, 0u);
+        for (int c4 = 0; c4 < NC / 4; ++c4)
+          nold[c4] = (pv && cbase / 4 + c4 < n32) ? src[(size_t)c4 * g.rows_slab] : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        const uint4* src = reinterpret_cast<const uint4*>(chunk_ptr(dst, sl, nd, cbase / 8, prow, g));
+#pragma unroll
+        for (int c8 = 0; c8 < NC / 8; ++c8)
+          nraw[c8] = (pv && cbase / 8 + c8 < dch) ? src[(size_t)c8 * g.rows_slab] : make_uint4(0u, 0u, 0u, 0u);
+      }
     };
     if (PREF) {
       int sl, tl;
@@ -543,21 +552,20 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       float old[MASTER ? NC : 1];
       uint4 raw[MASTER ? 1 : NC / 8];
       if (PREF) {
+        if constexpr (MASTER) {
 #pragma unroll
-        for (int c8 = 0; c8 < NC / 8; ++c8) raw[c8] = nraw[c8];
+          for (int c4 = 0; c4 < NC / 4; ++c4) {
+            old[4 * c4 + 0] = nold[c4].x;
+            old[4 * c4 + 1] = nold[c4].y;
+            old[4 * c4 + 2] = nold[c4].z;
+            old[4 * c4 + 3] = nold[c4].w;
+          }
+        } else {
+#pragma unroll
+          for (int c8 = 0; c8 < NC / 8; ++c8) raw[c8] = nraw[c8];
+        }
         int sl, tl;
         if (wp.next(sl, tl)) load_res(sl, tl);
-      } else if (MODE == EPI_RESIDUAL) {  // bf16: fp32 residual stream, loads issued before the accumulator wait
-#pragma unroll
-        for (int c4 = 0; c4 < NC / 4; ++c4) {
-          const int cc = cbase / 4 + c4;
-          float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (valid && cc < n32) o = *reinterpret_cast<const float4*>(chunk_ptr(p.dst32, slab, n32, cc, row, g));
-          old[4 * c4 + 0] = o.x;
-          old[4 * c4 + 1] = o.y;
-          old[4 * c4 + 2] = o.z;
-          old[4 * c4 + 3] = o.w;
-        }
       }
       NRX_T(t0);
       mbar_wait(B_tfull + 8u * (acc), aph);

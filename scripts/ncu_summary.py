@@ -20,7 +20,7 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
 
 # kernel template -> bench / profile_kernels name, in launch order of one forward
-NAMES = [(r"k_ls_feat", "ls_feat"), (r"k_conv_x3<\d+, 0, 3, 2, 0|k_conv_tc<.*64, 0, 0, 3, 2, 0>", "conv_state_init0"),
+NAMES = [(r"k_ls_feat", "ls_feat"), (r"k_conv_x3<\d+, 0, 3, 2, 0|k_conv_tc<.*64, 0, 0, 3, 2, 0\b", "conv_state_init0"),
          (r"k_conv_x3<\d+, 1,|k_conv_tc<.*64, 1,", "conv_state_init1"), (r"k_msg_tc", "msg_agg"),
          (r"k_conv_x3<\d+, 0, 3, (4, 4|7, 0)|k_conv_tc<.*64, 0, 0, 3, 4, 4>", "conv_update0"),
          (r"k_conv_x3<\d+, 2,|k_conv_tc<.*64, 2,", "conv_update1"), (r"k_readout_tc", "readout")]
