@@ -28,8 +28,17 @@ namespace tc {
 // warps: 0 producer, 1 MMA, HW hidden-epilogue warps, OW output-epilogue warps
 // (OW / 4 groups per TMEM lane quarter, each draining a share of the columns)
 constexpr int mlp_threads(int hw, int ow = 4) { return 64 + 32 * hw + 32 * ow; }
-constexpr int MSG_HW = 8, READOUT_HW = 8;  // 8 hidden-epilogue warps (32 columns each; fp32x3 message 0.29 -> 0.25 ms)
-constexpr int MSG_OW = 8;  // the message epilogue (2 UEs x 64 columns, split planes) is the long pole
+#ifndef NRX_MSG_HW  // build-time overrides for A/B runs
+#define NRX_MSG_HW 8
+#endif
+#ifndef NRX_MSG_OW
+#define NRX_MSG_OW 8
+#endif
+#ifndef NRX_READOUT_HW
+#define NRX_READOUT_HW 8
+#endif
+constexpr int MSG_HW = NRX_MSG_HW, READOUT_HW = NRX_READOUT_HW;  // 8 hidden-epilogue warps (32 columns each; fp32x3 message 0.29 -> 0.25 ms)
+constexpr int MSG_OW = NRX_MSG_OW;  // the message epilogue (2 UEs x 64 columns, split planes) is the long pole
 constexpr int MSG_MAXU = 4;  // UEs per slot on the tensor-core path
 constexpr int A_STAGES = 4;  // maximum; fp32x3 uses fewer (p.astages)
 
