@@ -55,7 +55,17 @@ struct ConvTcParams {
   void* msg;            // TAIL_MSG output: [slab][Ca/8][rows][8] ET
   float* llr;           // TAIL_READOUT outputs
   float2* chest;
+  int racc;             // residual through the accumulator (conv_racc): three state tiles + identity B
 };
+
+// fp16 update.conv1 with the RT message / readout tail: the previous state
+// enters the accumulator as a fifth K block (the state tile by TMA into the
+// tail's A buffer, times a 64 x 64 identity B; fp16 -> fp32 is exact) instead
+// of a global load + convert + add per element in the epilogue.
+template <typename ET, int MODE, int TPC, int TH>
+__host__ __device__ constexpr bool conv_racc() {
+  return std::is_same<ET, __half>::value && MODE == 2 && TPC == 7 && TH > 0;
+}
 
 // warp 0 TMA producer, warp 1 MMA issuer, then NP/16 groups of four epilogue
 // warps (one per TMEM lane quarter); every epilogue thread drains 16
@@ -66,7 +76,7 @@ __host__ __device__ constexpr int conv_threads(int np) { return 64 + conv_epi_th
 
 // Shared-memory carve-up (identical on host and device).
 struct ConvSmem {
-  uint32_t w, a, tw0, tw1, ta, th, bars, tmem_ptr, sbias, tb0, tb1, dt, total;
+  uint32_t w, a, tw0, tw1, ta, th, ident, bars, tmem_ptr, sbias, tb0, tb1, dt, total;
 };
 __host__ __device__ inline ConvSmem conv_smem_layout(const ConvTcParams& p, int tail) {
   ConvSmem s;
@@ -82,12 +92,14 @@ __host__ __device__ inline ConvSmem conv_smem_layout(const ConvTcParams& p, int 
     s.tw1 = off;
     off += p.tw1bytes;
     s.ta = off;
-    off += 2u * p.g.Cs * NRX_TILE_M * 2;
+    off += (p.racc ? 3u : 2u) * p.g.Cs * NRX_TILE_M * 2;
     s.th = off;
     off += (tail == TAIL_MSG ? 2u : 1u) * p.thp * NRX_TILE_M * 2;
   }
+  s.ident = off;  // racc: identity B operand (64 x 64 fp16, K-major core matrices)
+  if (p.racc) off += 64 * 64 * 2;
   s.bars = off;
-  off += 32 * 8;
+  off += 40 * 8;
   s.tmem_ptr = off;
   off += 16;
   s.sbias = off;
@@ -127,15 +139,20 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   uint64_t* tfull = bars + 16;
   uint64_t* tempty = bars + 18;
   uint64_t* wbar = bars + 20;
-  uint64_t* ta_ready = bars + 21;   // [2] tail: state tile in shared memory
+  uint64_t* ta_ready = bars + 29;   // [NTA] tail: state tile in shared memory
   uint64_t* hid_full = bars + 23;   // [2] tail: fc0 done
   uint64_t* h_ready = bars + 25;    // [2] tail: hidden layer in shared memory
   uint64_t* tout_full = bars + 27;  // [2] tail: fc1 done
+  uint64_t* ta_free = bars + 32;    // [3] racc: fc0 read the state tile
+  uint64_t* res_full = bars + 35;   // [3] racc: previous state tile loaded
+  constexpr bool RACC = conv_racc<ET, MODE, TPC, TH>();
+  constexpr int NTA = RACC ? 3 : 2;  // state tiles (fc0's A operand)
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L.tmem_ptr);
   // shared-space addresses of the barriers (8 B each)
   const uint32_t B_full = smem_u32(full), B_empty = smem_u32(empty), B_tfull = smem_u32(tfull),
                  B_tempty = smem_u32(tempty), B_wbar = smem_u32(wbar), B_ta_ready = smem_u32(ta_ready),
-                 B_hid_full = smem_u32(hid_full), B_h_ready = smem_u32(h_ready), B_tout_full = smem_u32(tout_full);
+                 B_hid_full = smem_u32(hid_full), B_h_ready = smem_u32(h_ready), B_tout_full = smem_u32(tout_full),
+                 B_ta_free = smem_u32(ta_free), B_res_full = smem_u32(res_full);
   float* sbias = reinterpret_cast<float*>(smem + L.sbias);
   float* stb0 = reinterpret_cast<float*>(smem + L.tb0);
   float* stb1 = reinterpret_cast<float*>(smem + L.tb1);
@@ -155,8 +172,13 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       mbar_init(&tempty[a], conv_epi_threads(NP));
     }
     mbar_init(wbar, 1);
+    for (int b = 0; b < NTA; ++b) mbar_init(&ta_ready[b], conv_epi_threads(NP));
+    if (RACC)
+      for (int b = 0; b < 3; ++b) {
+        mbar_init(&ta_free[b], 1);
+        mbar_init(&res_full[b], 1);
+      }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&ta_ready[b], conv_epi_threads(NP));
       mbar_init(&hid_full[b], 1);
       mbar_init(&h_ready[b], conv_epi_threads(NP));
       mbar_init(&tout_full[b], 1);
@@ -166,6 +188,16 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   if (threadIdx.x >= 64 && threadIdx.x < 64 + NP)
     sbias[threadIdx.x - 64] = reinterpret_cast<const float*>(p.wbase + p.b_off[io])[threadIdx.x - 64];
   if (threadIdx.x < 32) sdt[threadIdx.x] = g.dt[threadIdx.x];
+  if (RACC) {  // identity B: chunk kc, row n holds e_n restricted to K = 8 kc .. 8 kc + 7
+    for (int i = threadIdx.x; i < 8 * 64; i += blockDim.x) {
+      const int kc = i >> 6, n = i & 63, e = n - 8 * kc;
+      const uint32_t one = (e & 1) ? 0x3c000000u : 0x3c00u;  // 1.0 in fp16, low / high half
+      const int wd = e >= 0 && e < 8 ? e >> 1 : -1;
+      *reinterpret_cast<uint4*>(smem + L.ident + 16u * i) =
+          make_uint4(wd == 0 ? one : 0u, wd == 1 ? one : 0u, wd == 2 ? one : 0u, wd == 3 ? one : 0u);
+    }
+    fence_proxy_async();  // generic-proxy stores -> tensor-core reads
+  }
   if (TAIL) {
     const float* b0 = reinterpret_cast<const float*>(p.wbase + p.tb0[io]);
     const float* b1 = reinterpret_cast<const float*>(p.wbase + p.tb1[io]);
@@ -208,7 +240,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       // one pipeline stage per (tile, input source): finer-grained stages keep
       // more loads in flight next to the resident weights
       WorkIter w(g, g.NU, g.tiles, p.n_io, p.mod_order);
-      int slab, tile, st = 0;
+      int slab, tile, st = 0, it = 0;
       uint32_t ph = 0;
       while (w.next(slab, tile)) {
         const int grp0 = (tile * NRX_TILE_M - p.hup) / 16;  // 16-row groups
@@ -221,6 +253,14 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
                       src ? (slab ^ p.src1_xor) : slab);
           if (++st == p.stages) { st = 0; ph ^= 1; }
         }
+        if constexpr (RACC) {  // previous state of this tile -> state tile it % 3 once fc0(it - 3) read it
+          const int b = it % 3;
+          mbar_wait(B_ta_free + 8u * b, ((it / 3) & 1) ^ 1);
+          mbar_expect_tx(B_res_full + 8u * b, 7u * NRX_TILE_M * 16);
+          tma_load_4d(smem_u32(smem + L.ta) + b * ta_bytes, &map1, B_res_full + 8u * b, 0, tile * (NRX_TILE_M / 16),
+                      0, slab);
+        }
+        ++it;
       }
     }
   } else if (warp == 1) {  // ---------------- MMA issuer (whole warp, elect.sync issues)
@@ -241,13 +281,13 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     // warp issues conv(i), fc0(i-1) (hidden = state_tile x W0, N = thp) and
     // fc1(i-LAG) (out = relu-hidden x W1, N = top); buffers alternate by tile parity
     auto issue_fc0 = [&](int j) {
-      const int b = j & 1;
+      const int b = j & 1, ta_b = j % NTA;
       const uint32_t id0 = idesc_f16kind<ET>(NRX_TILE_M, thp);
       NRX_T(tw);
-      mbar_wait(B_ta_ready + 8u * (b), (j >> 1) & 1);
+      mbar_wait(B_ta_ready + 8u * ta_b, (j / NTA) & 1);
       NRX_TADD(t_c, tw);
       tc_fence_after();
-      uint64_t ad = smem_desc(smem_u32(smem + L.ta + b * ta_bytes), NRX_TILE_M * 16, 128);
+      uint64_t ad = smem_desc(smem_u32(smem + L.ta + ta_b * ta_bytes), NRX_TILE_M * 16, 128);
       uint64_t bd = smem_desc(smem_u32(smem + L.tw0), thp * 16, 128);
 #pragma unroll 4
       for (int kc = 0; kc < tcs / 8; kc += 2) {
@@ -256,6 +296,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         bd += 2 * thp;
       }
       mma_commit_warp(B_hid_full + 8u * (b));
+      if (RACC) mma_commit_warp(B_ta_free + 8u * ta_b);
     };
     auto issue_fc1 = [&](int j) {
       const int b = j & 1;
@@ -317,6 +358,19 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
 #pragma unroll
         for (int k = 0; k < HALF; ++k) step(a8 + (uint32_t)(2 * k * R));
         step(a8 + (uint32_t)((TPC - 2) * R));  // zero-weight slot over chunk C-2, then chunk C-1
+        if constexpr (RACC) {  // + previous state: its tile (chunk 7 zero) x identity, K = 64
+          const int b = it % 3;
+          mbar_wait(B_res_full + 8u * b, (it / 3) & 1);
+          tc_fence_after();
+          uint64_t ad = smem_desc(smem_u32(smem + L.ta) + b * ta_bytes, NRX_TILE_M * 16, 128);
+          uint64_t bd = smem_desc(smem_u32(smem + L.ident), NP * 16, 128);
+#pragma unroll
+          for (int kc = 0; kc < 8; kc += 2) {
+            mma_bf16_warp(d, ad, bd, idesc, 1);
+            ad += 2 * NRX_TILE_M;
+            bd += 2 * NP;
+          }
+        }
         mma_commit_warp(B_empty + 8u * (st));
         if (++st == p.stages) { st = 0; ph ^= 1; }
       } else if constexpr (KS > 0) {
@@ -401,7 +455,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     // the residual update skips them (and their zero rows in the tail's A tile)
     const int dch = (g.d + 7) / 8;
     if (TAIL && MODE == EPI_RESIDUAL && part == PARTS - 1) {
-      for (int b = 0; b < 2; ++b)
+      for (int b = 0; b < NTA; ++b)
         for (int cc = dch; cc < nd; ++cc)
           st_shared_u4(ta_s + b * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u, make_uint4(0u, 0u, 0u, 0u));
     }
@@ -517,7 +571,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     // residual: the previous state of the next tile (fp16: the state buffer
     // itself; bf16: the fp32 master) is loaded while this tile is processed
     // (each row is read and rewritten only by its own thread)
-    constexpr bool PREF = MODE == EPI_RESIDUAL;
+    constexpr bool PREF = MODE == EPI_RESIDUAL && !RACC;  // RACC: the residual is in the accumulator
     WorkIter wp = w;
     uint4 nraw[PREF && !MASTER ? NC / 8 : 1];
     float4 nold[PREF && MASTER ? NC / 4 : 1];
@@ -594,25 +648,25 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         const int cc = cbase / 8 + c8;
         if (MODE == EPI_RESIDUAL && cc >= dch) continue;   // constant positional / zero chunk
         float o8[8], bb[8];
-        if (MODE == EPI_RESIDUAL && !MASTER) unpack_chunk(raw[c8], static_cast<const ET*>(nullptr), o8);
+        if (PREF && !MASTER) unpack_chunk(raw[c8], static_cast<const ET*>(nullptr), o8);
         ld_shared_f8(sbias_s + 32u * cc, bb);
         float* x = v + 8 * c8;
         const bool full = 8 * cc + 8 <= g.d;  // warp-uniform
         if (!MASTER && full) {  // fast path: pack, then ReLU / pad-row mask on the packed words
 #pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = MODE == EPI_RESIDUAL ? o8[e] + (x[e] + bb[e]) : x[e] + bb[e];
+          for (int e = 0; e < 8; ++e) x[e] = PREF ? o8[e] + (x[e] + bb[e]) : x[e] + bb[e];
           uint4 qx = pack_chunk(x, static_cast<const ET*>(nullptr));
           if (MODE == EPI_RELU) qx = relu_chunk(qx, static_cast<const ET*>(nullptr));
           qx = mask_chunk(qx, vmask);
           *reinterpret_cast<uint4*>(drow + cc * dcs) = qx;
-          if (TAIL) st_shared_u4(ta_s + (it & 1) * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u, qx);
+          if (TAIL) st_shared_u4(ta_s + (it % NTA) * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u, qx);
           continue;
         }
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           float y = x[e] + bb[e];  // conv + bias first, as the reference adds them
           if (MODE == EPI_RELU) y = relu_f(y);
-          if (MODE == EPI_RESIDUAL) y = (MASTER ? old[8 * c8 + e] : o8[e]) + y;
+          if (PREF) y = (MASTER ? old[8 * c8 + e] : o8[e]) + y;
           x[e] = (valid && (full || 8 * cc + e < g.d)) ? y : 0.f;
         }
         if (MODE != EPI_RELU) {
@@ -633,7 +687,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         if (cc < nd) {
           const uint4 qx = pack_chunk(x, static_cast<const ET*>(nullptr));
           *reinterpret_cast<uint4*>(drow + cc * dcs) = qx;
-          if (TAIL) st_shared_u4(ta_s + (it & 1) * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u, qx);
+          if (TAIL) st_shared_u4(ta_s + (it % NTA) * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u, qx);
         }
       }
       if (part == PARTS - 1) {  // buffer channels beyond the accumulator: positional / zero only
@@ -643,14 +697,14 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
           for (int e = 0; e < 8; ++e)
             o[e] = (valid && MODE != EPI_RELU) ? state_extra(8 * cc + e, s, t, slab % g.U, g) : 0.f;
           store_chunk(chunk_ptr(dst, slab, nd, cc, row, g), o);
-          if (TAIL) st_shared_u4(ta_s + (it & 1) * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u,
+          if (TAIL) st_shared_u4(ta_s + (it % NTA) * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u,
                                  pack_chunk(o, static_cast<const ET*>(nullptr)));
         }
       }
       if (TAIL) {
         fence_proxy_async();  // state tile (generic-proxy stores) -> tensor-core reads
         tc_fence_before();
-        mbar_arrive(B_ta_ready + 8u * (it & 1));
+        mbar_arrive(B_ta_ready + 8u * (it % NTA));
         // pipelined tail stages: outputs of tile it-LAG (frees its hidden
         // tile), then the hidden layer of tile it-1
         if (it >= LAG) tail_out(it - LAG, hs[LAG - 1], ht[LAG - 1]);
@@ -723,6 +777,14 @@ static KFn select_conv(const Geom& g, int np, int mode, int tail, int c0, int c1
   return select_conv_tail<ET, TAIL_NONE>(g, np, mode, c0, c1, tpc, false);
 }
 
+static bool racc_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("NRX_RACC");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 struct ConvLaunch {
   const ConvOff* offs;
   int n_off;
@@ -792,11 +854,6 @@ static int launch_conv(const Geom& g, const ConvLaunch& c, const uint8_t* wb, co
   const uint32_t cols = 2 * p.np + (c.tail ? 2 * (p.thp + p.top) : 0);
   p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   if (cols > 512) return NRX_ERR_UNSUPPORTED;
-  int stages = 8;
-  p.stages = stages;
-  while (stages > 2 && conv_smem_layout(p, c.tail).total > SMEM_LIMIT) p.stages = --stages;
-  if (conv_smem_layout(p, c.tail).total > SMEM_LIMIT || p.rbox > 256) return NRX_ERR_UNSUPPORTED;
-  const size_t smem = conv_smem_layout(p, c.tail).total;
   // tap-pair layers (tp2_chunks; the packer wrote their weights in that K order): state_init.conv0
   // over the feature chunks, the conv1 layers over h; only their data chunks are loaded
   int tpc = 0;
@@ -804,15 +861,27 @@ static int launch_conv(const Geom& g, const ConvLaunch& c, const uint8_t* wb, co
     if (c.mode == EPI_RELU && c.c0 == g.Cf && tp2_chunks(g.d, g.ks, g.prec, c.c0, g.Cin) == 3) tpc = 3;
     if (c.mode != EPI_RELU && c.c0 == g.Ch && tp2_layer(g.d, g.ks, g.prec)) tpc = 7;
   }
+  // the RT tail shape (message: hidden 64 -> 64; readout: hidden 128 -> 32) as compile-time sizes
+  bool rt = tpc == 7 && g.Cs == 64 && g.Ca == 64 && g.ks == 3 &&
+            ((c.tail == TAIL_MSG && p.thp == 64 && p.top == 64) || (c.tail == TAIL_READOUT && p.thp == 128));
+  // fp16 residual update with the RT tail: the residual through the accumulator (conv_racc;
+  // NRX_RACC=0 selects the epilogue residual add instead, for A/B runs)
+  p.racc = rt && g.prec == NRX_FP16 && c.mode == EPI_RESIDUAL && g.d == 56;
+  if (p.racc && !racc_enabled()) rt = false, p.racc = 0;
+  int stages = 8;
+  p.stages = stages;
+  while (stages > 2 && conv_smem_layout(p, c.tail).total > SMEM_LIMIT) p.stages = --stages;
+  if (conv_smem_layout(p, c.tail).total > SMEM_LIMIT || p.rbox > 256) return NRX_ERR_UNSUPPORTED;
+  const size_t smem = conv_smem_layout(p, c.tail).total;
   CUtensorMap m0, m1;
   int rc = make_map(&m0, c.src0, g, c.c0, p.rbox, tpc);
   if (rc) return rc;
-  rc = make_map(&m1, c.src1 ? c.src1 : c.src0, g, c.c1 ? c.c1 : c.c0, p.rbox);
+  if (p.racc)  // source 1 = the previous state: 128-row tiles of its 7 state chunks, no halo
+    rc = make_map(&m1, c.dst, g, c.cdst, NRX_TILE_M, 7);
+  else
+    rc = make_map(&m1, c.src1 ? c.src1 : c.src0, g, c.c1 ? c.c1 : c.c0, p.rbox);
   if (rc) return rc;
   if (p.np % 16 || p.np < 16 || p.np > 64 || c.mode < 0 || c.mode > 2) return NRX_ERR_UNSUPPORTED;
-  // the RT tail shape (message: hidden 64 -> 64; readout: hidden 128 -> 32) as compile-time sizes
-  const bool rt = tpc == 7 && g.Cs == 64 && g.Ca == 64 &&
-                  ((c.tail == TAIL_MSG && p.thp == 64 && p.top == 64) || (c.tail == TAIL_READOUT && p.thp == 128));
   const KFn fn = g.prec == NRX_FP16 ? select_conv<__half>(g, p.np, c.mode, c.tail, c.c0, c.c1, tpc, rt)
                                     : select_conv<__nv_bfloat16>(g, p.np, c.mode, c.tail, c.c0, c.c1, tpc, rt);
   if (set_smem((const void*)fn, SMEM_LIMIT)) return NRX_ERR_CUDA;
