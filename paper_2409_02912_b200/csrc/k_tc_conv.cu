@@ -868,10 +868,19 @@ static int launch_conv(const Geom& g, const ConvLaunch& c, const uint8_t* wb, co
   // NRX_RACC=0 selects the epilogue residual add instead, for A/B runs)
   p.racc = rt && g.prec == NRX_FP16 && c.mode == EPI_RESIDUAL && g.d == 56;
   if (p.racc && !racc_enabled()) rt = false, p.racc = 0;
-  int stages = 8;
-  p.stages = stages;
-  while (stages > 2 && conv_smem_layout(p, c.tail).total > SMEM_LIMIT) p.stages = --stages;
-  if (conv_smem_layout(p, c.tail).total > SMEM_LIMIT || p.rbox > 256) return NRX_ERR_UNSUPPORTED;
+  auto fit = [&]() {  // pipeline stages that fit next to the resident weights (at least 2)
+    int stages = 8;
+    p.stages = stages;
+    while (stages > 2 && conv_smem_layout(p, c.tail).total > SMEM_LIMIT) p.stages = --stages;
+    return conv_smem_layout(p, c.tail).total <= SMEM_LIMIT;
+  };
+  bool fits = fit();
+  if (p.racc && !fits) {  // the third state tile + identity do not fit next to two stages: epilogue add
+    p.racc = 0;
+    rt = false;
+    fits = fit();
+  }
+  if (!fits || p.rbox > 256) return NRX_ERR_UNSUPPORTED;
   const size_t smem = conv_smem_layout(p, c.tail).total;
   CUtensorMap m0, m1;
   int rc = make_map(&m0, c.src0, g, c.c0, p.rbox, tpc);

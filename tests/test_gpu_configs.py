@@ -8,6 +8,8 @@ C2 slot (which tests/test_gpu_parity.py covers):
 All against the float64 CPU oracle with the per-precision gates of
 tests/test_gpu_parity.py."""
 
+import warnings
+
 import numpy as np
 import pytest
 
@@ -206,7 +208,11 @@ def test_random_configs_vs_oracle(seed, precision):
         with pytest.warns(RuntimeWarning, match="does not support"):
             got, ref, chest, ref_chest = _run(cfg, config, w, mcs, 2, 20 + seed, precision)
         precision = "fp32_simt"
-    else:
-        got, ref, chest, ref_chest = _run(cfg, config, w, mcs, 2, 20 + seed, precision)
+    else:  # inside the limits: the tensor-core path itself must take it (no silent fallback)
+        with warnings.catch_warnings(record=True) as caught:
+            warnings.simplefilter("always")
+            got, ref, chest, ref_chest = _run(cfg, config, w, mcs, 2, 20 + seed, precision)
+        fallbacks = [str(c.message) for c in caught if "does not support" in str(c.message)]
+        assert not fallbacks, fallbacks
     check_llrs(got, ref, precision, f"random config {seed}: {_random_config(seed)}")
     check_chest(chest, ref_chest, precision)
