@@ -188,14 +188,27 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
   if (threadIdx.x >= 64 && threadIdx.x < 64 + NP)
     sbias[threadIdx.x - 64] = reinterpret_cast<const float*>(p.wbase + p.b_off[io])[threadIdx.x - 64];
   if (threadIdx.x < 32) sdt[threadIdx.x] = g.dt[threadIdx.x];
-  if (RACC) {  // identity B: chunk kc, row n holds e_n restricted to K = 8 kc .. 8 kc + 7
+  if (RACC) {
+    // B of the fifth K block: chunk kc, row n < d holds e_n over K = 8 kc .. 8 kc + 7 (identity:
+    // + previous state), and in chunk 7 (K = 56..63, the state tile's pad channels) the conv
+    // bias split into fp16 hi / lo at K = 62 / 63, which the state tiles hold as constant ones
+    const float* cb = reinterpret_cast<const float*>(p.wbase + p.b_off[io]);
     for (int i = threadIdx.x; i < 8 * 64; i += blockDim.x) {
       const int kc = i >> 6, n = i & 63, e = n - 8 * kc;
       const uint32_t one = (e & 1) ? 0x3c000000u : 0x3c00u;  // 1.0 in fp16, low / high half
-      const int wd = e >= 0 && e < 8 ? e >> 1 : -1;
-      *reinterpret_cast<uint4*>(smem + L.ident + 16u * i) =
-          make_uint4(wd == 0 ? one : 0u, wd == 1 ? one : 0u, wd == 2 ? one : 0u, wd == 3 ? one : 0u);
+      const int wd = n < g.d && e >= 0 && e < 8 ? e >> 1 : -1;
+      uint4 v = make_uint4(wd == 0 ? one : 0u, wd == 1 ? one : 0u, wd == 2 ? one : 0u, wd == 3 ? one : 0u);
+      if (kc == 7 && n < g.d) {
+        const __half bh = __float2half_rn(cb[n]);
+        const __half bl = __float2half_rn(cb[n] - __half2float(bh));
+        v.w = (uint32_t)__half_as_ushort(bh) | ((uint32_t)__half_as_ushort(bl) << 16);
+      }
+      *reinterpret_cast<uint4*>(smem + L.ident + 16u * i) = v;
     }
+    // the state tiles' pad chunks (never loaded or written per tile): zero, ones at K = 62, 63
+    for (int i = threadIdx.x; i < 3 * NRX_TILE_M; i += blockDim.x)
+      *reinterpret_cast<uint4*>(smem + L.ta + (i / NRX_TILE_M) * (uint32_t)g.Cs * NRX_TILE_M * 2 +
+                                ((uint32_t)7 * NRX_TILE_M + i % NRX_TILE_M) * 16u) = make_uint4(0u, 0u, 0u, 0x3c003c00u);
     fence_proxy_async();  // generic-proxy stores -> tensor-core reads
   }
   if (TAIL) {
@@ -454,7 +467,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     // channels: constant over the iterations, written once by the state init;
     // the residual update skips them (and their zero rows in the tail's A tile)
     const int dch = (g.d + 7) / 8;
-    if (TAIL && MODE == EPI_RESIDUAL && part == PARTS - 1) {
+    if (TAIL && MODE == EPI_RESIDUAL && !RACC && part == PARTS - 1) {
       for (int b = 0; b < NTA; ++b)
         for (int cc = dch; cc < nd; ++cc)
           st_shared_u4(ta_s + b * ta_bytes + (uint32_t)(cc * NRX_TILE_M + r) * 16u, make_uint4(0u, 0u, 0u, 0u));
@@ -649,12 +662,12 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         if (MODE == EPI_RESIDUAL && cc >= dch) continue;   // constant positional / zero chunk
         float o8[8], bb[8];
         if (PREF && !MASTER) unpack_chunk(raw[c8], static_cast<const ET*>(nullptr), o8);
-        ld_shared_f8(sbias_s + 32u * cc, bb);
+        if (!RACC) ld_shared_f8(sbias_s + 32u * cc, bb);
         float* x = v + 8 * c8;
         const bool full = 8 * cc + 8 <= g.d;  // warp-uniform
         if (!MASTER && full) {  // fast path: pack, then ReLU / pad-row mask on the packed words
 #pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = PREF ? o8[e] + (x[e] + bb[e]) : x[e] + bb[e];
+          for (int e = 0; e < 8; ++e) x[e] = PREF ? o8[e] + (x[e] + bb[e]) : RACC ? x[e] : x[e] + bb[e];
           uint4 qx = pack_chunk(x, static_cast<const ET*>(nullptr));
           if (MODE == EPI_RELU) qx = relu_chunk(qx, static_cast<const ET*>(nullptr));
           qx = mask_chunk(qx, vmask);
@@ -664,7 +677,7 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
         }
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          float y = x[e] + bb[e];  // conv + bias first, as the reference adds them
+          float y = RACC ? x[e] : x[e] + bb[e];  // conv + bias first, as the reference adds them (RACC: in the accumulator)
           if (MODE == EPI_RELU) y = relu_f(y);
           if (PREF) y = (MASTER ? old[8 * c8 + e] : o8[e]) + y;
           x[e] = (valid && (full || 8 * cc + e < g.d)) ? y : 0.f;
