@@ -330,6 +330,18 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
     };
     mbar_wait(B_wbar, 0);
     tc_fence_after();
+    if constexpr (RACC) {
+      // the hidden bias into fc0 as well: W0's rows K = 62 / 63 (zero: pad channels of the state)
+      // take b0 split into fp16 hi / lo, against the state tiles' constant ones
+      for (int n = lane; n < thp; n += 32) {
+        const __half bh = __float2half_rn(stb0[n]);
+        const __half bl = __float2half_rn(stb0[n] - __half2float(bh));
+        *reinterpret_cast<uint32_t*>(smem + L.tw0 + ((uint32_t)(7 * thp + n) * 16u + 12u)) =
+            (uint32_t)__half_as_ushort(bh) | ((uint32_t)__half_as_ushort(bl) << 16);
+      }
+      fence_proxy_async();
+      __syncwarp();
+    }
     WorkIter w(g, g.NU, g.tiles, p.n_io, p.mod_order);
     int slab, tile, st = 0, it = 0;
     uint32_t ph = 0;
@@ -485,10 +497,11 @@ __global__ void __launch_bounds__(conv_threads(NP), 1)
       auto hchunk = [&](int c8) {
         float hv[8], bb[8];
         tmem_ld8(tmem_base + lane_off + col_h + b * thp + 8 * c8, hv);
-        ld_shared_f8(stb0_s + 32u * c8, bb);
+        if (!RACC) ld_shared_f8(stb0_s + 32u * c8, bb);  // RACC: b0 is in the accumulator
         tmem_wait_ld();
+        if (!RACC)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) hv[e] += bb[e];
+          for (int e = 0; e < 8; ++e) hv[e] += bb[e];
         st_shared_u4(thb + (uint32_t)(c8 * NRX_TILE_M + r) * 16u,
                      relu_chunk(pack_chunk(hv, static_cast<const ET*>(nullptr)), static_cast<const ET*>(nullptr)));
       };
